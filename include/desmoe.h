@@ -1,0 +1,192 @@
+/*
+ * desmoe.h — C ABI of the B200-native (sm_100a) Dynamic Expert Sharing MoE
+ * layer. Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Every entry point replaces one function of the reference library's C++
+ * operator API (dessim, /root/reference/proj/core/include/dessim/*.hpp); the
+ * reference interface is cited beside each declaration. The C++ facade
+ * (include/dessim_gpu.hpp) and the Python mirror (paper_2602_00879_b200/dessim.py)
+ * sit on top of this header.
+ *
+ * Conventions
+ *  - Pointers named *_dev are device pointers; everything is stream-ordered on
+ *    `stream` (a cudaStream_t, NULL = legacy default stream) and never
+ *    synchronises unless stated.
+ *  - Return value: DESMOE_OK (0), DESMOE_EINVAL (1, the reference would throw
+ *    std::invalid_argument; message identical to the reference's), DESMOE_ECUDA
+ *    (2), DESMOE_ENCCL (3). desmoe_last_error() returns the message of the last
+ *    failure on the calling thread.
+ *  - Data-dependent checks the reference performs on the logits (finiteness,
+ *    core.cpp:81-96) run on the device and latch a flag in the context; read it
+ *    with desmoe_check(), which synchronises `stream`.
+ *  - Expert-index outputs follow the reference's layout: per token the
+ *    selected experts in ascending order (core.hpp:63-68), padded with -1 up
+ *    to top_k; gates aligned, padded with 0.
+ *  - All routing arithmetic is fp64 in the reference's operation order
+ *    (SPEC.md:61); ties break to the lowest index everywhere.
+ */
+#ifndef DESMOE_H_
+#define DESMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DESMOE_OK 0
+#define DESMOE_EINVAL 1
+#define DESMOE_ECUDA 2
+#define DESMOE_ENCCL 3
+
+/* GateActivation (core.hpp:11) plus IDENTITY: the input already holds gate
+ * weights (topk_route(const GateMatrix&), gating.hpp:43). */
+#define DESMOE_SOFTMAX 0
+#define DESMOE_SIGMOID 1
+#define DESMOE_IDENTITY 2
+
+/* DesStrategy (des.hpp:16) plus VANILLA = plain top-K routing (gating.cpp:84) */
+#define DESMOE_VANILLA (-1)
+#define DESMOE_SEQ 0
+#define DESMOE_VOTE 1
+
+/* VoteSource (des.hpp:20) */
+#define DESMOE_VOTE_ACTIVATED 0
+#define DESMOE_VOTE_RAW_LOGITS 1
+
+/* expert FFN kinds: the reference's synthetic linear D x D map
+ * (ExpertBank, gating.hpp:48-63) and the north-star SwiGLU expert */
+#define DESMOE_FFN_SWIGLU 0
+#define DESMOE_FFN_LINEAR 1
+
+typedef struct desmoe_ctx desmoe_ctx;
+typedef struct desmoe_experts desmoe_experts;
+
+/* Routing configuration = PoolConfig (core.hpp:13-19) + DesParams (des.hpp:20-24). */
+typedef struct {
+  int experts;      /* M = experts_total */
+  int top_k;        /* K */
+  int activation;   /* DESMOE_SOFTMAX | DESMOE_SIGMOID | DESMOE_IDENTITY */
+  int strategy;     /* DESMOE_VANILLA | DESMOE_SEQ | DESMOE_VOTE */
+  int seq_k;        /* DesParams::seq_k, strategy == SEQ */
+  double vote_beta; /* DesParams::vote_beta, strategy == VOTE */
+  int vote_source;  /* DESMOE_VOTE_ACTIVATED | DESMOE_VOTE_RAW_LOGITS */
+} desmoe_route_cfg;
+
+/* Device outputs of a routing call. Any pointer may be NULL if not wanted,
+ * except route_* for the routing entry points. */
+typedef struct {
+  int* route_idx_dev;     /* [n x top_k] ascending experts, -1 padded        */
+  double* route_gate_dev; /* [n x top_k] renormalised gates, 0 padded        */
+  int* route_cnt_dev;     /* [n] = min(top_k, |coreset|)                    */
+  int* coreset_dev;       /* [experts] ascending members (Coreset::members)  */
+  int* coreset_size_dev;  /* [1]                                             */
+  double* votes_dev;      /* [experts] VoteVector::votes (VOTE only)         */
+  double* probs_dev;      /* [n x experts] activated gates (GateMatrix)      */
+} desmoe_route_out;
+
+/* ---- context --------------------------------------------------------------
+ * One context per (device, host thread); owns workspaces, tensor maps and
+ * CUDA graphs. Capacities bound every later call. */
+int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
+                  int max_top_k, int max_hidden);
+void desmoe_destroy(desmoe_ctx* ctx);
+const char* desmoe_last_error(void);
+/* Synchronises `stream` and reports (then clears) the device-side data
+ * checks latched since the last call ("non-finite logit"). */
+int desmoe_check(desmoe_ctx* ctx, void* stream);
+int desmoe_version(void);
+
+/* ---- validation (host only) ----------------------------------------------- */
+/* validate_config (core.cpp:11-28): same invariants, same messages. */
+int desmoe_validate_pool(int experts, int top_k, uint64_t bytes_per_expert, int hidden_dim);
+/* vote_budget (des.cpp:29-31): floor(beta * experts). */
+int desmoe_vote_budget(double beta, int experts);
+
+/* ---- gating / routing (logits in, device pointers) ------------------------
+ * logits_dev is [n x experts] row-major, fp64 (the reference's RouterBlock,
+ * core.hpp:32-44) or fp32 (the router GEMM's output / MOET trace values). */
+
+/* activate (gating.cpp:10-40) -> probs [n x experts] fp64 */
+int desmoe_activate(desmoe_ctx* ctx, const double* logits_dev, int n, int experts,
+                    int activation, double* probs_dev, void* stream);
+
+/* Full routing stage in one call:
+ *   VANILLA: topk_route(activate(block), K)                (gating.cpp:84-97)
+ *   SEQ/VOTE: des_run(block, cfg, params)                  (des.cpp:120-127)
+ * also exposes the stage-1 products: coreset (for VANILLA the union of the
+ * selections = unique_experts, gating.cpp:159-165) and votes. */
+int desmoe_route(desmoe_ctx* ctx, const double* logits_dev, int n, const desmoe_route_cfg* cfg,
+                 const desmoe_route_out* out, void* stream);
+int desmoe_route_f32(desmoe_ctx* ctx, const float* logits_dev, int n,
+                     const desmoe_route_cfg* cfg, const desmoe_route_out* out, void* stream);
+
+/* Stage 1 only: des_seq_coreset (des.cpp:33-45) / des_vote_coreset
+ * (des.cpp:65-95, also the contract of fused_vote_pipeline des.cpp:166-224).
+ * cfg->strategy selects which; out->coreset_dev / coreset_size_dev required. */
+int desmoe_coreset(desmoe_ctx* ctx, const double* logits_dev, int n,
+                   const desmoe_route_cfg* cfg, const desmoe_route_out* out, void* stream);
+
+/* Stage 2 only: constrained_route (des.cpp:97-118) over a caller-given
+ * coreset (ascending, unique, host array of n_members entries). */
+int desmoe_constrained_route(desmoe_ctx* ctx, const double* logits_dev, int n,
+                             const desmoe_route_cfg* cfg, const int* members_host,
+                             int n_members, const desmoe_route_out* out, void* stream);
+
+/* ---- permutation (K3) -------------------------------------------------------
+ * Per-expert counts (moe_latency's count route, analysis.cpp:16-30), ascending
+ * exclusive offsets, stable (ascending token) slot lists, the ascending list of
+ * active experts (unique_experts, gating.cpp:159-165) and its size U. */
+int desmoe_permute(desmoe_ctx* ctx, const int* route_idx_dev, const int* route_cnt_dev, int n,
+                   int top_k, int experts, int* expert_count_dev, int* expert_offset_dev,
+                   int* slot_of_dev, int* slot_token_dev, int* active_dev, int* n_active_dev,
+                   void* stream);
+
+/* ---- experts (K4) -----------------------------------------------------------
+ * Registers device-resident bf16 expert weights (no copy; caller keeps them
+ * alive). SWIGLU: w_gate/w_up [experts x ffn x hidden], w_down
+ * [experts x hidden x ffn]. LINEAR: w_gate = W [experts x hidden x hidden]
+ * (ExpertBank::expert_weights layout [out][in], gating.cpp:122-134),
+ * w_up = w_down = NULL, ffn = hidden. hidden % 128 == 0, ffn % 128 == 0. */
+int desmoe_experts_create(desmoe_ctx* ctx, int kind, int experts, int hidden, int ffn,
+                          const void* w_gate_dev, const void* w_up_dev, const void* w_down_dev,
+                          desmoe_experts** out);
+void desmoe_experts_destroy(desmoe_experts* ex);
+
+/* Expert FFN + combine for a routed block (moe_forward, gating.cpp:136-157):
+ * y[t] = sum over the token's experts in ascending order of gate * expert(x_t).
+ * x_dev [n x hidden] bf16, route_* as produced by desmoe_route, y_dev
+ * [n x hidden] fp32. Streams each active expert's weights once. */
+int desmoe_expert_ffn(desmoe_ctx* ctx, const desmoe_experts* ex, const void* x_dev, int n,
+                      int top_k, const int* route_idx_dev, const double* route_gate_dev,
+                      const int* route_cnt_dev, float* y_dev, void* stream);
+
+/* ---- router GEMM (K1) -------------------------------------------------------
+ * logits[n x experts] fp32 = x[n x hidden] (bf16) . w_router[experts x hidden]^T
+ * (bf16). The reference takes logits as input; this is the producer the
+ * paper's layer puts in front of it. */
+int desmoe_router_logits(desmoe_ctx* ctx, const void* x_dev, const void* w_router_dev, int n,
+                         int experts, int hidden, float* logits_dev, void* stream);
+
+/* ---- whole layer --------------------------------------------------------------
+ * router -> activation/top-K -> coreset -> constrained route -> permute ->
+ * expert FFN + combine. stats_dev (optional, int[4]): {U unique experts,
+ * coreset size, total selections, 0}. */
+int desmoe_layer_forward(desmoe_ctx* ctx, const desmoe_experts* ex, const void* w_router_dev,
+                         const void* x_dev, int n, const desmoe_route_cfg* cfg, float* y_dev,
+                         int* stats_dev, void* stream);
+
+/* Same with HOST buffers: copies x (bf16) in, runs the layer, copies y
+ * (fp32) and stats back; synchronises. The end-to-end entry a C/C++ caller
+ * without device memory uses. */
+int desmoe_layer_forward_host(desmoe_ctx* ctx, const desmoe_experts* ex,
+                              const void* w_router_dev, const void* x_host, int n,
+                              const desmoe_route_cfg* cfg, float* y_host, int* stats_host,
+                              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DESMOE_H_ */

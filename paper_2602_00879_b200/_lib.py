@@ -1,0 +1,100 @@
+"""ctypes binding of the C ABI (include/desmoe.h) -> libdesmoe.so.
+
+The library is built in-tree (``make -C paper_2602_00879_b200``, or
+``__graft_entry__.build()``). There is deliberately no fallback: if the shared
+object is missing or fails to load, every public entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdesmoe.so")
+
+OK, EINVAL, ECUDA, ENCCL = 0, 1, 2, 3
+SOFTMAX, SIGMOID, IDENTITY = 0, 1, 2
+VANILLA, SEQ, VOTE = -1, 0, 1
+VOTE_ACTIVATED, VOTE_RAW_LOGITS = 0, 1
+FFN_SWIGLU, FFN_LINEAR = 0, 1
+
+
+class RouteCfg(C.Structure):
+    _fields_ = [("experts", C.c_int), ("top_k", C.c_int), ("activation", C.c_int),
+                ("strategy", C.c_int), ("seq_k", C.c_int), ("vote_beta", C.c_double),
+                ("vote_source", C.c_int)]
+
+
+class RouteOut(C.Structure):
+    _fields_ = [("route_idx_dev", C.c_void_p), ("route_gate_dev", C.c_void_p),
+                ("route_cnt_dev", C.c_void_p), ("coreset_dev", C.c_void_p),
+                ("coreset_size_dev", C.c_void_p), ("votes_dev", C.c_void_p),
+                ("probs_dev", C.c_void_p)]
+
+
+# name -> (restype, argtypes)
+_P, _I, _D = C.c_void_p, C.c_int, C.c_double
+_SIGS = {
+    "desmoe_create": (_I, [C.POINTER(C.c_void_p), _I, _I, _I, _I, _I]),
+    "desmoe_destroy": (None, [_P]),
+    "desmoe_last_error": (C.c_char_p, []),
+    "desmoe_check": (_I, [_P, _P]),
+    "desmoe_version": (_I, []),
+    "desmoe_validate_pool": (_I, [_I, _I, C.c_uint64, _I]),
+    "desmoe_vote_budget": (_I, [_D, _I]),
+    "desmoe_activate": (_I, [_P, _P, _I, _I, _I, _P, _P]),
+    "desmoe_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
+    "desmoe_route_f32": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
+    "desmoe_coreset": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
+    "desmoe_constrained_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(C.c_int), _I,
+                                      C.POINTER(RouteOut), _P]),
+    "desmoe_permute": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "desmoe_experts_create": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, C.POINTER(C.c_void_p)]),
+    "desmoe_experts_destroy": (None, [_P]),
+    "desmoe_expert_ffn": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
+    "desmoe_router_logits": (_I, [_P, _P, _P, _I, _I, _I, _P, _P]),
+    "desmoe_layer_forward": (_I, [_P, _P, _P, _P, _I, C.POINTER(RouteCfg), _P, _P, _P]),
+    "desmoe_layer_forward_host": (_I, [_P, _P, _P, _P, _I, C.POINTER(RouteCfg), _P, _P, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class DesmoeError(RuntimeError):
+    pass
+
+
+def lib():
+    """Loads libdesmoe.so once; raises (never falls back) when it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DesmoeError(
+                    f"{LIB_PATH} is missing: build it with `make -C {HERE}` "
+                    "(or __graft_entry__.build()); there is no CPU fallback")
+            handle = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def check(rc: int):
+    """Maps a C-ABI status to the reference's exception types."""
+    if rc == OK:
+        return
+    msg = lib().desmoe_last_error().decode()
+    if rc == EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    raise DesmoeError(msg)

@@ -1,0 +1,830 @@
+// C-ABI layer (include/desmoe.h): host-side validation with the reference's
+// exact error messages, context-owned workspaces, TMA descriptor creation and
+// the launch sequences of the routing stage, permutation, expert FFN and the
+// whole layer. No computation happens on the host: every entry point only
+// validates scalars and enqueues sm_100a kernels on the caller's stream.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/desmoe.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace desmoe;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define DESMOE_CUDA(expr)                                                               \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(DESMOE_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+#define DESMOE_LAUNCHED()                                                               \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(DESMOE_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [rows x cols] row-major, box [box_rows x 64], SWIZZLE_128B.
+int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DESMOE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DESMOE_ECUDA, "cuTensorMapEncodeTiled failed (" +
+                                                       std::to_string(static_cast<int>(r)) + ")");
+  return DESMOE_OK;
+}
+
+int make_box_maps(BoxMaps* maps, const void* base, uint64_t rows, uint64_t cols) {
+  for (int i = 0; i < kMaxBoxes; ++i) {
+    int rc = make_map(&maps->map[i], base, rows, cols, 16u << i);
+    if (rc) return rc;
+  }
+  return DESMOE_OK;
+}
+
+int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+constexpr int kSmemBudget = 220 * 1024;
+
+}  // namespace
+
+struct desmoe_ctx {
+  int device = 0, max_n = 0, max_m = 0, max_k = 0, max_d = 0, num_sms = 148;
+  // routing workspace
+  double* probs = nullptr;
+  int* topk_idx = nullptr;
+  int* members = nullptr;
+  int* n_members = nullptr;
+  uint8_t* member_flag = nullptr;
+  double* votes = nullptr;
+  int* route_idx = nullptr;
+  double* route_gate = nullptr;
+  float* route_gate32 = nullptr;
+  int* route_cnt = nullptr;
+  int* err = nullptr;
+  // permutation workspace
+  int* expert_count = nullptr;
+  int* expert_offset = nullptr;
+  int* slot_of = nullptr;
+  int* slot_token = nullptr;
+  float* slot_gate = nullptr;
+  int* active = nullptr;
+  int* n_active = nullptr;
+  int* total = nullptr;
+  // router
+  float* logits32 = nullptr;
+  float* partials = nullptr;
+  int max_splits = 32;
+  // staging for the host entry point
+  void* x_dev = nullptr;
+  float* y_dev = nullptr;
+  int* stats_dev = nullptr;
+  // cached router descriptors
+  const void* x_map_ptr = nullptr;
+  int x_map_n = -1, x_map_d = -1;
+  BoxMaps x_maps{};
+  const void* wr_map_ptr = nullptr;
+  int wr_map_m = -1, wr_map_d = -1;
+  CUtensorMap wr_map{};
+};
+
+struct desmoe_experts {
+  desmoe_ctx* ctx = nullptr;
+  int kind = 0, m = 0, d = 0, f = 0;
+  CUtensorMap wg{}, wu{}, wd{};
+  BoxMaps xp_maps{}, h_maps{};
+  __nv_bfloat16* x_perm = nullptr;  // [max_n*max_k x d]
+  __nv_bfloat16* h_perm = nullptr;  // [max_n*max_k x f]
+  float* y_slot = nullptr;          // [max_n*max_k x d]
+};
+
+extern "C" {
+
+const char* desmoe_last_error(void) { return g_err.c_str(); }
+
+int desmoe_version(void) { return 1; }
+
+int desmoe_validate_pool(int experts, int top_k, uint64_t bytes_per_expert, int hidden_dim) {
+  // validate_config, core.cpp:11-28 (same order, same messages)
+  if (experts < 1) return fail(DESMOE_EINVAL, "experts_total < 1");
+  if (top_k < 1) return fail(DESMOE_EINVAL, "top_k < 1");
+  if (top_k > experts) return fail(DESMOE_EINVAL, "top_k > experts_total");
+  if (bytes_per_expert == 0) return fail(DESMOE_EINVAL, "bytes_per_expert == 0");
+  if (hidden_dim < 1) return fail(DESMOE_EINVAL, "hidden_dim < 1");
+  return DESMOE_OK;
+}
+
+int desmoe_vote_budget(double beta, int experts) {
+  return static_cast<int>(std::floor(beta * experts));
+}
+
+int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts, int max_top_k,
+                  int max_hidden) {
+  if (!out) return fail(DESMOE_EINVAL, "null output handle");
+  if (max_tokens < 1 || max_tokens > 1024)
+    return fail(DESMOE_EINVAL, "max_tokens outside [1, 1024]");
+  if (max_experts < 1 || max_experts > 1024)
+    return fail(DESMOE_EINVAL, "max_experts outside [1, 1024]");
+  if (max_top_k < 1 || max_top_k > 32) return fail(DESMOE_EINVAL, "max_top_k outside [1, 32]");
+  if (max_hidden < 1) return fail(DESMOE_EINVAL, "max_hidden < 1");
+  DESMOE_CUDA(cudaSetDevice(device));
+  auto* c = new desmoe_ctx();
+  c->device = device;
+  c->max_n = max_tokens;
+  c->max_m = max_experts;
+  c->max_k = max_top_k;
+  c->max_d = max_hidden;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t nm = static_cast<size_t>(max_tokens) * max_experts;
+  const size_t nk = static_cast<size_t>(max_tokens) * max_top_k;
+  auto alloc = [&](auto** p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(**p) * std::max<size_t>(count, 1));
+  };
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) {
+    if (e == cudaSuccess) e = r;
+  };
+  A(alloc(&c->probs, nm));
+  A(alloc(&c->topk_idx, nk));
+  A(alloc(&c->members, max_experts));
+  A(alloc(&c->n_members, 1));
+  A(alloc(&c->member_flag, max_experts));
+  A(alloc(&c->votes, max_experts));
+  A(alloc(&c->route_idx, nk));
+  A(alloc(&c->route_gate, nk));
+  A(alloc(&c->route_gate32, nk));
+  A(alloc(&c->route_cnt, max_tokens));
+  A(alloc(&c->err, 1));
+  A(alloc(&c->expert_count, max_experts));
+  A(alloc(&c->expert_offset, max_experts));
+  A(alloc(&c->slot_of, nk));
+  A(alloc(&c->slot_token, nk));
+  A(alloc(&c->slot_gate, nk));
+  A(alloc(&c->active, max_experts));
+  A(alloc(&c->n_active, 1));
+  A(alloc(&c->total, 1));
+  A(alloc(&c->logits32, nm));
+  A(alloc(&c->partials, nm * c->max_splits));
+  A(alloc(reinterpret_cast<__nv_bfloat16**>(&c->x_dev), static_cast<size_t>(max_tokens) * max_hidden));
+  A(alloc(&c->y_dev, static_cast<size_t>(max_tokens) * max_hidden));
+  A(alloc(&c->stats_dev, 4));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    desmoe_destroy(c);
+    return fail(DESMOE_ECUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return DESMOE_OK;
+}
+
+void desmoe_destroy(desmoe_ctx* c) {
+  if (!c) return;
+  void* ptrs[] = {c->probs, c->topk_idx, c->members, c->n_members, c->member_flag, c->votes,
+                  c->route_idx, c->route_gate, c->route_gate32, c->route_cnt, c->err,
+                  c->expert_count, c->expert_offset, c->slot_of, c->slot_token, c->slot_gate,
+                  c->active, c->n_active, c->total, c->logits32, c->partials, c->x_dev,
+                  c->y_dev, c->stats_dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+}
+
+int desmoe_check(desmoe_ctx* c, void* stream) {
+  if (!c) return fail(DESMOE_EINVAL, "null context");
+  DESMOE_CUDA(cudaStreamSynchronize(S(stream)));
+  int flag = 0;
+  DESMOE_CUDA(cudaMemcpy(&flag, c->err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    DESMOE_CUDA(cudaMemset(c->err, 0, sizeof(int)));
+    return fail(DESMOE_EINVAL, "non-finite logit");
+  }
+  return DESMOE_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// routing launch helpers
+// ---------------------------------------------------------------------------
+namespace {
+
+int check_block(desmoe_ctx* c, int n, int m) {
+  if (!c) return fail(DESMOE_EINVAL, "null context");
+  if (n < 1) return fail(DESMOE_EINVAL, "block_size < 1");
+  if (n > c->max_n) return fail(DESMOE_EINVAL, "block_size exceeds context capacity");
+  if (m < 1 || m > c->max_m) return fail(DESMOE_EINVAL, "experts outside context capacity");
+  return DESMOE_OK;
+}
+
+template <typename T>
+int launch_gate_topk(desmoe_ctx* c, const T* logits, const float* partials, int splits, int n,
+                     int m, int k, int act, int mode, double* probs, int kmax, int* route_idx,
+                     double* route_gate, int* route_cnt, cudaStream_t st) {
+  GateTopkArgs<T> a{};
+  a.logits = logits;
+  a.partials = partials;
+  a.logits_out = partials ? c->logits32 : nullptr;
+  a.splits = splits;
+  a.m_pad = m;
+  a.n = n;
+  a.m = m;
+  a.k = k;
+  a.kmax = kmax;
+  a.act = act;
+  a.mode = mode;
+  a.probs = probs;
+  a.topk_idx = c->topk_idx;
+  a.route_idx = route_idx;
+  a.route_gate = route_gate;
+  a.route_gate32 = (route_gate == c->route_gate) ? c->route_gate32 : nullptr;
+  a.route_cnt = route_cnt;
+  a.err = c->err;
+  const int warps = 8;
+  const size_t smem = static_cast<size_t>(warps) * m * sizeof(double) + warps * 32 * sizeof(int);
+  cudaError_t e = launch_gate_topk_kernel<T>(a, (n + warps - 1) / warps, warps * 32, smem, st);
+  if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("gate_topk: ") + cudaGetErrorString(e));
+  return DESMOE_OK;
+}
+
+template <typename T>
+int launch_coreset(desmoe_ctx* c, const T* logits, int n, const desmoe_route_cfg* cfg,
+                   double* votes, cudaStream_t st) {
+  CoresetArgs a{};
+  a.n = n;
+  a.m = cfg->experts;
+  a.k = cfg->top_k;
+  a.strategy = cfg->strategy;
+  a.seq_k = cfg->seq_k;
+  a.m_core = desmoe_vote_budget(cfg->vote_beta, cfg->experts);
+  a.raw = cfg->vote_source == DESMOE_VOTE_RAW_LOGITS;
+  a.topk_idx = c->topk_idx;
+  a.probs = c->probs;
+  if constexpr (sizeof(T) == 8)
+    a.logits64 = reinterpret_cast<const double*>(logits);
+  else
+    a.logits32 = reinterpret_cast<const float*>(logits);
+  a.votes = votes;
+  a.members = c->members;
+  a.n_members = c->n_members;
+  a.member_flag = c->member_flag;
+  const int m = cfg->experts;
+  const int words = (m + 31) / 32;
+  const size_t smem = static_cast<size_t>(n) * words * 4 + 8 + static_cast<size_t>(m) * 8 +
+                      static_cast<size_t>(m) * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(coreset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  const int threads = std::max(128, round_up(m, 32));
+  coreset_kernel<<<1, threads, smem, st>>>(a);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+int launch_reroute(desmoe_ctx* c, int n, int m, int k, bool fast_path, int* route_idx,
+                   double* route_gate, int* route_cnt, cudaStream_t st) {
+  RerouteArgs a{};
+  a.n = n;
+  a.m = m;
+  a.k = k;
+  a.probs = c->probs;
+  a.topk_idx = fast_path ? c->topk_idx : nullptr;
+  a.member_flag = c->member_flag;
+  a.n_members = c->n_members;
+  a.route_idx = route_idx;
+  a.route_gate = route_gate;
+  a.route_gate32 = (route_gate == c->route_gate) ? c->route_gate32 : nullptr;
+  a.route_cnt = route_cnt;
+  const int warps = 8;
+  constrained_route_kernel<<<(n + warps - 1) / warps, warps * 32, warps * 32 * sizeof(int), st>>>(a);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+// Validation of des_run's parameters (des.cpp:10-27, validate_config first).
+int check_des_params(const desmoe_route_cfg* cfg) {
+  int rc = desmoe_validate_pool(cfg->experts, cfg->top_k, 1, 1);
+  if (rc) return rc;
+  if (cfg->strategy == DESMOE_SEQ) {
+    if (cfg->seq_k < 1) return fail(DESMOE_EINVAL, "seq_k < 1");
+    if (cfg->seq_k > cfg->top_k) return fail(DESMOE_EINVAL, "seq_k > top_k");
+  } else if (cfg->strategy == DESMOE_VOTE) {
+    if (!(cfg->vote_beta > 0.0) || cfg->vote_beta > 1.0)
+      return fail(DESMOE_EINVAL, "vote_beta outside (0, 1]");
+    if (desmoe_vote_budget(cfg->vote_beta, cfg->experts) < 1)
+      return fail(DESMOE_EINVAL, "vote budget floor(beta*M) < 1");
+  } else {
+    return fail(DESMOE_EINVAL, "unknown strategy");
+  }
+  return DESMOE_OK;
+}
+
+// Full routing from logits of type T (fp64 RouterBlock or fp32), or from the
+// router's split-K partials (partials != nullptr).
+template <typename T>
+int route_impl(desmoe_ctx* c, const T* logits, const float* partials, int splits, int n,
+               const desmoe_route_cfg* cfg, const desmoe_route_out* out, cudaStream_t st) {
+  const int m = cfg->experts, k = cfg->top_k;
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  if (k > c->max_k) return fail(DESMOE_EINVAL, "top_k exceeds context capacity");
+  if (cfg->activation < 0 || cfg->activation > 2)
+    return fail(DESMOE_EINVAL, "unknown gate activation");
+  int* ridx = out && out->route_idx_dev ? out->route_idx_dev : c->route_idx;
+  double* rgate = out && out->route_gate_dev ? out->route_gate_dev : c->route_gate;
+  int* rcnt = out && out->route_cnt_dev ? out->route_cnt_dev : c->route_cnt;
+  if (cfg->strategy == DESMOE_VANILLA) {
+    // topk_route(activate(block), K): gating.cpp:84-87
+    if (k < 1 || k > m) return fail(DESMOE_EINVAL, "top_k out of range");
+    rc = launch_gate_topk<T>(c, logits, partials, splits, n, m, k, cfg->activation, 0,
+                             out && out->probs_dev ? out->probs_dev : c->probs, k, ridx, rgate,
+                             rcnt, st);
+    if (rc) return rc;
+    if (out && (out->coreset_dev || out->coreset_size_dev)) {
+      // unique_experts(assign) via the permutation's active list
+      PermuteArgs p{};
+      p.n = n;
+      p.m = m;
+      p.k = k;
+      p.route_idx = ridx;
+      p.route_cnt = rcnt;
+      p.active = out->coreset_dev ? out->coreset_dev : c->active;
+      p.n_active = out->coreset_size_dev ? out->coreset_size_dev : c->n_active;
+      p.total = c->total;
+      const int tw = (n + 31) / 32;
+      const size_t smem = static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+      permute_kernel<<<1, std::max(128, round_up(m, 32)), smem, st>>>(p);
+      DESMOE_LAUNCHED();
+    }
+    return DESMOE_OK;
+  }
+  rc = check_des_params(cfg);
+  if (rc) return rc;
+  rc = launch_gate_topk<T>(c, logits, partials, splits, n, m, k, cfg->activation, 1, c->probs,
+                           k, nullptr, nullptr, nullptr, st);
+  if (rc) return rc;
+  if (out && out->probs_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(out->probs_dev, c->probs, sizeof(double) * n * m,
+                                cudaMemcpyDeviceToDevice, st));
+  const T* raw = partials ? reinterpret_cast<const T*>(c->logits32) : logits;
+  rc = launch_coreset<T>(c, raw, n, cfg, out ? out->votes_dev : nullptr, st);
+  if (rc) return rc;
+  rc = launch_reroute(c, n, m, k, true, ridx, rgate, rcnt, st);
+  if (rc) return rc;
+  if (out && out->coreset_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(out->coreset_dev, c->members, sizeof(int) * m,
+                                cudaMemcpyDeviceToDevice, st));
+  if (out && out->coreset_size_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(out->coreset_size_dev, c->n_members, sizeof(int),
+                                cudaMemcpyDeviceToDevice, st));
+  return DESMOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int desmoe_activate(desmoe_ctx* c, const double* logits, int n, int m, int act, double* probs,
+                    void* stream) {
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  // selection of 1 keeps the kernel's top-K path trivially valid
+  return launch_gate_topk<double>(c, logits, nullptr, 0, n, m, 1, act, 1, probs, 1, nullptr,
+                                  nullptr, nullptr, S(stream));
+}
+
+int desmoe_route(desmoe_ctx* c, const double* logits, int n, const desmoe_route_cfg* cfg,
+                 const desmoe_route_out* out, void* stream) {
+  if (!cfg) return fail(DESMOE_EINVAL, "null config");
+  return route_impl<double>(c, logits, nullptr, 0, n, cfg, out, S(stream));
+}
+
+int desmoe_route_f32(desmoe_ctx* c, const float* logits, int n, const desmoe_route_cfg* cfg,
+                     const desmoe_route_out* out, void* stream) {
+  if (!cfg) return fail(DESMOE_EINVAL, "null config");
+  return route_impl<float>(c, logits, nullptr, 0, n, cfg, out, S(stream));
+}
+
+int desmoe_coreset(desmoe_ctx* c, const double* logits, int n, const desmoe_route_cfg* cfg,
+                   const desmoe_route_out* out, void* stream) {
+  if (!cfg) return fail(DESMOE_EINVAL, "null config");
+  const int m = cfg->experts, k = cfg->top_k;
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  if (k < 1 || k > m || k > c->max_k) return fail(DESMOE_EINVAL, "top_k out of range");
+  if (cfg->strategy == DESMOE_SEQ) {
+    // des_seq_coreset (des.cpp:34-36)
+    if (cfg->seq_k < 1 || cfg->seq_k > k)
+      return fail(DESMOE_EINVAL, "local_k outside [1, top_k]");
+  } else if (cfg->strategy == DESMOE_VOTE) {
+    // checked_budget (des.cpp:49-61)
+    if (!(cfg->vote_beta > 0.0)) return fail(DESMOE_EINVAL, "beta <= 0");
+    int mc = desmoe_vote_budget(cfg->vote_beta, m);
+    if (mc < 1) return fail(DESMOE_EINVAL, "vote budget floor(beta*M) < 1");
+    if (mc > m) return fail(DESMOE_EINVAL, "beta > 1");
+  } else {
+    return fail(DESMOE_EINVAL, "unknown strategy");
+  }
+  cudaStream_t st = S(stream);
+  rc = launch_gate_topk<double>(c, logits, nullptr, 0, n, m, k, cfg->activation, 1, c->probs, k,
+                                nullptr, nullptr, nullptr, st);
+  if (rc) return rc;
+  rc = launch_coreset<double>(c, logits, n, cfg, out ? out->votes_dev : nullptr, st);
+  if (rc) return rc;
+  if (out && out->coreset_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(out->coreset_dev, c->members, sizeof(int) * m,
+                                cudaMemcpyDeviceToDevice, st));
+  if (out && out->coreset_size_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(out->coreset_size_dev, c->n_members, sizeof(int),
+                                cudaMemcpyDeviceToDevice, st));
+  return DESMOE_OK;
+}
+
+int desmoe_constrained_route(desmoe_ctx* c, const double* logits, int n,
+                             const desmoe_route_cfg* cfg, const int* members_host, int n_members,
+                             const desmoe_route_out* out, void* stream) {
+  if (!cfg) return fail(DESMOE_EINVAL, "null config");
+  const int m = cfg->experts, k = cfg->top_k;
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  if (k < 1 || k > m || k > c->max_k) return fail(DESMOE_EINVAL, "top_k out of range");
+  // des.cpp:100-105
+  if (n_members < 1 || !members_host) return fail(DESMOE_EINVAL, "empty coreset");
+  if (members_host[n_members - 1] >= m) return fail(DESMOE_EINVAL, "coreset member out of range");
+  for (int i = 0; i < n_members; ++i)
+    if (members_host[i] < 0 || (i > 0 && members_host[i] <= members_host[i - 1]))
+      return fail(DESMOE_EINVAL, "coreset members must be ascending, unique, non-negative");
+  cudaStream_t st = S(stream);
+  DESMOE_CUDA(cudaMemcpyAsync(c->members, members_host, sizeof(int) * n_members,
+                              cudaMemcpyHostToDevice, st));
+  set_members_kernel<<<1, 256, 0, st>>>(c->members, n_members, m, c->member_flag, c->n_members);
+  DESMOE_LAUNCHED();
+  rc = launch_gate_topk<double>(c, logits, nullptr, 0, n, m, 1, cfg->activation, 1, c->probs, 1,
+                                nullptr, nullptr, nullptr, st);
+  if (rc) return rc;
+  int* ridx = out && out->route_idx_dev ? out->route_idx_dev : c->route_idx;
+  double* rgate = out && out->route_gate_dev ? out->route_gate_dev : c->route_gate;
+  int* rcnt = out && out->route_cnt_dev ? out->route_cnt_dev : c->route_cnt;
+  return launch_reroute(c, n, m, k, false, ridx, rgate, rcnt, st);
+}
+
+int desmoe_permute(desmoe_ctx* c, const int* route_idx, const int* route_cnt, int n, int k,
+                   int m, int* expert_count, int* expert_offset, int* slot_of, int* slot_token,
+                   int* active, int* n_active, void* stream) {
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  if (k < 1 || k > c->max_k) return fail(DESMOE_EINVAL, "top_k out of range");
+  PermuteArgs p{};
+  p.n = n;
+  p.m = m;
+  p.k = k;
+  p.route_idx = route_idx;
+  p.route_cnt = route_cnt;
+  p.expert_count = expert_count;
+  p.expert_offset = expert_offset;
+  p.slot_of = slot_of;
+  p.slot_token = slot_token;
+  p.active = active ? active : c->active;
+  p.n_active = n_active ? n_active : c->n_active;
+  p.total = c->total;
+  const int tw = (n + 31) / 32;
+  const size_t smem = static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  permute_kernel<<<1, std::max(128, round_up(m, 32)), smem, S(stream)>>>(p);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const void* wg,
+                          const void* wu, const void* wd, desmoe_experts** out) {
+  if (!c || !out) return fail(DESMOE_EINVAL, "null argument");
+  if (kind != DESMOE_FFN_SWIGLU && kind != DESMOE_FFN_LINEAR)
+    return fail(DESMOE_EINVAL, "unknown expert kind");
+  if (m < 1 || m > c->max_m) return fail(DESMOE_EINVAL, "experts outside context capacity");
+  if (kind == DESMOE_FFN_LINEAR) f = d;
+  if (d < 128 || d % 128 || d > c->max_d) return fail(DESMOE_EINVAL, "hidden must be a multiple of 128 within capacity");
+  if (f < 128 || f % 128) return fail(DESMOE_EINVAL, "ffn must be a multiple of 128");
+  if (!wg || (kind == DESMOE_FFN_SWIGLU && (!wu || !wd)))
+    return fail(DESMOE_EINVAL, "missing expert weights");
+  auto* ex = new desmoe_experts();
+  ex->ctx = c;
+  ex->kind = kind;
+  ex->m = m;
+  ex->d = d;
+  ex->f = f;
+  const size_t slots = static_cast<size_t>(c->max_n) * c->max_k;
+  cudaError_t e = cudaMalloc(&ex->x_perm, slots * d * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&ex->h_perm, slots * f * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&ex->y_slot, slots * d * 4);
+  if (e != cudaSuccess) {
+    desmoe_experts_destroy(ex);
+    return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
+  }
+  int rc = DESMOE_OK;
+  if (kind == DESMOE_FFN_SWIGLU) {
+    rc = make_map(&ex->wg, wg, static_cast<uint64_t>(m) * f, d, kBM);
+    if (!rc) rc = make_map(&ex->wu, wu, static_cast<uint64_t>(m) * f, d, kBM);
+    if (!rc) rc = make_map(&ex->wd, wd, static_cast<uint64_t>(m) * d, f, kBM);
+    if (!rc) rc = make_box_maps(&ex->h_maps, ex->h_perm, slots, f);
+  } else {
+    rc = make_map(&ex->wd, wg, static_cast<uint64_t>(m) * d, d, kBM);
+    ex->wg = ex->wd;
+    ex->wu = ex->wd;
+  }
+  if (!rc) rc = make_box_maps(&ex->xp_maps, ex->x_perm, slots, d);
+  if (rc) {
+    desmoe_experts_destroy(ex);
+    return rc;
+  }
+  *out = ex;
+  return DESMOE_OK;
+}
+
+void desmoe_experts_destroy(desmoe_experts* ex) {
+  if (!ex) return;
+  if (ex->x_perm) cudaFree(ex->x_perm);
+  if (ex->h_perm) cudaFree(ex->h_perm);
+  if (ex->y_slot) cudaFree(ex->y_slot);
+  delete ex;
+}
+
+}  // extern "C"
+
+namespace {
+
+int b_rows_for(int n) {
+  int b = 16;
+  while (b < n && b < 256) b <<= 1;
+  return b;
+}
+
+int launch_tile(int mode, const CUtensorMap& wa, const CUtensorMap& wb, const BoxMaps& acts,
+                TileArgs a, int grid, cudaStream_t st) {
+  const int stage_bytes = kATile * (mode == kGateUp ? 2 : 1) + a.b_rows * 128;
+  const int per_unit_kb = mode == kRouter ? (a.kb_total + a.splits - 1) / a.splits : a.kb_total;
+  int stages = (kSmemBudget - 1024 - 256) / stage_bytes;
+  stages = std::max(1, std::min(stages, std::max(per_unit_kb, 1)));
+  a.stages = stages;
+  a.mode = mode;
+  const size_t smem = static_cast<size_t>(stages) * stage_bytes + 1024 + 256;
+  cudaFuncSetAttribute(tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  tile_gemm_kernel<<<grid, 256, smem, st>>>(wa, wb, acts, a);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
+             const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
+             cudaStream_t st) {
+  const int m = ex->m, d = ex->d, f = ex->f;
+  if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
+  // K3: permutation
+  PermuteArgs p{};
+  p.n = n;
+  p.m = m;
+  p.k = k;
+  p.route_idx = route_idx;
+  p.route_cnt = route_cnt;
+  p.route_gate = route_gate;
+  p.expert_count = c->expert_count;
+  p.expert_offset = c->expert_offset;
+  p.slot_of = c->slot_of;
+  p.slot_token = c->slot_token;
+  p.slot_gate = c->slot_gate;
+  p.active = c->active;
+  p.n_active = c->n_active;
+  p.total = c->total;
+  const int tw = (n + 31) / 32;
+  const size_t psmem = static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;
+  if (psmem > 48 * 1024)
+    cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(psmem));
+  permute_kernel<<<1, std::max(128, round_up(m, 32)), psmem, st>>>(p);
+  DESMOE_LAUNCHED();
+  // gather token rows into expert-grouped order
+  gather_rows_kernel<<<n * k, std::min(256, d / 8), 0, st>>>(
+      reinterpret_cast<const uint4*>(x), c->slot_token, c->total,
+      reinterpret_cast<uint4*>(ex->x_perm), d / 8);
+  DESMOE_LAUNCHED();
+
+  TileArgs a{};
+  a.n_tok = n;
+  a.splits = 1;
+  a.n_active = c->n_active;
+  a.active = c->active;
+  a.expert_offset = c->expert_offset;
+  a.expert_count = c->expert_count;
+  a.b_rows = b_rows_for(n);
+  a.slot_gate = c->slot_gate;
+  int rc;
+  if (ex->kind == DESMOE_FFN_SWIGLU) {
+    TileArgs g = a;
+    g.tiles_per_unit_expert = f / kBM;
+    g.kb_total = d / kBK;
+    g.weight_rows_per_expert = f;
+    g.ld_out = f;
+    g.h_out = ex->h_perm;
+    rc = launch_tile(kGateUp, ex->wg, ex->wu, ex->xp_maps, g, m * (f / kBM), st);
+    if (rc) return rc;
+    TileArgs dn = a;
+    dn.tiles_per_unit_expert = d / kBM;
+    dn.kb_total = f / kBK;
+    dn.weight_rows_per_expert = d;
+    dn.ld_out = d;
+    dn.y_out = ex->y_slot;
+    rc = launch_tile(kDown, ex->wd, ex->wd, ex->h_maps, dn, m * (d / kBM), st);
+    if (rc) return rc;
+  } else {
+    TileArgs dn = a;
+    dn.tiles_per_unit_expert = d / kBM;
+    dn.kb_total = d / kBK;
+    dn.weight_rows_per_expert = d;
+    dn.ld_out = d;
+    dn.y_out = ex->y_slot;
+    rc = launch_tile(kDown, ex->wd, ex->wd, ex->xp_maps, dn, m * (d / kBM), st);
+    if (rc) return rc;
+  }
+  combine_kernel<<<n, 256, 0, st>>>(ex->y_slot, c->slot_of, route_cnt, n, k, d, y);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+int router_impl(desmoe_ctx* c, const void* x, const void* w_r, int n, int m, int d,
+                int* splits_out, cudaStream_t st) {
+  if (d % kBK) return fail(DESMOE_EINVAL, "hidden must be a multiple of 64");
+  if (n > 256) return fail(DESMOE_EINVAL, "router supports up to 256 tokens per block");
+  if (x != c->x_map_ptr || n != c->x_map_n || d != c->x_map_d) {
+    int rc = make_box_maps(&c->x_maps, x, n, d);
+    if (rc) return rc;
+    c->x_map_ptr = x;
+    c->x_map_n = n;
+    c->x_map_d = d;
+  }
+  if (w_r != c->wr_map_ptr || m != c->wr_map_m || d != c->wr_map_d) {
+    int rc = make_map(&c->wr_map, w_r, m, d, kBM);
+    if (rc) return rc;
+    c->wr_map_ptr = w_r;
+    c->wr_map_m = m;
+    c->wr_map_d = d;
+  }
+  const int kb = d / kBK;
+  const int et = (m + kBM - 1) / kBM;
+  int splits = std::max(1, std::min(kb, std::min(c->max_splits, c->num_sms / et)));
+  // equalise K blocks per split
+  const int per = (kb + splits - 1) / splits;
+  splits = (kb + per - 1) / per;
+  TileArgs a{};
+  a.n_tok = n;
+  a.kb_total = kb;
+  a.splits = splits;
+  a.n_units_static = et * splits;
+  a.b_rows = b_rows_for(n);
+  a.m_pad = m;
+  a.y_out = c->partials;
+  int rc = launch_tile(kRouter, c->wr_map, c->wr_map, c->x_maps, a, et * splits, st);
+  if (rc) return rc;
+  *splits_out = splits;
+  return DESMOE_OK;
+}
+
+__global__ void stats_kernel(const int* n_active, const int* n_members, const int* total,
+                             int* stats) {
+  stats[0] = *n_active;
+  stats[1] = n_members ? *n_members : *n_active;
+  stats[2] = *total;
+  stats[3] = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int desmoe_expert_ffn(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
+                      const int* route_idx, const double* route_gate, const int* route_cnt,
+                      float* y, void* stream) {
+  if (!c || !ex) return fail(DESMOE_EINVAL, "null argument");
+  int rc = check_block(c, n, ex->m);
+  if (rc) return rc;
+  if (k < 1 || k > c->max_k) return fail(DESMOE_EINVAL, "top_k out of range");
+  return ffn_impl(c, ex, x, n, k, route_idx, route_gate, route_cnt, y, S(stream));
+}
+
+int desmoe_router_logits(desmoe_ctx* c, const void* x, const void* w_r, int n, int m, int d,
+                         float* logits, void* stream) {
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  int splits = 0;
+  cudaStream_t st = S(stream);
+  rc = router_impl(c, x, w_r, n, m, d, &splits, st);
+  if (rc) return rc;
+  // reduce the partials in ascending split order (the same reduction the
+  // fused gating kernel performs)
+  GateTopkArgs<float> a{};
+  a.partials = c->partials;
+  a.logits_out = logits;
+  a.splits = splits;
+  a.m_pad = m;
+  a.n = n;
+  a.m = m;
+  a.k = 1;
+  a.kmax = 1;
+  a.act = DESMOE_IDENTITY;
+  a.mode = 1;
+  a.topk_idx = c->topk_idx;
+  a.err = c->err;
+  const int warps = 8;
+  const size_t smem = static_cast<size_t>(warps) * m * sizeof(double) + warps * 32 * sizeof(int);
+  cudaError_t e = launch_gate_topk_kernel<float>(a, (n + warps - 1) / warps, warps * 32, smem, st);
+  if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("gate_topk: ") + cudaGetErrorString(e));
+  return DESMOE_OK;
+}
+
+int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
+                         int n, const desmoe_route_cfg* cfg, float* y, int* stats, void* stream) {
+  if (!c || !ex || !cfg) return fail(DESMOE_EINVAL, "null argument");
+  if (cfg->experts != ex->m) return fail(DESMOE_EINVAL, "config experts differ from expert bank");
+  int rc = check_block(c, n, cfg->experts);
+  if (rc) return rc;
+  cudaStream_t st = S(stream);
+  int splits = 0;
+  rc = router_impl(c, x, w_r, n, cfg->experts, ex->d, &splits, st);
+  if (rc) return rc;
+  rc = route_impl<float>(c, nullptr, c->partials, splits, n, cfg, nullptr, st);
+  if (rc) return rc;
+  rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y, st);
+  if (rc) return rc;
+  if (stats) {
+    stats_kernel<<<1, 1, 0, st>>>(c->n_active,
+                                  cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members,
+                                  c->total, stats);
+    DESMOE_LAUNCHED();
+  }
+  return DESMOE_OK;
+}
+
+int desmoe_layer_forward_host(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
+                              const void* x_host, int n, const desmoe_route_cfg* cfg,
+                              float* y_host, int* stats_host, void* stream) {
+  if (!c || !ex || !cfg || !x_host || !y_host) return fail(DESMOE_EINVAL, "null argument");
+  int rc = check_block(c, n, cfg->experts);
+  if (rc) return rc;
+  if (ex->d > c->max_d) return fail(DESMOE_EINVAL, "hidden exceeds context capacity");
+  cudaStream_t st = S(stream);
+  const size_t xb = static_cast<size_t>(n) * ex->d * 2, yb = static_cast<size_t>(n) * ex->d * 4;
+  DESMOE_CUDA(cudaMemcpyAsync(c->x_dev, x_host, xb, cudaMemcpyHostToDevice, st));
+  rc = desmoe_layer_forward(c, ex, w_r, c->x_dev, n, cfg, c->y_dev, c->stats_dev, stream);
+  if (rc) return rc;
+  DESMOE_CUDA(cudaMemcpyAsync(y_host, c->y_dev, yb, cudaMemcpyDeviceToHost, st));
+  if (stats_host)
+    DESMOE_CUDA(cudaMemcpyAsync(stats_host, c->stats_dev, 4 * sizeof(int),
+                                cudaMemcpyDeviceToHost, st));
+  DESMOE_CUDA(cudaStreamSynchronize(st));
+  return desmoe_check(c, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+"""The DES MoE layer (router -> DES coreset -> constrained re-route ->
+permutation -> grouped SwiGLU expert FFN + combine) on one B200, through the
+C ABI's desmoe_layer_forward / desmoe_layer_forward_host.
+
+Weights live in HBM as bf16: router [M x d], experts w_gate/w_up [M x F x d],
+w_down [M x d x F] (the 2-D row-major views the TMA descriptors stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _lib
+from ._lib import RouteCfg, check, lib
+from .dessim import ExpertWeights, _Ctx, _ptr, _stream
+
+STRATEGIES = {"vanilla": _lib.VANILLA, "seq": _lib.SEQ, "vote": _lib.VOTE}
+
+
+@dataclass
+class LayerConfig:
+    experts: int
+    top_k: int
+    hidden: int
+    ffn: int
+    strategy: str = "vote"   # vanilla | seq | vote
+    seq_k: int = 3
+    vote_beta: float = 0.4
+    activation: int = _lib.SOFTMAX
+
+    def route_cfg(self, strategy=None):
+        s = STRATEGIES[strategy or self.strategy]
+        return RouteCfg(self.experts, self.top_k, self.activation, s, self.seq_k,
+                        float(self.vote_beta), _lib.VOTE_ACTIVATED)
+
+
+class DesMoeLayer:
+    def __init__(self, cfg: LayerConfig, w_router, w_gate, w_up, w_down, max_tokens=256):
+        import torch
+        self.cfg = cfg
+        self.w_router = w_router.contiguous()
+        self.experts = ExpertWeights.swiglu(w_gate, w_up, w_down)
+        self.ctx = self.experts.ctx
+        self.stats = torch.zeros(4, dtype=torch.int32, device="cuda")
+
+    def forward(self, x, y=None, strategy=None, stream=None):
+        """x [n x d] bf16 on the device -> y [n x d] fp32 (stream-ordered)."""
+        import torch
+        n = x.shape[0]
+        if y is None:
+            y = torch.empty((n, self.cfg.hidden), dtype=torch.float32, device=x.device)
+        rc = self.cfg.route_cfg(strategy)
+        st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream()
+        check(lib().desmoe_layer_forward(self.ctx.h, self.experts.h, _ptr(self.w_router),
+                                         _ptr(x), n, C.byref(rc), _ptr(y), _ptr(self.stats), st))
+        return y
+
+    def forward_host(self, x_host, y_host, stats_host=None, strategy=None):
+        """Host (pinned) bf16 x -> host fp32 y through desmoe_layer_forward_host
+        (H2D copy, layer, D2H copy, synchronise)."""
+        rc = self.cfg.route_cfg(strategy)
+        check(lib().desmoe_layer_forward_host(
+            self.ctx.h, self.experts.h, _ptr(self.w_router), _ptr(x_host), x_host.shape[0],
+            C.byref(rc), _ptr(y_host), _ptr(stats_host) if stats_host is not None else None,
+            _stream()))
+        return y_host
+
+    def check(self):
+        check(lib().desmoe_check(self.ctx.h, _stream()))
