@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the DES MoE layer on B200 (BASELINE.json metric: MoE-layer
+µs/block and expert-weight HBM GB/s vs vanilla top-k, unique experts loaded).
+
+Workload (BASELINE.json configs[1]): LLaDA-MoE-7B-shaped layer, M=64 experts,
+top-8, hidden d=2048, SwiGLU expert width F=1024 (not fixed by the reference;
+stated), block N=32 tokens, softmax router, DES-Vote beta=0.4 (M_core=25).
+Random-init bf16 weights; synthetic hidden states X = rho*b + (1-rho)*eps
+(rho=0.3). One step = one block through the whole layer: router GEMM ->
+activation/top-K -> DES coreset -> constrained re-route -> permutation ->
+grouped SwiGLU expert FFN -> combine.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c1|c2|c3|c4] [--block N]
+
+`value` = device-timed µs/block of the DES-Vote layer (inputs resident in HBM,
+L2 flushed by a 256 MiB write before every timed step, CUDA events on the
+layer's stream); `e2e` = the same through the host-buffer C-ABI entry
+(desmoe_layer_forward_host: pinned H2D of X, layer, D2H of Y, synchronise).
+`--impl reference` times the reference library's own CPU layer
+(oracle/_ref: des_run + moe_forward with its linear dim x dim experts) on the
+host cores.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: experts, top_k, hidden, ffn, block, beta, rho, description
+    "c1": dict(experts=64, top_k=8, hidden=512, ffn=512, block=32, beta=0.4, rho=0.3,
+               desc="tiny synthetic MoE layer (proj/tests shape)"),
+    "c2": dict(experts=64, top_k=8, hidden=2048, ffn=1024, block=32, beta=0.4, rho=0.3,
+               desc="LLaDA-MoE-7B-A1B-shaped layer"),
+    "c3": dict(experts=256, top_k=8, hidden=2048, ffn=512, block=32, beta=0.15, rho=0.3,
+               desc="LLaDA2.0-mini-shaped layer"),
+    "c4": dict(experts=128, top_k=8, hidden=2048, ffn=768, block=32, beta=0.3, rho=0.3,
+               desc="Qwen3-30B-A3B-shaped layer"),
+}
+METRIC = "DES MoE-layer µs/block and expert-weight HBM GB/s vs vanilla top-k"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, cfg):
+    """Reference arm: the reference's own CPU layer (oracle/_ref)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import Ref
+    from paper_2602_00879_b200 import synth
+    import numpy as np
+    ref = Ref()
+    threads = os.cpu_count() or 1
+    n, m, k, d = cfg["block"], cfg["experts"], cfg["top_k"], cfg["hidden"]
+    vals = []
+    u = 0
+    for i in range(args.warmup + args.steps):
+        x = synth.gen_trace_block(m, n, 42, rho=cfg["rho"], block_index=i)
+        sec, u = ref.time_layer(x, k, "vote", beta=cfg["beta"], dim=d, reps=1, threads=threads,
+                                ffn_tokens=args.ref_ffn_tokens)
+        if i >= args.warmup:
+            vals.append(sec * 1e6)
+    v = float(np.mean(vals))
+    sample = (f"per step: {threads} threads x 1 block each; des_run(vote beta={cfg['beta']}) on "
+              f"all {n} tokens + moe_forward (reference linear {d}x{d} fp64 experts) on "
+              f"{args.ref_ffn_tokens or n} tokens scaled to {n}; gen_trace shared_bias rho="
+              f"{cfg['rho']} logits")
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "us/block", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v / 1e3, 6),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": config_dict(cfg, "vote"),
+            "cpu_baseline": {"value": round(v, 3), "unit": "us/block", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": round(v, 3), "unit": "us/block", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "unique_experts": u}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, strategy):
+    return {"workload": f"{cfg['desc']}: M={cfg['experts']} experts top-{cfg['top_k']}, "
+                        f"d={cfg['hidden']}, SwiGLU F={cfg['ffn']}, block N={cfg['block']}, "
+                        f"DES-Vote beta={cfg['beta']}",
+            "experts": cfg["experts"], "top_k": cfg["top_k"], "hidden": cfg["hidden"],
+            "ffn": cfg["ffn"], "block_size": cfg["block"], "strategy": strategy,
+            "vote_beta": cfg["beta"], "activation": "softmax", "rho": cfg["rho"],
+            "l2": "flushed by a 256 MiB write before every timed step",
+            "parallelism": "ep1"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--block", type=int, default=0, help="override block size N")
+    ap.add_argument("--ref-ffn-tokens", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also report N=8..256 and strategies")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = dict(CONFIGS[args.config])
+    if args.block:
+        cfg["block"] = args.block
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2602_00879_b200 import _lib, synth
+    from paper_2602_00879_b200.dessim import _ptr
+    from paper_2602_00879_b200.layer import DesMoeLayer, LayerConfig
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, m, k, d, f = cfg["block"], cfg["experts"], cfg["top_k"], cfg["hidden"], cfg["ffn"]
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000 + rank)
+    wr = synth.router_weights(m, d, seed=2000 + rank)
+    lc = LayerConfig(m, k, d, f, strategy="vote", seq_k=3, vote_beta=cfg["beta"])
+    layer = DesMoeLayer(lc, wr, wg, wu, wd)
+    L = _lib.lib()
+    L.desmoe_set_profiling(layer.ctx.h, 1)
+    total = args.warmup + args.steps
+    xs = [synth.hidden_states(n, d, seed=10_000 * (rank + 1) + i, rho=cfg["rho"])
+          for i in range(total)]
+    y = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    ph = (C.c_float * 8)()
+
+    def run(strategy, steps_list, record=True):
+        times, phases, us = [], [], []
+        lc.seq_k = 3 if strategy != "seq2" else 2
+        strat = "seq" if strategy.startswith("seq") else strategy
+        for i, x in steps_list:
+            flush.fill_(i & 0xFF)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            layer.forward(x, y, strategy=strat)
+            e1.record(stream)
+            e1.synchronize()
+            if record:
+                times.append(e0.elapsed_time(e1) * 1e3)
+                cnt = L.desmoe_get_phase_ms(layer.ctx.h, ph, 8)
+                phases.append([ph[j] * 1e3 for j in range(cnt)])
+                us.append(layer.stats.cpu().numpy().copy())
+        return times, phases, us
+
+    steps = list(enumerate(xs))
+    warm, timed = steps[: args.warmup], steps[args.warmup:]
+    results = {}
+    for strategy in ("vanilla", "seq3", "seq2", "vote"):
+        run(strategy, warm, record=False)
+        if strategy == "vote":
+            if ws > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            with ClockSampler(local) as clk:
+                t, p, s = run(strategy, timed)
+            torch.cuda.synchronize()
+            clocks = clk.summary()
+        else:
+            t, p, s = run(strategy, timed)
+        results[strategy] = (np.array(t), np.array(p), np.array(s))
+    launches = L.desmoe_last_launch_count(layer.ctx.h)
+
+    # e2e: host buffers through desmoe_layer_forward_host
+    xh = [x.cpu().pin_memory() for _, x in timed]
+    yh = torch.empty((n, d), dtype=torch.float32).pin_memory()
+    sh = torch.empty(4, dtype=torch.int32).pin_memory()
+    L.desmoe_set_profiling(layer.ctx.h, 0)
+    for _, x in warm:
+        layer.forward_host(x.cpu().pin_memory(), yh, sh, strategy="vote")
+    e2e = []
+    for i, x in enumerate(xh):
+        flush.fill_(i & 0xFF)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        layer.forward_host(x, yh, sh, strategy="vote")
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1) * 1e3)
+    e2e_us = float(np.mean(e2e))
+
+    # max over ranks (µs per block for the timed steps)
+    t_vote, p_vote, s_vote = results["vote"]
+    tot_us = float(t_vote.sum())
+    if ws > 1:
+        tt = torch.tensor([tot_us, e2e_us * len(e2e)], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        tot_us, e2e_tot = float(tt[0]), float(tt[1])
+        e2e_us = e2e_tot / len(e2e)
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+    value = tot_us / (args.steps * ws)
+    peak, peak_kind = measured_peaks()
+    wbytes_per_expert = 3 * d * f * 2
+
+    def summarize(name):
+        t, p, s = results[name]
+        gu, dn = p[:, 3], p[:, 4]
+        u = s[:, 0].astype(float)
+        gbps = (u * wbytes_per_expert) / ((gu + dn) * 1e-6) / 1e9
+        return {"us_per_block": round(float(t.mean()), 3),
+                "us_median": round(float(np.median(t)), 3),
+                "unique_experts": round(float(u.mean()), 2),
+                "coreset": round(float(s[:, 1].mean()), 2),
+                "expert_weight_GBps": round(float(gbps.mean()), 1),
+                "phase_us": {nm: round(float(p[:, j].mean()), 2) for j, nm in enumerate(
+                    ["router", "routing", "permute_gather", "ffn_gate_up", "ffn_down",
+                     "combine"]) if j < p.shape[1]}}
+
+    summ = {nm: summarize(nm) for nm in results}
+    v, van = summ["vote"], summ["vanilla"]
+    ffn_us = v["phase_us"]["ffn_gate_up"] + v["phase_us"]["ffn_down"]
+    achieved = v["unique_experts"] * wbytes_per_expert / (ffn_us * 1e-6) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("ffn_dram_bytes_per_block")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "us/block", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1e3, 6),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init weights, rho-correlated hidden states)",
+        "config": config_dict(cfg, "vote"),
+        "latency_reduction_vs_vanilla": round(1.0 - v["us_per_block"] / van["us_per_block"], 4),
+        "unique_expert_reduction_vs_vanilla": round(
+            1.0 - v["unique_experts"] / van["unique_experts"], 4),
+        "strategies": summ,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "tile_gemm_kernel (gate/up + down expert GEMMs)",
+                     "algorithmic_bytes": "U*3*d*F*2 expert-weight bytes per block",
+                     "peak_kind": peak_kind},
+        "e2e": {"value": round(e2e_us, 3), "unit": "us/block",
+                "h2d_bytes_per_step": n * d * 2, "d2h_bytes_per_step": n * d * 4 + 16},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        try:
+            from oracle.oracle import Ref
+            ref = Ref()
+            threads = os.cpu_count() or 1
+            x0 = synth.gen_trace_block(m, n, 42, rho=cfg["rho"])
+            sec, _u = ref.time_layer(x0, k, "vote", beta=cfg["beta"], dim=d, reps=1,
+                                     threads=threads)
+            line["cpu_baseline"] = {
+                "value": round(sec * 1e6, 1), "unit": "us/block", "cores": threads,
+                "kind": "reference",
+                "sample": f"1 step: {threads} threads x 1 block; reference des_run(vote) + "
+                          f"moe_forward with its linear {d}x{d} fp64 experts (the reference has "
+                          f"no SwiGLU expert), gen_trace shared_bias logits"}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "unit": "us/block", "cores": 0,
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

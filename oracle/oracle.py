@@ -229,6 +229,25 @@ class Ref(_Base):
             x, n, m, k, s, seq_k, beta, reps, threads)
 
 
+def _ref_time_layer(self, logits, k, strategy, seq_k=1, beta=1.0, dim=2048, reps=1, threads=1,
+                    seed=7, ffn_tokens=0):
+    """Estimated seconds per block of the reference layer (routing on the whole
+    block + moe_forward with linear experts on `ffn_tokens` tokens, scaled);
+    returns (seconds_per_block, unique_experts)."""
+    x = _f64(logits)
+    n, m = x.shape
+    s = {"vanilla": -1, "seq": 0, "vote": 1}[strategy]
+    u = C.c_int()
+    f = self._fn("time_layer", [_f64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                C.c_int, C.c_int, C.c_int, C.c_ulonglong, C.c_int,
+                                C.POINTER(C.c_int)], C.c_double)
+    sec = f(x, n, m, k, s, seq_k, beta, dim, reps, threads, seed, ffn_tokens, C.byref(u))
+    return sec, u.value
+
+
+Ref.time_layer = _ref_time_layer
+
+
 class Port(_Base):
     """The C restatement (oracle/liboracle.so)."""
 

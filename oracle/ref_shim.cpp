@@ -18,6 +18,7 @@
 //   Rng                 core.cpp:111-158
 // Errors: 0 ok, 1 std::invalid_argument, 2 any other exception; the message is
 // kept per thread and returned by dsref_last_error().
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -288,6 +289,62 @@ double dsref_time_routing(const double* logits, int n, int m, int k, int strateg
   for (auto& t : pool_threads) t.join();
   double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return static_cast<double>(reps) * threads / s;
+}
+
+// CPU timing of the reference's whole MoE layer for one block (bench.py's
+// reference arm and cpu_baseline): routing (strategy -1 vanilla
+// topk_route(activate), 0 seq / 1 vote des_run) followed by moe_forward
+// (gating.cpp:136-157) with the reference's own expert model, a linear
+// dim x dim map, over a bank holding the experts the block routes to (ids
+// remapped; the bank is generated once, outside the timed region).
+// Bounded sample: routing runs on the whole block; moe_forward runs on the
+// first `ffn_tokens` tokens' routes and its time is scaled by n / ffn_tokens
+// (its cost is linear in tokens). `threads` workers each process `reps`
+// samples (per-block parallelism). Returns estimated wall seconds
+// per block at that parallelism; *unique_out = U of the block.
+double dsref_time_layer(const double* logits, int n, int m, int k, int strategy, int seq_k,
+                        double beta, int dim, int reps, int threads, unsigned long long seed,
+                        int ffn_tokens, int* unique_out) {
+  RouterBlock blk = block_of(logits, n, m);
+  PoolConfig cfg = pool(m, k, 0, dim);
+  DesParams p;
+  p.strategy = strategy == 0 ? DesStrategy::seq : DesStrategy::vote;
+  p.seq_k = seq_k;
+  p.vote_beta = beta;
+  if (ffn_tokens < 1 || ffn_tokens > n) ffn_tokens = n;
+  auto route = [&]() {
+    return strategy < 0 ? topk_route(activate(blk, cfg), k) : des_run(blk, cfg, p).assignment;
+  };
+  RoutingAssignment probe = route();
+  Coreset used = unique_experts(probe);
+  *unique_out = used.size();
+  std::vector<int> local(m, -1);
+  for (int i = 0; i < used.size(); ++i) local[used.members[i]] = i;
+  ExpertBank bank =
+      make_expert_bank(pool(used.size(), std::min(k, used.size()), 0, dim), ffn_tokens, seed);
+  std::vector<double> t_route(threads, 0.0), t_ffn(threads, 0.0);
+  auto work = [&](int tid) {
+    for (int r = 0; r < reps; ++r) {
+      auto t0 = std::chrono::steady_clock::now();
+      RoutingAssignment a = route();
+      auto t1 = std::chrono::steady_clock::now();
+      a.tokens.resize(ffn_tokens);
+      for (TokenRoute& t : a.tokens)
+        for (int& e : t.experts) e = local[e];
+      volatile double sink = moe_forward(a, bank)[0];
+      (void)sink;
+      auto t2 = std::chrono::steady_clock::now();
+      t_route[tid] += std::chrono::duration<double>(t1 - t0).count();
+      t_ffn[tid] += std::chrono::duration<double>(t2 - t1).count();
+    }
+  };
+  std::vector<std::thread> ts;
+  for (int t = 0; t < threads; ++t) ts.emplace_back(work, t);
+  for (auto& t : ts) t.join();
+  double per_block = 0.0;  // slowest worker's per-sample estimate
+  for (int t = 0; t < threads; ++t)
+    per_block = std::max(per_block, (t_route[t] + t_ffn[t] * n / ffn_tokens) / reps);
+  return per_block / threads;
 }
 
 }  // extern "C"

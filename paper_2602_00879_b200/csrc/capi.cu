@@ -123,6 +123,11 @@ struct desmoe_ctx {
   const void* x_map_ptr = nullptr;
   int x_map_n = -1, x_map_d = -1;
   BoxMaps x_maps{};
+  // live phase timing
+  bool profiling = false;
+  cudaEvent_t ev[8] = {};
+  int n_ev = 0;
+  int launches = 0;
   const void* wr_map_ptr = nullptr;
   int wr_map_m = -1, wr_map_d = -1;
   CUtensorMap wr_map{};
@@ -226,6 +231,8 @@ void desmoe_destroy(desmoe_ctx* c) {
                   c->y_dev, c->stats_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -596,6 +603,13 @@ void desmoe_experts_destroy(desmoe_experts* ex) {
 
 namespace {
 
+void mark(desmoe_ctx* c, cudaStream_t st) {
+  if (!c->profiling || c->n_ev >= 8) return;
+  if (!c->ev[c->n_ev]) cudaEventCreate(&c->ev[c->n_ev]);
+  cudaEventRecord(c->ev[c->n_ev], st);
+  c->n_ev++;
+}
+
 int b_rows_for(int n) {
   int b = 16;
   while (b < n && b < 256) b <<= 1;
@@ -651,6 +665,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
       reinterpret_cast<const uint4*>(x), c->slot_token, c->total,
       reinterpret_cast<uint4*>(ex->x_perm), d / 8);
   DESMOE_LAUNCHED();
+  c->launches += 2;
+  mark(c, st);
 
   TileArgs a{};
   a.n_tok = n;
@@ -671,6 +687,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
     g.h_out = ex->h_perm;
     rc = launch_tile(kGateUp, ex->wg, ex->wu, ex->xp_maps, g, m * (f / kBM), st);
     if (rc) return rc;
+    c->launches += 1;
+    mark(c, st);
     TileArgs dn = a;
     dn.tiles_per_unit_expert = d / kBM;
     dn.kb_total = f / kBK;
@@ -679,6 +697,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
     dn.y_out = ex->y_slot;
     rc = launch_tile(kDown, ex->wd, ex->wd, ex->h_maps, dn, m * (d / kBM), st);
     if (rc) return rc;
+    c->launches += 1;
+    mark(c, st);
   } else {
     TileArgs dn = a;
     dn.tiles_per_unit_expert = d / kBM;
@@ -688,9 +708,13 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
     dn.y_out = ex->y_slot;
     rc = launch_tile(kDown, ex->wd, ex->wd, ex->xp_maps, dn, m * (d / kBM), st);
     if (rc) return rc;
+    c->launches += 1;
+    mark(c, st);
+    mark(c, st);
   }
   combine_kernel<<<n, 256, 0, st>>>(ex->y_slot, c->slot_of, route_cnt, n, k, d, y);
   DESMOE_LAUNCHED();
+  c->launches += 1;
   return DESMOE_OK;
 }
 
@@ -791,11 +815,18 @@ int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_
   int rc = check_block(c, n, cfg->experts);
   if (rc) return rc;
   cudaStream_t st = S(stream);
+  c->n_ev = 0;
+  c->launches = 0;
+  mark(c, st);
   int splits = 0;
   rc = router_impl(c, x, w_r, n, cfg->experts, ex->d, &splits, st);
   if (rc) return rc;
+  c->launches += 1;
+  mark(c, st);
   rc = route_impl<float>(c, nullptr, c->partials, splits, n, cfg, nullptr, st);
   if (rc) return rc;
+  c->launches += cfg->strategy == DESMOE_VANILLA ? 1 : 3;
+  mark(c, st);
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y, st);
   if (rc) return rc;
   if (stats) {
@@ -803,9 +834,29 @@ int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_
                                   cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members,
                                   c->total, stats);
     DESMOE_LAUNCHED();
+    c->launches += 1;
   }
+  mark(c, st);
   return DESMOE_OK;
 }
+
+int desmoe_set_profiling(desmoe_ctx* c, int enable) {
+  if (!c) return fail(DESMOE_EINVAL, "null context");
+  c->profiling = enable != 0;
+  return DESMOE_OK;
+}
+
+int desmoe_get_phase_ms(desmoe_ctx* c, float* ms, int max_phases) {
+  if (!c || !ms) return fail(DESMOE_EINVAL, "null argument");
+  if (c->n_ev < 2) return 0;
+  DESMOE_CUDA(cudaEventSynchronize(c->ev[c->n_ev - 1]));
+  int w = 0;
+  for (int i = 0; i + 1 < c->n_ev && w < max_phases; ++i, ++w)
+    DESMOE_CUDA(cudaEventElapsedTime(&ms[w], c->ev[i], c->ev[i + 1]));
+  return w;
+}
+
+int desmoe_last_launch_count(desmoe_ctx* c) { return c ? c->launches : 0; }
 
 int desmoe_layer_forward_host(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
                               const void* x_host, int n, const desmoe_route_cfg* cfg,
