@@ -185,13 +185,18 @@ int desmoe_layer_forward_host(desmoe_ctx* ctx, const desmoe_experts* ex,
                               const desmoe_route_cfg* cfg, float* y_host, int* stats_host,
                               void* stream);
 
+/* desmoe_layer_forward captures its launch sequence into a CUDA graph the
+ * first time it sees a given (experts, router, x, n, cfg, y, stats) tuple and
+ * replays it afterwards; enable = 0 launches eagerly instead. Default on. */
+int desmoe_set_graphs(desmoe_ctx* ctx, int enable);
+
 /* ---- live phase timing -------------------------------------------------------
  * When enabled, desmoe_layer_forward records CUDA events on its stream between
- * its phases: [0] router GEMM, [1] gating/coreset/re-route, [2] permutation +
- * gather, [3] gate/up expert GEMM, [4] down expert GEMM (+ combine when fused),
- * [5] combine/stats. desmoe_get_phase_ms synchronises on the last event and
- * writes up to max_phases elapsed times (ms) of the LAST call; returns the
- * number written. */
+ * its phases: [0] router GEMM, [1] gating + coreset + constrained re-route,
+ * [2] persistent expert FFN (permutation, gather, gate/up + down GEMMs, fused
+ * combine). desmoe_get_phase_ms synchronises on the last event and writes up
+ * to max_phases elapsed times (ms) of the LAST call; returns the number
+ * written. */
 int desmoe_set_profiling(desmoe_ctx* ctx, int enable);
 int desmoe_get_phase_ms(desmoe_ctx* ctx, float* ms_out, int max_phases);
 /* Kernels launched by the last desmoe_layer_forward call. */

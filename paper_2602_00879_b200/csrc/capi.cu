@@ -85,6 +85,7 @@ int make_box_maps(BoxMaps* maps, const void* base, uint64_t rows, uint64_t cols)
 int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
 constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemLimit = 227 * 1024;
 
 }  // namespace
 
@@ -123,6 +124,19 @@ struct desmoe_ctx {
   const void* x_map_ptr = nullptr;
   int x_map_n = -1, x_map_d = -1;
   BoxMaps x_maps{};
+  // CUDA graph of the whole layer (re-captured when any argument changes)
+  bool use_graphs = true;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  struct Key {
+    const void *ex, *wr, *x;
+    int n;
+    desmoe_route_cfg cfg;
+    float* y;
+    int* stats;
+    bool prof;
+  } gkey{};
+  int g_n_ev = 0, g_launches = 0;
   // live phase timing
   bool profiling = false;
   cudaEvent_t ev[8] = {};
@@ -141,6 +155,7 @@ struct desmoe_experts {
   __nv_bfloat16* x_perm = nullptr;  // [max_n*max_k x d]
   __nv_bfloat16* h_perm = nullptr;  // [max_n*max_k x f]
   float* y_slot = nullptr;          // [max_n*max_k x d]
+  int* counters = nullptr;          // FFN scheduler / readiness counters
 };
 
 extern "C" {
@@ -214,6 +229,8 @@ int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
   A(alloc(&c->y_dev, static_cast<size_t>(max_tokens) * max_hidden));
   A(alloc(&c->stats_dev, 4));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = desmoe::set_kernel_smem_limits();
   if (e != cudaSuccess) {
     desmoe_destroy(c);
     return fail(DESMOE_ECUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -233,6 +250,8 @@ void desmoe_destroy(desmoe_ctx* c) {
     if (p) cudaFree(p);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
 
@@ -318,9 +337,6 @@ int launch_coreset(desmoe_ctx* c, const T* logits, int n, const desmoe_route_cfg
   const int words = (m + 31) / 32;
   const size_t smem = static_cast<size_t>(n) * words * 4 + 8 + static_cast<size_t>(m) * 8 +
                       static_cast<size_t>(m) * 4;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(coreset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
   const int threads = std::max(128, round_up(m, 32));
   coreset_kernel<<<1, threads, smem, st>>>(a);
   DESMOE_LAUNCHED();
@@ -399,9 +415,6 @@ int route_impl(desmoe_ctx* c, const T* logits, const float* partials, int splits
       p.total = c->total;
       const int tw = (n + 31) / 32;
       const size_t smem = static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
       permute_kernel<<<1, std::max(128, round_up(m, 32)), smem, st>>>(p);
       DESMOE_LAUNCHED();
     }
@@ -538,9 +551,6 @@ int desmoe_permute(desmoe_ctx* c, const int* route_idx, const int* route_cnt, in
   p.total = c->total;
   const int tw = (n + 31) / 32;
   const size_t smem = static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
   permute_kernel<<<1, std::max(128, round_up(m, 32)), smem, S(stream)>>>(p);
   DESMOE_LAUNCHED();
   return DESMOE_OK;
@@ -567,6 +577,8 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
   cudaError_t e = cudaMalloc(&ex->x_perm, slots * d * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ex->h_perm, slots * f * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ex->y_slot, slots * d * 4);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&ex->counters, sizeof(int) * ffn_counter_words(m, c->max_n, d));
   if (e != cudaSuccess) {
     desmoe_experts_destroy(ex);
     return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
@@ -596,6 +608,7 @@ void desmoe_experts_destroy(desmoe_experts* ex) {
   if (ex->x_perm) cudaFree(ex->x_perm);
   if (ex->h_perm) cudaFree(ex->h_perm);
   if (ex->y_slot) cudaFree(ex->y_slot);
+  if (ex->counters) cudaFree(ex->counters);
   delete ex;
 }
 
@@ -616,105 +629,69 @@ int b_rows_for(int n) {
   return b;
 }
 
-int launch_tile(int mode, const CUtensorMap& wa, const CUtensorMap& wb, const BoxMaps& acts,
-                TileArgs a, int grid, cudaStream_t st) {
-  const int stage_bytes = kATile * (mode == kGateUp ? 2 : 1) + a.b_rows * 128;
-  const int per_unit_kb = mode == kRouter ? (a.kb_total + a.splits - 1) / a.splits : a.kb_total;
+int launch_router_tiles(const CUtensorMap& wa, const BoxMaps& acts, TileArgs a, int grid,
+                        cudaStream_t st) {
+  const int stage_bytes = kATile + a.b_rows * 128;
+  const int per_unit_kb = (a.kb_total + a.splits - 1) / a.splits;
   int stages = (kSmemBudget - 1024 - 256) / stage_bytes;
   stages = std::max(1, std::min(stages, std::max(per_unit_kb, 1)));
   a.stages = stages;
-  a.mode = mode;
   const size_t smem = static_cast<size_t>(stages) * stage_bytes + 1024 + 256;
-  cudaFuncSetAttribute(tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem));
-  tile_gemm_kernel<<<grid, 256, smem, st>>>(wa, wb, acts, a);
+  tile_gemm_kernel<<<grid, 256, smem, st>>>(wa, wa, acts, a);
   DESMOE_LAUNCHED();
   return DESMOE_OK;
 }
 
 int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
-             cudaStream_t st) {
+             const int* n_members, int* stats, cudaStream_t st) {
   const int m = ex->m, d = ex->d, f = ex->f;
   if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
-  // K3: permutation
-  PermuteArgs p{};
-  p.n = n;
-  p.m = m;
-  p.k = k;
-  p.route_idx = route_idx;
-  p.route_cnt = route_cnt;
-  p.route_gate = route_gate;
-  p.expert_count = c->expert_count;
-  p.expert_offset = c->expert_offset;
-  p.slot_of = c->slot_of;
-  p.slot_token = c->slot_token;
-  p.slot_gate = c->slot_gate;
-  p.active = c->active;
-  p.n_active = c->n_active;
-  p.total = c->total;
-  const int tw = (n + 31) / 32;
-  const size_t psmem = static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;
-  if (psmem > 48 * 1024)
-    cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(psmem));
-  permute_kernel<<<1, std::max(128, round_up(m, 32)), psmem, st>>>(p);
-  DESMOE_LAUNCHED();
-  // gather token rows into expert-grouped order
-  gather_rows_kernel<<<n * k, std::min(256, d / 8), 0, st>>>(
-      reinterpret_cast<const uint4*>(x), c->slot_token, c->total,
-      reinterpret_cast<uint4*>(ex->x_perm), d / 8);
-  DESMOE_LAUNCHED();
-  c->launches += 2;
-  mark(c, st);
-
-  TileArgs a{};
+  const int words = ffn_counter_words(m, n, d);
+  DESMOE_CUDA(cudaMemsetAsync(ex->counters, 0, sizeof(int) * words, st));
+  FfnArgs a{};
+  a.mode = ex->kind == DESMOE_FFN_SWIGLU ? 0 : 1;
   a.n_tok = n;
-  a.splits = 1;
-  a.n_active = c->n_active;
-  a.active = c->active;
-  a.expert_offset = c->expert_offset;
-  a.expert_count = c->expert_count;
+  a.top_k = k;
+  a.m = m;
+  a.d = d;
+  a.f = f;
   a.b_rows = b_rows_for(n);
-  a.slot_gate = c->slot_gate;
-  int rc;
-  if (ex->kind == DESMOE_FFN_SWIGLU) {
-    TileArgs g = a;
-    g.tiles_per_unit_expert = f / kBM;
-    g.kb_total = d / kBK;
-    g.weight_rows_per_expert = f;
-    g.ld_out = f;
-    g.h_out = ex->h_perm;
-    rc = launch_tile(kGateUp, ex->wg, ex->wu, ex->xp_maps, g, m * (f / kBM), st);
-    if (rc) return rc;
-    c->launches += 1;
-    mark(c, st);
-    TileArgs dn = a;
-    dn.tiles_per_unit_expert = d / kBM;
-    dn.kb_total = f / kBK;
-    dn.weight_rows_per_expert = d;
-    dn.ld_out = d;
-    dn.y_out = ex->y_slot;
-    rc = launch_tile(kDown, ex->wd, ex->wd, ex->h_maps, dn, m * (d / kBM), st);
-    if (rc) return rc;
-    c->launches += 1;
-    mark(c, st);
-  } else {
-    TileArgs dn = a;
-    dn.tiles_per_unit_expert = d / kBM;
-    dn.kb_total = d / kBK;
-    dn.weight_rows_per_expert = d;
-    dn.ld_out = d;
-    dn.y_out = ex->y_slot;
-    rc = launch_tile(kDown, ex->wd, ex->wd, ex->xp_maps, dn, m * (d / kBM), st);
-    if (rc) return rc;
-    c->launches += 1;
-    mark(c, st);
-    mark(c, st);
-  }
-  combine_kernel<<<n, 256, 0, st>>>(ex->y_slot, c->slot_of, route_cnt, n, k, d, y);
-  DESMOE_LAUNCHED();
+  a.route_idx = route_idx;
+  a.route_cnt = route_cnt;
+  a.route_gate = route_gate;
+  a.x = reinterpret_cast<const __nv_bfloat16*>(x);
+  a.x_perm = ex->x_perm;
+  a.h_perm = ex->h_perm;
+  a.y_slot = ex->y_slot;
+  a.y = y;
+  a.counters = ex->counters;
+  a.stats = stats;
+  a.n_members = n_members;
+  const int stage_bytes = 2 * kATile + 2 * a.b_rows * 128;
+  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
+                    4 * (4 + n + 3 * m + 3 * n * k) + 64;
+  int stages = (kSmemLimit - fixed) / stage_bytes;
+  stages = std::max(2, std::min(stages, 8));
+  a.stages = stages;
+  const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
+  if (smem > static_cast<size_t>(kSmemLimit))
+    return fail(DESMOE_EINVAL, "expert FFN shared-memory plan exceeds 227 KB");
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(c->num_sms);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (x_ready handshake)
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  const CUtensorMap& wa = ex->kind == DESMOE_FFN_SWIGLU ? ex->wg : ex->wd;
+  DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, wa, ex->wu, ex->wd, ex->xp_maps,
+                                 ex->kind == DESMOE_FFN_SWIGLU ? ex->h_maps : ex->xp_maps, a));
   c->launches += 1;
+  mark(c, st);
   return DESMOE_OK;
 }
 
@@ -750,19 +727,12 @@ int router_impl(desmoe_ctx* c, const void* x, const void* w_r, int n, int m, int
   a.b_rows = b_rows_for(n);
   a.m_pad = m;
   a.y_out = c->partials;
-  int rc = launch_tile(kRouter, c->wr_map, c->wr_map, c->x_maps, a, et * splits, st);
+  int rc = launch_router_tiles(c->wr_map, c->x_maps, a, et * splits, st);
   if (rc) return rc;
   *splits_out = splits;
   return DESMOE_OK;
 }
 
-__global__ void stats_kernel(const int* n_active, const int* n_members, const int* total,
-                             int* stats) {
-  stats[0] = *n_active;
-  stats[1] = n_members ? *n_members : *n_active;
-  stats[2] = *total;
-  stats[3] = 0;
-}
 
 }  // namespace
 
@@ -775,7 +745,8 @@ int desmoe_expert_ffn(desmoe_ctx* c, const desmoe_experts* ex, const void* x, in
   int rc = check_block(c, n, ex->m);
   if (rc) return rc;
   if (k < 1 || k > c->max_k) return fail(DESMOE_EINVAL, "top_k out of range");
-  return ffn_impl(c, ex, x, n, k, route_idx, route_gate, route_cnt, y, S(stream));
+  return ffn_impl(c, ex, x, n, k, route_idx, route_gate, route_cnt, y, nullptr, nullptr,
+                  S(stream));
 }
 
 int desmoe_router_logits(desmoe_ctx* c, const void* x, const void* w_r, int n, int m, int d,
@@ -808,13 +779,14 @@ int desmoe_router_logits(desmoe_ctx* c, const void* x, const void* w_r, int n, i
   return DESMOE_OK;
 }
 
-int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
-                         int n, const desmoe_route_cfg* cfg, float* y, int* stats, void* stream) {
-  if (!c || !ex || !cfg) return fail(DESMOE_EINVAL, "null argument");
-  if (cfg->experts != ex->m) return fail(DESMOE_EINVAL, "config experts differ from expert bank");
-  int rc = check_block(c, n, cfg->experts);
-  if (rc) return rc;
-  cudaStream_t st = S(stream);
+}  // extern "C"
+
+namespace {
+
+int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
+                       int n, const desmoe_route_cfg* cfg, float* y, int* stats,
+                       cudaStream_t st) {
+  int rc;
   c->n_ev = 0;
   c->launches = 0;
   mark(c, st);
@@ -827,16 +799,77 @@ int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_
   if (rc) return rc;
   c->launches += cfg->strategy == DESMOE_VANILLA ? 1 : 3;
   mark(c, st);
-  rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y, st);
+  rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
+                cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st);
   if (rc) return rc;
-  if (stats) {
-    stats_kernel<<<1, 1, 0, st>>>(c->n_active,
-                                  cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members,
-                                  c->total, stats);
-    DESMOE_LAUNCHED();
-    c->launches += 1;
+  return DESMOE_OK;
+}
+
+bool same_key(const desmoe_ctx::Key& a, const desmoe_ctx::Key& b) {
+  return a.ex == b.ex && a.wr == b.wr && a.x == b.x && a.n == b.n && a.y == b.y &&
+         a.stats == b.stats && a.prof == b.prof && a.cfg.experts == b.cfg.experts &&
+         a.cfg.top_k == b.cfg.top_k && a.cfg.activation == b.cfg.activation &&
+         a.cfg.strategy == b.cfg.strategy && a.cfg.seq_k == b.cfg.seq_k &&
+         a.cfg.vote_beta == b.cfg.vote_beta && a.cfg.vote_source == b.cfg.vote_source;
+}
+
+}  // namespace
+
+extern "C" {
+
+int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
+                         int n, const desmoe_route_cfg* cfg, float* y, int* stats, void* stream) {
+  if (!c || !ex || !cfg) return fail(DESMOE_EINVAL, "null argument");
+  if (cfg->experts != ex->m) return fail(DESMOE_EINVAL, "config experts differ from expert bank");
+  int rc = check_block(c, n, cfg->experts);
+  if (rc) return rc;
+  cudaStream_t st = S(stream);
+  if (!c->use_graphs) return layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, st);
+  desmoe_ctx::Key key{ex, w_r, x, n, *cfg, y, stats, c->profiling};
+  if (!c->gexec || !same_key(key, c->gkey)) {
+    // validate + capture the whole launch sequence on the context's capture
+    // stream, then instantiate (or update) the executable graph
+    cudaGraph_t g = nullptr;
+    DESMOE_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, c->cap_stream);
+    cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(DESMOE_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    bool updated = false;
+    if (c->gexec) {
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(c->gexec, g, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+    }
+    if (!updated) {
+      cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
+      if (ie != cudaSuccess) {
+        cudaGraphDestroy(g);
+        c->gexec = nullptr;
+        return fail(DESMOE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+      }
+    }
+    cudaGraphDestroy(g);
+    c->gkey = key;
+    c->g_n_ev = c->n_ev;
+    c->g_launches = c->launches;
   }
-  mark(c, st);
+  DESMOE_CUDA(cudaGraphLaunch(c->gexec, st));
+  c->n_ev = c->g_n_ev;
+  c->launches = c->g_launches;
+  return DESMOE_OK;
+}
+
+int desmoe_set_graphs(desmoe_ctx* c, int enable) {
+  if (!c) return fail(DESMOE_EINVAL, "null context");
+  c->use_graphs = enable != 0;
   return DESMOE_OK;
 }
 

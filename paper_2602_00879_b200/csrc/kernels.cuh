@@ -72,51 +72,56 @@ template <typename T>
 cudaError_t launch_gate_topk_kernel(const GateTopkArgs<T>& a, int grid, int block, size_t smem,
                                     cudaStream_t st);
 __global__ void coreset_kernel(CoresetArgs a);
+cudaError_t set_kernel_smem_limits();
 __global__ void constrained_route_kernel(RerouteArgs a);
 __global__ void set_members_kernel(const int* members, int nm, int m, uint8_t* flag,
                                    int* n_members);
 __global__ void permute_kernel(PermuteArgs a);
-__global__ void gather_rows_kernel(const uint4* __restrict__ x, const int* __restrict__ slot_token,
-                                   const int* __restrict__ total, uint4* __restrict__ xp,
-                                   int row_vec);
-__global__ void combine_kernel(const float* __restrict__ y_slot, const int* __restrict__ slot_of,
-                               const int* __restrict__ route_cnt, int n, int k, int d,
-                               float* __restrict__ y);
 
-// ---- tcgen05 swap-AB tile GEMM (router / expert FFN) -----------------------
+// ---- tcgen05 swap-AB tiles (router GEMM / expert FFN) ----------------------
 constexpr int kBM = 128;             // weight rows per tile (MMA M)
 constexpr int kBK = 64;              // K elements per pipeline stage (128 B rows)
 constexpr int kATile = kBM * kBK * 2;  // 16 KB
 constexpr int kMaxBoxes = 5;         // activation box heights 16, 32, 64, 128, 256
 
-enum TileMode : int { kRouter = 0, kGateUp = 1, kDown = 2 };
-
 struct BoxMaps {
   CUtensorMap map[kMaxBoxes];  // same tensor, box heights 16 << i
 };
 
-struct TileArgs {
-  int mode;
-  // schedule
-  int n_tok;          // tokens in the block (router: rows of x)
-  int tiles_per_unit_expert;  // weight tiles per expert (ffn/128 or hidden/128)
-  int kb_total;       // K blocks of the full contraction
-  int splits;         // router split-K factor (1 otherwise)
-  int n_units_static; // router: expert tiles * splits
-  const int* n_active;  // device U (ffn modes)
-  const int* active;
-  const int* expert_offset;
-  const int* expert_count;
-  int weight_rows_per_expert;  // rows of the 2-D weight view per expert
+struct TileArgs {  // router GEMM (tile_gemm.cu)
+  int n_tok;           // tokens in the block (rows of x)
+  int kb_total;        // K blocks of the full contraction
+  int splits;          // split-K factor
+  int n_units_static;  // expert tiles * splits
   int stages;
-  int b_rows;         // smem rows reserved for the activation tile
-  // epilogue
-  int ld_out;         // leading dim (elements) of the output rows
-  int m_pad;          // router: padded expert count of the partial rows
-  const float* slot_gate;
-  __nv_bfloat16* h_out;  // kGateUp: H [slots x ffn]
-  float* y_out;          // kDown: y_slot [slots x hidden]; kRouter: partials
+  int b_rows;          // smem rows reserved for the activation tile
+  int m_pad;           // experts (row stride of the partials)
+  float* y_out;        // partials [split][token][expert]
 };
+
+struct FfnArgs {
+  int mode;  // 0 = SwiGLU (phase A + B), 1 = linear expert (phase B on x)
+  int n_tok, top_k, m, d, f, b_rows, stages;
+  const int* route_idx;      // [n x k]
+  const int* route_cnt;      // [n]
+  const double* route_gate;  // [n x k]
+  const __nv_bfloat16* x;    // [n x d]
+  __nv_bfloat16* x_perm;     // [n*k x d]
+  __nv_bfloat16* h_perm;     // [n*k x f]
+  float* y_slot;             // [n*k x d]
+  float* y;                  // [n x d]
+  int* counters;             // zeroed: sched, x_ready, h_ready[m], tok_done[n][d/128]
+  int* stats;                // optional [4]: U, coreset size, slots, 0
+  const int* n_members;      // optional coreset size
+};
+
+inline int ffn_counter_words(int m, int n, int d) { return 2 + m + n * (d / 128); }
+
+__global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,
+                                      const __grid_constant__ CUtensorMap w_b,
+                                      const __grid_constant__ CUtensorMap w_c,
+                                      const __grid_constant__ BoxMaps xp_maps,
+                                      const __grid_constant__ BoxMaps h_maps, FfnArgs a);
 
 __global__ void tile_gemm_kernel(const __grid_constant__ CUtensorMap wa,
                                  const __grid_constant__ CUtensorMap wb,

@@ -1,19 +1,14 @@
-// K1 / K4: swap-AB tcgen05 tile GEMM for the router and the grouped expert FFN.
+// K1: router GEMM as a split-K swap-AB tcgen05 tile GEMM.
 //
-// Weights are the MMA's A operand (M = 128 weight rows per tile, K-major), the
-// block's tokens are the B operand (N = tokens routed to the expert, rounded up
-// to 16), so the 1–256 tokens per expert fill the N dimension instead of
-// wasting a 128-row M tile. Both operands arrive by TMA (SWIZZLE_128B, 64-wide
-// K blocks) into a multi-stage shared-memory ring guarded by mbarriers; one
-// elected thread issues tcgen05.mma into a TMEM accumulator; four epilogue
-// warps drain TMEM with tcgen05.ld.
-//
-//   kRouter : logits^T tile = W_r[128 experts x K-slice] . X^T   (split-K)
-//             -> fp32 partials [split][token][expert]
-//   kGateUp : G = W_g[e][f-tile] . X_e^T, U = W_u[e][f-tile] . X_e^T (two
-//             accumulators) -> H[slot][f] = bf16(silu(G) * U)
-//   kDown   : Y = W_d[e][d-tile] . H_e^T (or the linear expert W[e] . X_e^T)
-//             -> y_slot[slot][d] = gate(slot) * Y
+// logits^T tile = W_r[128 experts x K-slice] . X^T: the router weights are the
+// MMA's A operand (M = 128 expert rows, K-major), the block's tokens the B
+// operand (N = tokens rounded to 16). Both arrive by TMA (SWIZZLE_128B, 64-wide
+// K blocks) into a shared-memory ring guarded by mbarriers; one elected thread
+// issues tcgen05.mma into a TMEM accumulator; four epilogue warps drain TMEM
+// with tcgen05.ld and write fp32 partials [split][token][expert]. The K range
+// is split over up to 32 CTAs so the (<= 1 MiB) router weights stream from
+// all SMs at once; the partials are reduced in fixed split order by the gating
+// kernel, so logits are deterministic.
 //
 // Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer,
 // warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM lane quarters 0-3).
@@ -36,33 +31,17 @@ struct Unit {
 
 __device__ inline Unit decode_unit(const TileArgs& a, int u) {
   Unit t{};
-  if (a.mode == kRouter) {
-    if (u >= a.n_units_static) return t;
-    const int et = u / a.splits, s = u % a.splits;
-    const int kbs = (a.kb_total + a.splits - 1) / a.splits;
-    t.valid = true;
-    t.wrow = et * kBM;
-    t.brow = 0;
-    t.count = a.n_tok;
-    t.kb0 = s * kbs;
-    t.kb1 = min(a.kb_total, t.kb0 + kbs);
-    t.out_col = et * kBM;
-    t.split = s;
-    if (t.kb0 >= t.kb1) t.valid = false;
-    return t;
-  }
-  const int tiles = a.tiles_per_unit_expert;
-  if (u >= *a.n_active * tiles) return t;
-  const int ei = u / tiles, tile = u % tiles;
-  const int e = a.active[ei];
-  t.valid = true;
-  t.wrow = e * a.weight_rows_per_expert + tile * kBM;
-  t.brow = a.expert_offset[e];
-  t.count = a.expert_count[e];
-  t.kb0 = 0;
-  t.kb1 = a.kb_total;
-  t.out_col = tile * kBM;
-  t.split = 0;
+  if (u >= a.n_units_static) return t;
+  const int et = u / a.splits, s = u % a.splits;
+  const int kbs = (a.kb_total + a.splits - 1) / a.splits;
+  t.wrow = et * kBM;
+  t.brow = 0;
+  t.count = a.n_tok;
+  t.kb0 = s * kbs;
+  t.kb1 = min(a.kb_total, t.kb0 + kbs);
+  t.out_col = et * kBM;
+  t.split = s;
+  t.valid = t.kb0 < t.kb1;
   return t;
 }
 
@@ -71,8 +50,6 @@ __device__ inline int box_index(int count) {
   while ((16 << b) < count && b < kMaxBoxes - 1) ++b;
   return b;
 }
-
-__device__ inline float silu(float g) { return g / (1.0f + expf(-g)); }
 
 }  // namespace
 
@@ -88,9 +65,8 @@ __global__ void __launch_bounds__(256, 1)
   const Unit unit = decode_unit(a, blockIdx.x);
   if (!unit.valid) return;
 
-  const bool two_a = a.mode == kGateUp;
   const int b_bytes_max = a.b_rows * 128;
-  const int stage_bytes = kATile * (two_a ? 2 : 1) + b_bytes_max;
+  const int stage_bytes = kATile + b_bytes_max;
   const int S = a.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * stage_bytes);
   uint64_t* empty = full + S;
@@ -100,13 +76,12 @@ __global__ void __launch_bounds__(256, 1)
   const int bi = box_index(unit.count);
   const int box_rows = 16 << bi;
   const int n_mma = (unit.count + 15) & ~15;
-  const uint32_t tmem_cols_needed = (two_a ? 2 : 1) * a.b_rows;
+  const uint32_t tmem_cols_needed = a.b_rows;
   uint32_t tmem_cols = 32;
   while (tmem_cols < tmem_cols_needed) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&wa);
-    if (two_a) tma_prefetch_desc(&wb);
     tma_prefetch_desc(&acts.map[bi]);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -127,7 +102,7 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       const uint64_t pol_w = l2_policy_evict_first();  // weights: streamed once
       const uint64_t pol_x = l2_policy_evict_last();   // activations: re-read per tile
-      const uint32_t bytes = kATile * (two_a ? 2 : 1) + box_rows * 128;
+      const uint32_t bytes = kATile + box_rows * 128;
       for (int i = 0; i < nkb; ++i) {
         const int s = i % S;
         const uint32_t ph = (i / S) & 1;
@@ -136,15 +111,13 @@ __global__ void __launch_bounds__(256, 1)
         const int kc = (unit.kb0 + i) * kBK;
         mbar_arrive_expect_tx(&full[s], bytes);
         tma_load_2d(st, &wa, &full[s], kc, unit.wrow, pol_w);
-        if (two_a) tma_load_2d(st + kATile, &wb, &full[s], kc, unit.wrow, pol_w);
-        tma_load_2d(st + kATile * (two_a ? 2 : 1), &acts.map[bi], &full[s], kc, unit.brow, pol_x);
+        tma_load_2d(st + kATile, &acts.map[bi], &full[s], kc, unit.brow, pol_x);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
-    const uint32_t d_gate = tmem_base;
-    const uint32_t d_up = tmem_base + a.b_rows;
+    const uint32_t d_acc = tmem_base;
     for (int i = 0; i < nkb; ++i) {
       const int s = i % S;
       const uint32_t ph = (i / S) & 1;
@@ -153,14 +126,12 @@ __global__ void __launch_bounds__(256, 1)
       if (elect_one()) {
         unsigned char* st = smem + static_cast<size_t>(s) * stage_bytes;
         const uint32_t a0 = smem_u32(st);
-        const uint32_t a1 = a0 + kATile;
-        const uint32_t b0 = a0 + kATile * (two_a ? 2 : 1);
+        const uint32_t b0 = a0 + kATile;
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
           const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
           const uint64_t bdesc = sw128_kmajor_desc(b0 + k * 32);
-          tc_mma_bf16(d_gate, sw128_kmajor_desc(a0 + k * 32), bdesc, idesc, acc);
-          if (two_a) tc_mma_bf16(d_up, sw128_kmajor_desc(a1 + k * 32), bdesc, idesc, acc);
+          tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + k * 32), bdesc, idesc, acc);
         }
         tc_commit(&empty[s]);
         if (i == nkb - 1) tc_commit(tmem_full);
@@ -177,29 +148,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int c0 = 0; c0 < n_mma; c0 += 16) {
       float v[16];
       tmem_ld16(lane_base + c0, v);
-      if (a.mode == kGateUp) {
-        float u[16];
-        tmem_ld16(lane_base + a.b_rows + c0, u);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = c0 + j;
-          if (col < unit.count) {
-            const float h = silu(v[j]) * u[j];
-            a.h_out[static_cast<size_t>(unit.brow + col) * a.ld_out + unit.out_col + r] =
-                __float2bfloat16_rn(h);
-          }
-        }
-      } else if (a.mode == kDown) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = c0 + j;
-          if (col < unit.count) {
-            const int slot = unit.brow + col;
-            a.y_out[static_cast<size_t>(slot) * a.ld_out + unit.out_col + r] =
-                v[j] * a.slot_gate[slot];
-          }
-        }
-      } else {  // router partials [split][token][expert]
+      {  // router partials [split][token][expert]
         const int e = unit.out_col + r;
         if (e < a.m_pad) {
 #pragma unroll
