@@ -415,19 +415,19 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
 // creation), so no attribute call happens inside a launch sequence / graph
 // capture.
 cudaError_t set_kernel_smem_limits() {
-  const int big = 227 * 1024;
   cudaError_t e = cudaSuccess;
-  auto set = [&](const void* fn) {
-    cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  auto set = [&](const void* fn, int bytes) {
+    cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e == cudaSuccess) e = r;
   };
-  set(reinterpret_cast<const void*>(gate_topk_kernel<double>));
-  set(reinterpret_cast<const void*>(gate_topk_kernel<float>));
-  set(reinterpret_cast<const void*>(coreset_kernel));
-  set(reinterpret_cast<const void*>(constrained_route_kernel));
-  set(reinterpret_cast<const void*>(permute_kernel));
-  set(reinterpret_cast<const void*>(tile_gemm_kernel));
-  set(reinterpret_cast<const void*>(ffn_persistent_kernel));
+  const int routing = 200 * 1024;  // leaves room for the kernels' static shared memory
+  set(reinterpret_cast<const void*>(gate_topk_kernel<double>), routing);
+  set(reinterpret_cast<const void*>(gate_topk_kernel<float>), routing);
+  set(reinterpret_cast<const void*>(coreset_kernel), routing);
+  set(reinterpret_cast<const void*>(constrained_route_kernel), routing);
+  set(reinterpret_cast<const void*>(permute_kernel), routing);
+  set(reinterpret_cast<const void*>(tile_gemm_kernel), 227 * 1024);
+  set(reinterpret_cast<const void*>(ffn_persistent_kernel), 227 * 1024);
   return e;
 }
 
