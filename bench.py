@@ -223,6 +223,8 @@ def main():
             if record:
                 times.append(e0.elapsed_time(e1) * 1e3)
                 cnt = L.desmoe_get_phase_ms(layer.ctx.h, ph, 8)
+                if cnt < 0 or cnt > 8:
+                    raise RuntimeError(L.desmoe_last_error().decode())
                 phases.append([ph[j] * 1e3 for j in range(cnt)])
                 us.append(layer.stats.cpu().numpy().copy())
         return times, phases, us

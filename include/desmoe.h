@@ -196,7 +196,7 @@ int desmoe_set_graphs(desmoe_ctx* ctx, int enable);
  * [2] persistent expert FFN (permutation, gather, gate/up + down GEMMs, fused
  * combine). desmoe_get_phase_ms synchronises on the last event and writes up
  * to max_phases elapsed times (ms) of the LAST call; returns the number
- * written. */
+ * written, or minus a DESMOE_E* code on failure. */
 int desmoe_set_profiling(desmoe_ctx* ctx, int enable);
 int desmoe_get_phase_ms(desmoe_ctx* ctx, float* ms_out, int max_phases);
 /* Kernels launched by the last desmoe_layer_forward call. */

@@ -619,7 +619,9 @@ namespace {
 void mark(desmoe_ctx* c, cudaStream_t st) {
   if (!c->profiling || c->n_ev >= 8) return;
   if (!c->ev[c->n_ev]) cudaEventCreate(&c->ev[c->n_ev]);
-  cudaEventRecord(c->ev[c->n_ev], st);
+  // External: inside a stream capture this becomes a real event-record node
+  // (a plain record would only mark a capture dependency)
+  cudaEventRecordWithFlags(c->ev[c->n_ev], st, cudaEventRecordExternal);
   c->n_ev++;
 }
 
@@ -880,12 +882,16 @@ int desmoe_set_profiling(desmoe_ctx* c, int enable) {
 }
 
 int desmoe_get_phase_ms(desmoe_ctx* c, float* ms, int max_phases) {
-  if (!c || !ms) return fail(DESMOE_EINVAL, "null argument");
+  if (!c || !ms) return -fail(DESMOE_EINVAL, "null argument");
   if (c->n_ev < 2) return 0;
-  DESMOE_CUDA(cudaEventSynchronize(c->ev[c->n_ev - 1]));
+  cudaError_t e = cudaEventSynchronize(c->ev[c->n_ev - 1]);
   int w = 0;
-  for (int i = 0; i + 1 < c->n_ev && w < max_phases; ++i, ++w)
-    DESMOE_CUDA(cudaEventElapsedTime(&ms[w], c->ev[i], c->ev[i + 1]));
+  for (int i = 0; e == cudaSuccess && i + 1 < c->n_ev && w < max_phases; ++i, ++w)
+    e = cudaEventElapsedTime(&ms[w], c->ev[i], c->ev[i + 1]);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return -fail(DESMOE_ECUDA, std::string("phase timing: ") + cudaGetErrorString(e));
+  }
   return w;
 }
 
