@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -194,6 +195,7 @@ int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
   c->max_m = max_experts;
   c->max_k = max_top_k;
   c->max_d = max_hidden;
+  if (const char* g = std::getenv("DESMOE_GRAPHS")) c->use_graphs = std::atoi(g) != 0;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   const size_t nm = static_cast<size_t>(max_tokens) * max_experts;
   const size_t nk = static_cast<size_t>(max_tokens) * max_top_k;
