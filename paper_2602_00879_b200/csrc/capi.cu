@@ -623,7 +623,12 @@ void mark(desmoe_ctx* c, cudaStream_t st) {
   if (!c->ev[c->n_ev]) cudaEventCreate(&c->ev[c->n_ev]);
   // External: inside a stream capture this becomes a real event-record node
   // (a plain record would only mark a capture dependency)
-  cudaEventRecordWithFlags(c->ev[c->n_ev], st, cudaEventRecordExternal);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(c->ev[c->n_ev], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(c->ev[c->n_ev], st);
   c->n_ev++;
 }
 
