@@ -201,6 +201,13 @@ int desmoe_set_profiling(desmoe_ctx* ctx, int enable);
 int desmoe_get_phase_ms(desmoe_ctx* ctx, float* ms_out, int max_phases);
 /* Kernels launched by the last desmoe_layer_forward call. */
 int desmoe_last_launch_count(desmoe_ctx* ctx);
+/* Timeline tracing of the persistent expert-FFN kernel (profiling aid):
+ * buf_dev[0] is an append cursor (zero it before a call), followed by
+ * `capacity` records of two u64 {unit<<32 | cta<<8 | event, globaltimer ns};
+ * events 0 start, 1 gather done, 2 unit dequeued, 3 unit epilogue done,
+ * 5 CTA exit, 6 activations ready, 7 H ready. capacity 0 disables. Takes
+ * effect on the next (re)captured launch sequence. */
+int desmoe_set_trace(desmoe_ctx* ctx, uint64_t* buf_dev, int capacity);
 
 #ifdef __cplusplus
 }

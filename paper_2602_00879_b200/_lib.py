@@ -60,6 +60,7 @@ _SIGS = {
     "desmoe_set_graphs": (_I, [_P, _I]),
     "desmoe_get_phase_ms": (_I, [_P, C.POINTER(C.c_float), _I]),
     "desmoe_last_launch_count": (_I, [_P]),
+    "desmoe_set_trace": (_I, [_P, _P, _I]),
 }
 
 _lib = None

@@ -143,6 +143,8 @@ struct desmoe_ctx {
   cudaEvent_t ev[8] = {};
   int n_ev = 0;
   int launches = 0;
+  uint64_t* trace = nullptr;  // optional FFN timeline buffer (device)
+  int trace_cap = 0;
   const void* wr_map_ptr = nullptr;
   int wr_map_m = -1, wr_map_d = -1;
   CUtensorMap wr_map{};
@@ -677,8 +679,10 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.counters = ex->counters;
   a.stats = stats;
   a.n_members = n_members;
+  a.trace = c->trace;
+  a.trace_cap = c->trace_cap;
   const int stage_bytes = 2 * kATile + 2 * a.b_rows * 128;
-  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
+  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8 + 16) + 16 + 32 + 16 + 48 +
                     4 * (4 + n + 3 * m + 3 * n * k) + 64;
   int stages = (kSmemLimit - fixed) / stage_bytes;
   stages = std::max(2, std::min(stages, 8));
@@ -885,6 +889,7 @@ int desmoe_set_graphs(desmoe_ctx* c, int enable) {
 int desmoe_set_profiling(desmoe_ctx* c, int enable) {
   if (!c) return fail(DESMOE_EINVAL, "null context");
   c->profiling = enable != 0;
+  c->gkey.ex = nullptr;  // force a re-capture
   return DESMOE_OK;
 }
 
@@ -903,6 +908,14 @@ int desmoe_get_phase_ms(desmoe_ctx* c, float* ms, int max_phases) {
 }
 
 int desmoe_last_launch_count(desmoe_ctx* c) { return c ? c->launches : 0; }
+
+int desmoe_set_trace(desmoe_ctx* c, uint64_t* buf_dev, int capacity) {
+  if (!c) return fail(DESMOE_EINVAL, "null context");
+  c->trace = capacity > 0 ? buf_dev : nullptr;
+  c->trace_cap = capacity > 0 ? capacity : 0;
+  c->gkey.ex = nullptr;  // force a re-capture
+  return DESMOE_OK;
+}
 
 int desmoe_layer_forward_host(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
                               const void* x_host, int n, const desmoe_route_cfg* cfg,

@@ -21,7 +21,10 @@
 // Warp roles (256 threads): warp 0 = scheduler + TMA producer, warp 1 = MMA
 // issuer (one elected lane, tcgen05.mma kind::f16, swap-AB: 128 weight rows
 // x N tokens, N = tokens of the expert rounded to 16), warp 2 = TMEM
-// allocator, warps 4-7 = epilogue (tcgen05.ld of TMEM lane quarters 0-3).
+// allocator, then gather, then combine worker; warp 3 = combine worker;
+// warps 4-7 = epilogue (tcgen05.ld of TMEM lane quarters 0-3). The gather and
+// the combine run on their own warps so neither delays the weight stream nor
+// the TMEM drain.
 // Shared-memory ring stages hold two 128x64 bf16 weight tiles (32 KB: gate +
 // up in phase A, two consecutive K blocks of W_d in phase B) and two
 // activation boxes, all SWIZZLE_128B as TMA writes them.
@@ -34,6 +37,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kQ = 4;  // unit queue depth
+constexpr int kC = 8;  // combine queue depth
 
 struct Tables {
   int* count;      // [m]
@@ -76,6 +80,24 @@ __device__ inline int box_for(int count) {
 }
 
 __device__ inline float silu(float g) { return g / (1.0f + expf(-g)); }
+
+__device__ inline uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Optional timeline trace: records {unit<<32 | cta<<8 | event, globaltimer ns}.
+__device__ inline void trace(uint64_t* buf, int cap, int event, int unit) {
+  if (!buf) return;
+  unsigned long long* cur = reinterpret_cast<unsigned long long*>(buf);
+  const unsigned long long i = atomicAdd(cur, 1ull);
+  if (i < static_cast<unsigned long long>(cap)) {
+    buf[2 + 2 * i] = (static_cast<uint64_t>(static_cast<uint32_t>(unit)) << 32) |
+                     (static_cast<uint64_t>(blockIdx.x) << 8) | static_cast<uint64_t>(event);
+    buf[3 + 2 * i] = gtime();
+  }
+}
 
 // Block-wide exclusive scan of v[0..n) (n <= 4 * kThreads) in place; returns total.
 __device__ int block_exclusive_scan(int* v, int n, int* warp_sums) {
@@ -132,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_tok = a.n_tok, k = a.top_k, m = a.m, d = a.d, f = a.f;
+  if (tid == 0) trace(a.trace, a.trace_cap, 0, -1);
   const bool swiglu = a.mode == 0;
   const int S = a.stages;
   const int b_box_bytes = a.b_rows * 128;
@@ -146,8 +169,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;  // [2]
   uint64_t* qfull = tempty + 2;  // [kQ]
   uint64_t* qempty = qfull + kQ; // [kQ]
-  int* unit_q = reinterpret_cast<int*>(qempty + kQ);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_q + kQ);
+  uint64_t* cfull = qempty + kQ; // [kC] combine queue
+  uint64_t* cempty = cfull + kC; // [kC]
+  int* unit_q = reinterpret_cast<int*>(cempty + kC);
+  int* comb_q = unit_q + kQ;     // [kC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(comb_q + kC);
   int* warp_sums = reinterpret_cast<int*>(tmem_slot + 4);  // [9]
   Tables t;
   t.scalars = warp_sums + 12;  // [4 + n_tok]
@@ -225,21 +251,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     a.stats[2] = total_slots;
     a.stats[3] = 0;
   }
-  // gather this CTA's share of token rows into x_perm (16-byte vectors)
-  {
-    const int vec = d / 8;
-    const uint4* src = reinterpret_cast<const uint4*>(a.x);
-    uint4* dst = reinterpret_cast<uint4*>(a.x_perm);
-    for (int s = blockIdx.x; s < total_slots; s += gridDim.x) {
-      const uint4* rs = src + static_cast<size_t>(t.slot_token[s]) * vec;
-      uint4* rd = dst + static_cast<size_t>(s) * vec;
-      for (int i = tid; i < vec; i += kThreads) rd[i] = rs[i];
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) atomic_add_release(x_ready, 1);
-
   // ---- barriers / TMEM ---------------------------------------------------
   const int tilesA = f / kBM, tilesB = d / kBM;
   const int nA = swiglu ? U * tilesA : 0;
@@ -268,6 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&qfull[q], 1);
       mbar_init(&qempty[q], 2);  // MMA lane + epilogue
     }
+    for (int q = 0; q < kC; ++q) {
+      mbar_init(&cfull[q], 1);
+      mbar_init(&cempty[q], 2);  // both combine warps
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -291,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         unit_q[q] = uu;
         mbar_arrive(&qfull[q]);
         if (uu < 0) break;
+        trace(a.trace, a.trace_cap, 2, uu);
         const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
         const int bi = box_for(ui.count);
         const int box_bytes = (16 << bi) * 128;
@@ -319,10 +335,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 while (ld_acquire(x_ready) < static_cast<int>(gridDim.x)) {
                 }
                 x_seen = true;
+                trace(a.trace, a.trace_cap, 6, uu);
               }
             } else {
               while (ld_acquire(&h_ready[ui.expert]) < tilesA) {
               }
+              trace(a.trace, a.trace_cap, 7, uu);
             }
             fence_proxy_async_global();
           }
@@ -390,22 +408,99 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++nunit;
     }
+  } else if (warp == 2 || warp == 3) {
+    // ============ gather (warp 2), then combine workers (warps 2-3) ============
+    if (warp == 2) {
+      const int vec = d / 8;
+      const uint4* src = reinterpret_cast<const uint4*>(a.x);
+      uint4* dst = reinterpret_cast<uint4*>(a.x_perm);
+      const int total_slots = t.scalars[1];
+      for (int s2 = blockIdx.x; s2 < total_slots; s2 += gridDim.x) {
+        const uint4* rs = src + static_cast<size_t>(t.slot_token[s2]) * vec;
+        uint4* rd = dst + static_cast<size_t>(s2) * vec;
+        for (int i = lane; i < vec; i += 32) rd[i] = rs[i];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomic_add_release(x_ready, 1);
+        trace(a.trace, a.trace_cap, 1, -1);
+      }
+    }
+    const int ctid = tid - 64;  // 0..63
+    const int dtiles = d / kBM;
+    int* list_n = t.scalars + 2;
+    int* list = t.scalars + 4;
+    for (int ci = 0;; ++ci) {
+      const int q = ci % kC;
+      mbar_wait(&cfull[q], (ci / kC) & 1);
+      const int uu = comb_q[q];
+      named_bar_sync(2, 64);
+      if (lane == 0) mbar_arrive(&cempty[q]);
+      if (uu < 0) break;
+      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
+      if (ctid == 0) *list_n = 0;
+      named_bar_sync(2, 64);
+      for (int c = ctid; c < ui.count; c += 64) {
+        const int tok = t.slot_token[ui.brow + c];
+        const int old = atomic_add_acq_rel(&tok_done[tok * dtiles + ui.tile], 1);
+        if (old + 1 == a.route_cnt[tok]) list[atomicAdd(list_n, 1)] = tok;
+      }
+      named_bar_sync(2, 64);
+      const int nl = *list_n;
+      // each thread owns rows ctid and ctid+64 of the d tile; all slot loads
+      // of a token are independent and issued together
+      for (int li = 0; li < nl; ++li) {
+        const int tok = list[li];
+        const int cnt = a.route_cnt[tok];
+        const float* base = a.y_slot + ui.tile * kBM + ctid;
+        float acc0 = 0.0f, acc1 = 0.0f;
+        float v0[8], v1[8];
+        for (int j0 = 0; j0 < cnt; j0 += 8) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int jj = j0 + j;
+            if (jj < cnt) {
+              const float* row = base + static_cast<size_t>(t.slot_of[tok * k + jj]) * d;
+              v0[j] = __ldcg(row);
+              v1[j] = __ldcg(row + 64);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j0 + j < cnt) {
+              acc0 += v0[j];
+              acc1 += v1[j];
+            }
+          }
+        }
+        float* out = a.y + static_cast<size_t>(tok) * d + ui.tile * kBM + ctid;
+        out[0] = acc0;
+        out[64] = acc1;
+      }
+      named_bar_sync(2, 64);
+    }
   } else if (warp >= 4) {
     // ============ epilogue ============
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;  // accumulator row = weight row within the tile
     const int etid = tid - 128;    // 0..127
-    const int dtiles = d / kBM;
-    int* list_n = t.scalars + 2;
-    int* list = t.scalars + 4;
-    uint32_t nunit = 0;
+    uint32_t nunit = 0, ncomb = 0;
     for (int qi = 0;; ++qi) {
       const int q = qi % kQ;
       mbar_wait(&qfull[q], (qi / kQ) & 1);
       const int uu = unit_q[q];
       named_bar_sync(1, 128);
       if (etid == 0) mbar_arrive(&qempty[q]);
-      if (uu < 0) break;
+      if (uu < 0) {
+        if (etid == 0) {
+          const int cq = ncomb % kC;
+          mbar_wait(&cempty[cq], ((ncomb / kC) & 1) ^ 1);
+          comb_q[cq] = -1;
+          mbar_arrive(&cfull[cq]);
+        }
+        break;
+      }
       const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
@@ -444,37 +539,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-      __threadfence();
       named_bar_sync(1, 128);
-      if (phaseA) {
-        if (etid == 0) atomic_add_release(&h_ready[ui.expert], 1);
-      } else {
-        // fused combine: the last unit to finish (token, d tile) sums it
-        if (etid == 0) *list_n = 0;
-        named_bar_sync(1, 128);
-        for (int c = etid; c < ui.count; c += 128) {
-          const int tok = t.slot_token[ui.brow + c];
-          const int old = atomic_add_acq_rel(&tok_done[tok * dtiles + ui.tile], 1);
-          if (old + 1 == a.route_cnt[tok]) list[atomicAdd(list_n, 1)] = tok;
+      if (etid == 0) {
+        __threadfence();  // all epilogue stores (ordered by the barrier) -> gpu scope
+        if (phaseA) {
+          atomic_add_release(&h_ready[ui.expert], 1);
+        } else {
+          const int q = ncomb % kC;
+          mbar_wait(&cempty[q], ((ncomb / kC) & 1) ^ 1);
+          comb_q[q] = uu;
+          mbar_arrive(&cfull[q]);
         }
-        named_bar_sync(1, 128);
-        const int nl = *list_n;
-        for (int li = 0; li < nl; ++li) {
-          const int tok = list[li];
-          const int cnt = a.route_cnt[tok];
-          float acc = 0.0f;
-          for (int j = 0; j < cnt; ++j) {
-            const int slot = t.slot_of[tok * k + j];
-            acc += __ldcg(a.y_slot + static_cast<size_t>(slot) * d + ui.tile * kBM + r);
-          }
-          a.y[static_cast<size_t>(tok) * d + ui.tile * kBM + r] = acc;
-        }
-        named_bar_sync(1, 128);
+        trace(a.trace, a.trace_cap, 3, uu);
       }
+      if (!phaseA) ++ncomb;
       ++nunit;
     }
   }
   __syncthreads();
+  if (tid == 0) trace(a.trace, a.trace_cap, 5, -1);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);

@@ -113,6 +113,8 @@ struct FfnArgs {
   int* counters;             // zeroed: sched, x_ready, h_ready[m], tok_done[n][d/128]
   int* stats;                // optional [4]: U, coreset size, slots, 0
   const int* n_members;      // optional coreset size
+  uint64_t* trace;           // optional timeline buffer ([0] cursor, then pairs)
+  int trace_cap;
 };
 
 inline int ffn_counter_words(int m, int n, int d) { return 2 + m + n * (d / 128); }

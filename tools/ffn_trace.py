@@ -1,0 +1,93 @@
+"""Timeline of the persistent expert-FFN kernel (desmoe_set_trace) for one
+DES MoE layer block: when each SM starts streaming, unit durations, the phase
+A -> B transition, the tail. Usage (GPU box):
+
+    python tools/ffn_trace.py [--config c2] [--strategy vote] [--json out.json]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--strategy", default="vote")
+    ap.add_argument("--json", default="")
+    args = ap.parse_args()
+    import torch
+    from bench import CONFIGS
+    from paper_2602_00879_b200 import _lib, synth
+    from paper_2602_00879_b200.dessim import _ptr
+    from paper_2602_00879_b200.layer import DesMoeLayer, LayerConfig
+
+    cfg = CONFIGS[args.config]
+    n, m, k, d, f = cfg["block"], cfg["experts"], cfg["top_k"], cfg["hidden"], cfg["ffn"]
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000)
+    wr = synth.router_weights(m, d, seed=2000)
+    layer = DesMoeLayer(LayerConfig(m, k, d, f, strategy=args.strategy, vote_beta=cfg["beta"]),
+                        wr, wg, wu, wd)
+    cap = 1 << 14
+    buf = torch.zeros(2 + 2 * cap, dtype=torch.int64, device="cuda")
+    L = _lib.lib()
+    x = synth.hidden_states(n, d, seed=7, rho=cfg["rho"])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        layer.forward(x)
+    L.desmoe_set_trace(layer.ctx.h, _ptr(buf), cap)
+    for _ in range(2):  # second call is the traced one (graph warm)
+        buf.zero_()
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        layer.forward(x)
+        torch.cuda.synchronize()
+    L.desmoe_set_trace(layer.ctx.h, None, 0)
+    raw = buf.cpu().numpy().view(np.uint64)
+    cnt = min(int(raw[0]), cap)
+    rec = raw[2: 2 + 2 * cnt].reshape(cnt, 2)
+    ev = (rec[:, 0] & 0xFF).astype(int)
+    cta = ((rec[:, 0] >> 8) & 0xFFFFFF).astype(int)
+    unit = (rec[:, 0] >> 32).astype(np.int64)
+    unit[unit >= 2 ** 31] -= 2 ** 32
+    t = rec[:, 1].astype(np.int64)
+    t0 = t[ev == 0].min()
+    t = (t - t0) / 1e3  # µs
+    stats = layer.stats.cpu().numpy()
+    U = int(stats[0])
+    tilesA = f // 128
+    nA = U * tilesA
+    out = {"U": U, "units": int((ev == 2).sum()), "records": cnt}
+    out["kernel_span_us"] = float(t[ev == 5].max())
+    out["cta_start_spread_us"] = float(t[ev == 0].max())
+    out["gather_done_us"] = [float(t[ev == 1].min()), float(t[ev == 1].max())]
+    out["first_dequeue_us"] = float(t[ev == 2].min())
+    out["x_ready_seen_us"] = [float(t[ev == 6].min()), float(t[ev == 6].max())] if (ev == 6).any() else None
+    done = {int(u): float(tt) for u, tt, e in zip(unit, t, ev) if e == 3}
+    deq = {int(u): float(tt) for u, tt, e in zip(unit, t, ev) if e == 2}
+    durA = [done[u] - deq[u] for u in deq if u < nA and u in done]
+    durB = [done[u] - deq[u] for u in deq if u >= nA and u in done]
+    out["phaseA_last_done_us"] = max(done[u] for u in done if u < nA) if nA else None
+    out["phaseB_first_dequeue_us"] = min(deq[u] for u in deq if u >= nA)
+    out["last_unit_done_us"] = max(done.values())
+    out["unit_dur_A_us"] = [float(np.min(durA)), float(np.median(durA)), float(np.max(durA))] if durA else None
+    out["unit_dur_B_us"] = [float(np.min(durB)), float(np.median(durB)), float(np.max(durB))]
+    exits = t[ev == 5]
+    out["cta_exit_us"] = [float(exits.min()), float(np.median(exits)), float(exits.max())]
+    hwait = [tt for tt, e in zip(t, ev) if e == 7]
+    out["h_ready_waits"] = len(hwait)
+    per_cta = np.bincount(cta[ev == 2], minlength=int(cta.max()) + 1)
+    out["units_per_cta"] = [int(per_cta.min()), float(per_cta.mean()), int(per_cta.max())]
+    print(json.dumps(out, indent=1))
+    if args.json:
+        json.dump(out, open(args.json, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
