@@ -582,7 +582,7 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
   if (e == cudaSuccess) e = cudaMalloc(&ex->h_perm, slots * f * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ex->y_slot, slots * d * 4);
   if (e == cudaSuccess)
-    e = cudaMalloc(&ex->counters, sizeof(int) * ffn_counter_words(m, c->max_n, d));
+    e = cudaMalloc(&ex->counters, sizeof(int) * ffn_counter_words(m, f));
   if (e != cudaSuccess) {
     desmoe_experts_destroy(ex);
     return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
@@ -658,7 +658,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
              const int* n_members, int* stats, cudaStream_t st) {
   const int m = ex->m, d = ex->d, f = ex->f;
   if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
-  const int words = ffn_counter_words(m, n, d);
+  const int words = ffn_counter_words(m, f);
   DESMOE_CUDA(cudaMemsetAsync(ex->counters, 0, sizeof(int) * words, st));
   FfnArgs a{};
   a.mode = ex->kind == DESMOE_FFN_SWIGLU ? 0 : 1;
@@ -675,15 +675,15 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.x_perm = ex->x_perm;
   a.h_perm = ex->h_perm;
   a.y_slot = ex->y_slot;
-  a.y = y;
+  a.slot_of = c->slot_of;
   a.counters = ex->counters;
   a.stats = stats;
   a.n_members = n_members;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
   const int stage_bytes = 2 * kATile + 2 * a.b_rows * 128;
-  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8 + 16) + 16 + 32 + 16 + 48 +
-                    4 * (4 + n + 3 * m + 3 * n * k) + 64;
+  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
+                    4 * (4 + 3 * m + 3 * n * k) + 64;
   int stages = (kSmemLimit - fixed) / stage_bytes;
   stages = std::max(2, std::min(stages, 8));
   a.stages = stages;
@@ -703,7 +703,19 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   const CUtensorMap& wa = ex->kind == DESMOE_FFN_SWIGLU ? ex->wg : ex->wd;
   DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, wa, ex->wu, ex->wd, ex->xp_maps,
                                  ex->kind == DESMOE_FFN_SWIGLU ? ex->h_maps : ex->xp_maps, a));
-  c->launches += 1;
+  // ordered combine, programmatically serialised behind the FFN kernel
+  cudaLaunchConfig_t cc{};
+  cc.gridDim = dim3((n * (d / 4) + 255) / 256);
+  cc.blockDim = dim3(256);
+  cc.stream = st;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cc.attrs = pdl;
+  cc.numAttrs = 1;
+  DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_slots_kernel, static_cast<const float*>(ex->y_slot),
+                                 static_cast<const int*>(c->slot_of), route_cnt, n, k, d, y));
+  c->launches += 2;
   mark(c, st);
   return DESMOE_OK;
 }

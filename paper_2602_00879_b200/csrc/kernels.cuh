@@ -109,21 +109,25 @@ struct FfnArgs {
   __nv_bfloat16* x_perm;     // [n*k x d]
   __nv_bfloat16* h_perm;     // [n*k x f]
   float* y_slot;             // [n*k x d]
-  float* y;                  // [n x d]
-  int* counters;             // zeroed: sched, x_ready, h_ready[m], tok_done[n][d/128]
+  int* slot_of;              // [n x k] written by CTA 0 for the combine kernel
+  int* counters;             // zeroed: sched, x_ready, h_ready[m][f/128]
   int* stats;                // optional [4]: U, coreset size, slots, 0
   const int* n_members;      // optional coreset size
   uint64_t* trace;           // optional timeline buffer ([0] cursor, then pairs)
   int trace_cap;
 };
 
-inline int ffn_counter_words(int m, int n, int d) { return 2 + m + n * (d / 128); }
+inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 128); }
 
 __global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,
                                       const __grid_constant__ CUtensorMap w_b,
                                       const __grid_constant__ CUtensorMap w_c,
                                       const __grid_constant__ BoxMaps xp_maps,
                                       const __grid_constant__ BoxMaps h_maps, FfnArgs a);
+__global__ void combine_slots_kernel(const float* __restrict__ y_slot,
+                                     const int* __restrict__ slot_of,
+                                     const int* __restrict__ route_cnt, int n, int k, int d,
+                                     float* __restrict__ y);
 
 __global__ void tile_gemm_kernel(const __grid_constant__ CUtensorMap wa,
                                  const __grid_constant__ CUtensorMap wb,
