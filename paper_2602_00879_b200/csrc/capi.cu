@@ -589,8 +589,9 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
   }
   int rc = DESMOE_OK;
   if (kind == DESMOE_FFN_SWIGLU) {
-    rc = make_map(&ex->wg, wg, static_cast<uint64_t>(m) * f, d, kBM);
-    if (!rc) rc = make_map(&ex->wu, wu, static_cast<uint64_t>(m) * f, d, kBM);
+    // phase-A tiles stack 64 gate rows over 64 up rows
+    rc = make_map(&ex->wg, wg, static_cast<uint64_t>(m) * f, d, kBM / 2);
+    if (!rc) rc = make_map(&ex->wu, wu, static_cast<uint64_t>(m) * f, d, kBM / 2);
     if (!rc) rc = make_map(&ex->wd, wd, static_cast<uint64_t>(m) * d, f, kBM);
     if (!rc) rc = make_box_maps(&ex->h_maps, ex->h_perm, slots, f);
   } else {
@@ -683,7 +684,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.trace_cap = c->trace_cap;
   const int stage_bytes = 2 * kATile + 2 * a.b_rows * 128;
   const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
-                    4 * (4 + 3 * m + 3 * n * k) + 64;
+                    4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
   int stages = (kSmemLimit - fixed) / stage_bytes;
   stages = std::max(2, std::min(stages, 8));
   a.stages = stages;

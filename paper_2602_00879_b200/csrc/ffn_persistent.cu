@@ -7,13 +7,16 @@
 //             the count route of moe_latency, analysis.cpp:16-30) in shared
 //             memory and gathers its share of token rows into the
 //             expert-grouped activation buffer x_perm;
-//   phase A   (SwiGLU) units (expert, 128-row F tile): G = W_g.X_e^T and
-//             U = W_u.X_e^T in two TMEM accumulators, H = bf16(silu(G) * U)
-//             written to h_perm; a readiness flag per (expert, F tile);
+//   phase A   (SwiGLU) units (expert, 64-row F tile): one 128-row MMA tile
+//             stacks 64 rows of W_g over the matching 64 rows of W_u, so one
+//             accumulator holds G (TMEM lanes 0-63) and U (lanes 64-127) of
+//             the same 64 F outputs; the epilogue pairs them through shared
+//             memory: H = bf16(silu(G) * U) -> h_perm; one readiness flag per
+//             (expert, F tile). 512 KB units keep the phase-A waves short;
 //   phase B   units (expert, 128-row d tile): Y = W_d.H_e^T (or the linear
 //             expert W.X_e^T) scaled by each slot's gate into y_slot. The
-//             k-loop of a phase-B unit walks F in 128-wide chunks = one phase-A
-//             tile each, and waits only for the chunk it is about to read.
+//             k-loop of a phase-B unit walks F in 128-wide chunks (= two
+//             phase-A tiles) and waits only for the chunk it is about to read.
 // Units are handed out by a global atomic counter (phase A before phase B,
 // expert-major), so every SM streams weights until the queue drains; each
 // active expert's weights are read from HBM exactly once.
@@ -28,8 +31,8 @@
 //   warp 3  activation producer: TMA of the x_perm / h_perm boxes once they
 //           are ready (gather handshake / per-chunk H flags);
 //   warps 4-7 epilogue (tcgen05.ld of TMEM lane quarters 0-3).
-// Ring stages: 32 KB of weights (gate+up tiles in phase A, two consecutive K
-// blocks of W_d in phase B) + two activation boxes, SWIZZLE_128B as TMA
+// Ring stages (both phases): two consecutive 64-wide K blocks of a 128-row
+// weight tile (32 KB) + the two matching activation boxes, SWIZZLE_128B as TMA
 // writes them; each stage's full barrier takes one arrival per producer.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -39,7 +42,8 @@ namespace desmoe {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kQ = 4;  // unit queue depth
+constexpr int kQ = 4;      // unit queue depth
+constexpr int kHalf = 64;  // F rows per phase-A tile (gate and up halves)
 
 struct Tables {
   int* count;       // [m]
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   int* sched = a.counters;
   int* x_ready = a.counters + 1;
-  const int tilesA = f / kBM, tilesB = d / kBM;
+  const int tilesA = f / kHalf, tilesB = d / kBM;
   int* h_ready = a.counters + 2;  // [m][tilesA]
 
   // ---- barrier init / TMEM allocation (independent of the route) ----------
@@ -309,11 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int nA = swiglu ? U * tilesA : 0;
   const int n_units = nA + U * tilesB;
-  const int ksA = d / kBK;                       // phase A k-steps (1 K block each)
-  const int ksB = (swiglu ? f : d) / (2 * kBK);  // phase B k-steps (2 K blocks each)
-  const bool dbuf = a.b_rows <= 128;
-  const uint32_t buf_cols = dbuf ? 256u : 512u;
-  const uint32_t up_off = dbuf ? static_cast<uint32_t>(a.b_rows) : 256u;
+  const int ksA = d / (2 * kBK);                 // k-steps: 2 K blocks each
+  const int ksB = (swiglu ? f : d) / (2 * kBK);
+  float* xchg = reinterpret_cast<float*>(t.slot_gate + n_tok * k);  // [16][64] U exchange
 
   if (warp == 0) {
     // ============ scheduler + weight producer ============
@@ -331,8 +333,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace(a.trace, a.trace_cap, 2, uu);
         const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
         const bool phaseA = ui.phase == 0;
-        const CUtensorMap* wmap = phaseA ? &w_a : (swiglu ? &w_c : &w_a);
-        const int wrow = phaseA ? ui.expert * f + ui.tile * kBM : ui.expert * d + ui.tile * kBM;
         const int ksteps = phaseA ? ksA : ksB;
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int s = it % S;
@@ -340,9 +340,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
           mbar_arrive_expect_tx(&full[s], 2 * kATile);
           if (phaseA) {
-            tma_load_2d(st, &w_a, &full[s], ks * kBK, wrow, pol_w);
-            tma_load_2d(st + kATile, &w_b, &full[s], ks * kBK, wrow, pol_w);
+            // rows 0-63 gate, 64-127 up, for two K blocks
+            const int wrow = ui.expert * f + ui.tile * kHalf;
+            for (int h = 0; h < 2; ++h) {
+              const int kc = (2 * ks + h) * kBK;
+              tma_load_2d(st + h * kATile, &w_a, &full[s], kc, wrow, pol_w);
+              tma_load_2d(st + h * kATile + kATile / 2, &w_b, &full[s], kc, wrow, pol_w);
+            }
           } else {
+            const CUtensorMap* wmap = swiglu ? &w_c : &w_a;
+            const int wrow = ui.expert * d + ui.tile * kBM;
             tma_load_2d(st, wmap, &full[s], 2 * ks * kBK, wrow, pol_w);
             tma_load_2d(st + kATile, wmap, &full[s], (2 * ks + 1) * kBK, wrow, pol_w);
           }
@@ -379,25 +386,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           if (!from_x) {
-            // H columns [128 ks, 128 ks + 128) = phase-A tile ks of this expert
-            const int* flag = &h_ready[ui.expert * tilesA + ks];
-            if (ld_acquire(flag) == 0) {
-              while (ld_acquire(flag) == 0) {
+            // H columns [128 ks, 128 ks + 128) = phase-A tiles 2ks, 2ks+1
+            for (int h = 0; h < 2; ++h) {
+              const int* flag = &h_ready[ui.expert * tilesA + 2 * ks + h];
+              if (ld_acquire(flag) == 0) {
+                while (ld_acquire(flag) == 0) {
+                }
+                trace(a.trace, a.trace_cap, 7, uu);
               }
-              trace(a.trace, a.trace_cap, 7, uu);
             }
             fence_proxy_async_global();
           }
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes + 2 * kATile;
-          if (phaseA) {
-            mbar_arrive_expect_tx(&full[s], box_bytes);
-            tma_load_2d(st, &acts.map[bi], &full[s], ks * kBK, ui.brow, pol_x);
-          } else {
-            mbar_arrive_expect_tx(&full[s], 2 * box_bytes);
-            tma_load_2d(st, &acts.map[bi], &full[s], 2 * ks * kBK, ui.brow, pol_x);
-            tma_load_2d(st + b_box_bytes, &acts.map[bi], &full[s], (2 * ks + 1) * kBK, ui.brow,
-                        pol_x);
-          }
+          mbar_arrive_expect_tx(&full[s], 2 * box_bytes);
+          tma_load_2d(st, &acts.map[bi], &full[s], 2 * ks * kBK, ui.brow, pol_x);
+          tma_load_2d(st + b_box_bytes, &acts.map[bi], &full[s], (2 * ks + 1) * kBK, ui.brow,
+                      pol_x);
         }
       }
     }
@@ -415,11 +419,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
-      const uint32_t buf = dbuf ? (nunit & 1u) : 0u;
-      const uint32_t use = dbuf ? (nunit >> 1) : nunit;
+      const uint32_t buf = nunit & 1u;
+      const uint32_t use = nunit >> 1;
       mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
       tc_fence_after();
-      const uint32_t d_acc = tmem_base + buf * buf_cols;
+      const uint32_t d_acc = tmem_base + buf * 256u;
       const int ksteps = phaseA ? ksA : ksB;
       for (int ks = 0; ks < ksteps; ++ks, ++it) {
         const int s = it % S;
@@ -427,27 +431,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
-          const uint32_t a1 = a0 + kATile;
           const uint32_t b0 = a0 + 2 * kATile;
-          const uint32_t b1 = b0 + b_box_bytes;
-          if (phaseA) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
-              const uint64_t bd = sw128_kmajor_desc(b0 + kk * 32);
-              tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + kk * 32), bd, idesc, acc);
-              tc_mma_bf16(d_acc + up_off, sw128_kmajor_desc(a1 + kk * 32), bd, idesc, acc);
-            }
-          } else {
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
-              tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + kk * 32), sw128_kmajor_desc(b0 + kk * 32),
-                          idesc, (ks > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-              tc_mma_bf16(d_acc, sw128_kmajor_desc(a1 + kk * 32), sw128_kmajor_desc(b1 + kk * 32),
-                          idesc, 1u);
-          }
+              tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + h * kATile + kk * 32),
+                          sw128_kmajor_desc(b0 + h * b_box_bytes + kk * 32), idesc,
+                          (ks > 0 || h > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&empty[s]);
           if (ks == ksteps - 1) tc_commit(&tfull[buf]);
         }
@@ -471,24 +462,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
-      const uint32_t buf = dbuf ? (nunit & 1u) : 0u;
-      const uint32_t use = dbuf ? (nunit >> 1) : nunit;
+      const uint32_t buf = nunit & 1u;
+      const uint32_t use = nunit >> 1;
       mbar_wait(&tfull[buf], use & 1u);
       tc_fence_after();
-      const uint32_t lane_base =
-          tmem_base + buf * buf_cols + (static_cast<uint32_t>(q4 * 32) << 16);
+      const uint32_t lane_base = tmem_base + buf * 256u + (static_cast<uint32_t>(q4 * 32) << 16);
       if (phaseA) {
-        __nv_bfloat16* hrow = a.h_perm + static_cast<size_t>(ui.brow) * f + ui.tile * kBM + r;
+        // lanes 0-63: G, lanes 64-127: U of F columns tile*64 + (r mod 64)
+        const bool is_g = r < kHalf;
+        const int rr = r & (kHalf - 1);
+        __nv_bfloat16* hrow =
+            a.h_perm + static_cast<size_t>(ui.brow) * f + ui.tile * kHalf + rr;
         for (int c0 = 0; c0 < n_mma; c0 += 16) {
-          float g[16], uacc[16];
-          tmem_ld16(lane_base + c0, g);
-          tmem_ld16(lane_base + up_off + c0, uacc);
+          float v[16];
+          tmem_ld16(lane_base + c0, v);
+          if (!is_g) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int col = c0 + j;
-            if (col < ui.count)
-              hrow[static_cast<size_t>(col) * f] = __float2bfloat16_rn(silu(g[j]) * uacc[j]);
+            for (int j = 0; j < 16; ++j) xchg[j * kHalf + rr] = v[j];
           }
+          named_bar_sync(1, 128);
+          if (is_g) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = c0 + j;
+              if (col < ui.count)
+                hrow[static_cast<size_t>(col) * f] =
+                    __float2bfloat16_rn(silu(v[j]) * xchg[j * kHalf + rr]);
+            }
+          }
+          named_bar_sync(1, 128);
         }
       } else {
         float* yrow = a.y_slot + static_cast<size_t>(ui.brow) * d + ui.tile * kBM + r;

@@ -110,14 +110,14 @@ struct FfnArgs {
   __nv_bfloat16* h_perm;     // [n*k x f]
   float* y_slot;             // [n*k x d]
   int* slot_of;              // [n x k] written by CTA 0 for the combine kernel
-  int* counters;             // zeroed: sched, x_ready, h_ready[m][f/128]
+  int* counters;             // zeroed: sched, x_ready, h_ready[m][f/64]
   int* stats;                // optional [4]: U, coreset size, slots, 0
   const int* n_members;      // optional coreset size
   uint64_t* trace;           // optional timeline buffer ([0] cursor, then pairs)
   int trace_cap;
 };
 
-inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 128); }
+inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }
 
 __global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,
                                       const __grid_constant__ CUtensorMap w_b,

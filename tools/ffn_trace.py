@@ -61,7 +61,7 @@ def main():
     t = (t - t0) / 1e3  # µs
     stats = layer.stats.cpu().numpy()
     U = int(stats[0])
-    tilesA = f // 128
+    tilesA = f // 64
     nA = U * tilesA
     out = {"U": U, "units": int((ev == 2).sum()), "records": cnt}
     out["kernel_span_us"] = float(t[ev == 5].max())
