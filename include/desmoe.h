@@ -144,8 +144,9 @@ int desmoe_permute(desmoe_ctx* ctx, const int* route_idx_dev, const int* route_c
                    void* stream);
 
 /* ---- experts (K4) -----------------------------------------------------------
- * Registers device-resident bf16 expert weights (no copy; caller keeps them
- * alive). SWIGLU: w_gate/w_up [experts x ffn x hidden], w_down
+ * Registers device-resident bf16 expert weights: they are packed once into a
+ * context-owned tile-contiguous copy the FFN kernel streams (the caller's
+ * tensors are only read during this call; synchronises). SWIGLU: w_gate/w_up [experts x ffn x hidden], w_down
  * [experts x hidden x ffn]. LINEAR: w_gate = W [experts x hidden x hidden]
  * (ExpertBank::expert_weights layout [out][in], gating.cpp:122-134),
  * w_up = w_down = NULL, ffn = hidden. hidden % 128 == 0, ffn % 128 == 0. */

@@ -75,6 +75,24 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, u
   return DESMOE_OK;
 }
 
+// Packed weights: n_tiles contiguous [128 x 64] bf16 blocks (16 KB each),
+// 3-D view {64 cols, 128 rows, n_tiles}, box = one block, SWIZZLE_128B.
+int make_packed_map(CUtensorMap* map, const void* base, uint64_t n_tiles) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DESMOE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, 128, n_tiles};
+  cuuint64_t strides[2] = {128, 128 * 128};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DESMOE_ECUDA, "cuTensorMapEncodeTiled (packed) failed (" +
+                                                       std::to_string(static_cast<int>(r)) + ")");
+  return DESMOE_OK;
+}
+
 int make_box_maps(BoxMaps* maps, const void* base, uint64_t rows, uint64_t cols) {
   for (int i = 0; i < kMaxBoxes; ++i) {
     int rc = make_map(&maps->map[i], base, rows, cols, 16u << i);
@@ -159,6 +177,8 @@ struct desmoe_experts {
   __nv_bfloat16* h_perm = nullptr;  // [max_n*max_k x f]
   float* y_slot = nullptr;          // [max_n*max_k x d]
   int* counters = nullptr;          // FFN scheduler / readiness counters
+  void* packed_a = nullptr;         // gate/up tiles (SwiGLU)
+  void* packed_b = nullptr;         // W_d / W_lin tiles
 };
 
 extern "C" {
@@ -588,14 +608,44 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
     return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
   }
   int rc = DESMOE_OK;
+  // pack the weights into tile-contiguous blocks (one-time)
+  const size_t b_elems = static_cast<size_t>(m) * d * f;
+  cudaError_t pe = cudaMalloc(&ex->packed_b, b_elems * 2);
+  if (pe == cudaSuccess && kind == DESMOE_FFN_SWIGLU) pe = cudaMalloc(&ex->packed_a, 2 * b_elems * 2);
+  if (pe != cudaSuccess) {
+    desmoe_experts_destroy(ex);
+    return fail(DESMOE_ECUDA, std::string("packed weights: ") + cudaGetErrorString(pe));
+  }
+  cudaStream_t ps = cudaStreamPerThread;
+  pe = cudaDeviceSynchronize();  // the caller's weights may still be in flight on any stream
+  if (pe != cudaSuccess) {
+    desmoe_experts_destroy(ex);
+    return fail(DESMOE_ECUDA, std::string("weight registration: ") + cudaGetErrorString(pe));
+  }
   if (kind == DESMOE_FFN_SWIGLU) {
-    // phase-A tiles stack 64 gate rows over 64 up rows
-    rc = make_map(&ex->wg, wg, static_cast<uint64_t>(m) * f, d, kBM / 2);
-    if (!rc) rc = make_map(&ex->wu, wu, static_cast<uint64_t>(m) * f, d, kBM / 2);
-    if (!rc) rc = make_map(&ex->wd, wd, static_cast<uint64_t>(m) * d, f, kBM);
+    pack_weights_kernel<<<1184, 256, 0, ps>>>(static_cast<const uint4*>(wg),
+                                              static_cast<const uint4*>(wu),
+                                              static_cast<uint4*>(ex->packed_a), m, f, d, 1);
+    pack_weights_kernel<<<1184, 256, 0, ps>>>(static_cast<const uint4*>(wd), nullptr,
+                                              static_cast<uint4*>(ex->packed_b), m, d, f, 0);
+  } else {
+    pack_weights_kernel<<<1184, 256, 0, ps>>>(static_cast<const uint4*>(wg), nullptr,
+                                              static_cast<uint4*>(ex->packed_b), m, d, d, 0);
+  }
+  pe = cudaGetLastError();
+  if (pe == cudaSuccess) pe = cudaStreamSynchronize(ps);
+  if (pe != cudaSuccess) {
+    desmoe_experts_destroy(ex);
+    return fail(DESMOE_ECUDA, std::string("weight packing: ") + cudaGetErrorString(pe));
+  }
+  const uint64_t tiles_b = b_elems / (128 * 64);
+  if (kind == DESMOE_FFN_SWIGLU) {
+    rc = make_packed_map(&ex->wg, ex->packed_a, 2 * tiles_b);
+    ex->wu = ex->wg;
+    if (!rc) rc = make_packed_map(&ex->wd, ex->packed_b, tiles_b);
     if (!rc) rc = make_box_maps(&ex->h_maps, ex->h_perm, slots, f);
   } else {
-    rc = make_map(&ex->wd, wg, static_cast<uint64_t>(m) * d, d, kBM);
+    rc = make_packed_map(&ex->wd, ex->packed_b, tiles_b);
     ex->wg = ex->wd;
     ex->wu = ex->wd;
   }
@@ -614,6 +664,8 @@ void desmoe_experts_destroy(desmoe_experts* ex) {
   if (ex->h_perm) cudaFree(ex->h_perm);
   if (ex->y_slot) cudaFree(ex->y_slot);
   if (ex->counters) cudaFree(ex->counters);
+  if (ex->packed_a) cudaFree(ex->packed_a);
+  if (ex->packed_b) cudaFree(ex->packed_b);
   delete ex;
 }
 
@@ -701,8 +753,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  const CUtensorMap& wa = ex->kind == DESMOE_FFN_SWIGLU ? ex->wg : ex->wd;
-  DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, wa, ex->wu, ex->wd, ex->xp_maps,
+  DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, ex->wg, ex->wu, ex->wd, ex->xp_maps,
                                  ex->kind == DESMOE_FFN_SWIGLU ? ex->h_maps : ex->xp_maps, a));
   // ordered combine, programmatically serialised behind the FFN kernel
   cudaLaunchConfig_t cc{};

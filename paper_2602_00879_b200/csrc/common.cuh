@@ -124,6 +124,17 @@ __device__ inline void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint6
       : "memory");
 }
 
+// 3-D tile load (packed weight tiles): coords (c0, c1, c2)
+__device__ inline void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                   int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+
 // Orders this thread's generic-proxy view (e.g. an acquire of a flag set by a
 // producer CTA) before its subsequent async-proxy (TMA) global reads.
 __device__ inline void fence_proxy_async_global() {

@@ -21,10 +21,15 @@
 // expert-major), so every SM streams weights until the queue drains; each
 // active expert's weights are read from HBM exactly once.
 //
+// Weights are pre-packed at registration (pack_weights_kernel) into
+// tile-contiguous 16 KB blocks [128 rows x 64 K] in (expert, row tile, K block)
+// order — phase-A blocks stack 64 gate rows over the matching 64 up rows — so
+// every unit streams one contiguous HBM region.
+//
 // Warp roles (256 threads):
-//   warp 0  scheduler + weight producer: TMA of the two 128x64 bf16 weight
-//           tiles of every stage; never waits for activations, so the HBM
-//           stream runs ahead as far as the ring allows;
+//   warp 0  scheduler + weight producer: TMA of the two 16 KB weight blocks of
+//           every stage; never waits for activations, so the HBM stream runs
+//           ahead as far as the ring allows;
 //   warp 1  MMA issuer (one elected lane, tcgen05.mma kind::f16, swap-AB:
 //           128 weight rows x N tokens, N = the expert's tokens rounded to 16);
 //   warp 2  TMEM allocator;
@@ -149,9 +154,9 @@ __device__ int block_exclusive_scan(int* v, int n, int* warp_sums) {
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1)
-    ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,   // W_g (A) or W_lin (B)
-                          const __grid_constant__ CUtensorMap w_b,   // W_u (A)
-                          const __grid_constant__ CUtensorMap w_c,   // W_d (B, SwiGLU)
+    ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,   // packed gate/up tiles
+                          const __grid_constant__ CUtensorMap w_b,   // (unused)
+                          const __grid_constant__ CUtensorMap w_c,   // packed W_d / W_lin tiles
                           const __grid_constant__ BoxMaps xp_maps,   // x_perm boxes
                           const __grid_constant__ BoxMaps h_maps,    // h_perm boxes
                           FfnArgs a) {
@@ -198,11 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---- barrier init / TMEM allocation (independent of the route) ----------
   if (tid == 0) {
-    tma_prefetch_desc(&w_a);
-    if (swiglu) {
-      tma_prefetch_desc(&w_b);
-      tma_prefetch_desc(&w_c);
-    }
+    if (swiglu) tma_prefetch_desc(&w_a);
+    tma_prefetch_desc(&w_c);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 2);  // weight producer + activation producer
       mbar_init(&empty[s], 1);
@@ -339,20 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
           mbar_arrive_expect_tx(&full[s], 2 * kATile);
-          if (phaseA) {
-            // rows 0-63 gate, 64-127 up, for two K blocks
-            const int wrow = ui.expert * f + ui.tile * kHalf;
-            for (int h = 0; h < 2; ++h) {
-              const int kc = (2 * ks + h) * kBK;
-              tma_load_2d(st + h * kATile, &w_a, &full[s], kc, wrow, pol_w);
-              tma_load_2d(st + h * kATile + kATile / 2, &w_b, &full[s], kc, wrow, pol_w);
-            }
-          } else {
-            const CUtensorMap* wmap = swiglu ? &w_c : &w_a;
-            const int wrow = ui.expert * d + ui.tile * kBM;
-            tma_load_2d(st, wmap, &full[s], 2 * ks * kBK, wrow, pol_w);
-            tma_load_2d(st + kATile, wmap, &full[s], (2 * ks + 1) * kBK, wrow, pol_w);
-          }
+          // packed weights: tile-contiguous 16 KB blocks in (expert, row tile,
+          // K block) order, so a unit streams one contiguous region
+          const int tile0 = phaseA ? (ui.expert * tilesA + ui.tile) * (2 * ksA) + 2 * ks
+                                   : (ui.expert * tilesB + ui.tile) * (2 * ksB) + 2 * ks;
+          const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
+          tma_load_3d(st, wmap, &full[s], 0, 0, tile0, pol_w);
+          tma_load_3d(st + kATile, wmap, &full[s], 0, 0, tile0 + 1, pol_w);
         }
       }
     }
@@ -524,6 +519,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// Packs row-major bf16 weights into tile-contiguous blocks:
+//   out[((e * row_tiles + rt) * kblocks + kb)][r][c] = src(e, rt, r)[kb * 64 + c]
+// with src row = e * rows_per_expert + rt * rows_per_tile + r for r < rows_per_tile
+// (stacked = 0), or, when stacked, rows 0-63 from src (gate) and 64-127 from
+// src2 (up) at row e * rows_per_expert + rt * 64 + (r mod 64). One thread per
+// 16-byte vector.
+__global__ void pack_weights_kernel(const uint4* __restrict__ src, const uint4* __restrict__ src2,
+                                    uint4* __restrict__ out, int experts, int rows_per_expert,
+                                    int cols, int stacked) {
+  const int row_tiles = stacked ? rows_per_expert / 64 : rows_per_expert / 128;
+  const int kblocks = cols / 64;
+  const size_t total = static_cast<size_t>(experts) * row_tiles * kblocks * 128 * 8;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i & 7);
+    const int r = static_cast<int>((i >> 3) & 127);
+    const size_t tile = i >> 10;
+    const int kb = static_cast<int>(tile % kblocks);
+    const size_t et = tile / kblocks;
+    const int rt = static_cast<int>(et % row_tiles);
+    const int e = static_cast<int>(et / row_tiles);
+    const uint4* base = src;
+    int row;
+    if (stacked) {
+      base = r < 64 ? src : src2;
+      row = e * rows_per_expert + rt * 64 + (r & 63);
+    } else {
+      row = e * rows_per_expert + rt * 128 + r;
+    }
+    out[i] = base[static_cast<size_t>(row) * (cols / 8) + kb * 8 + c8];
   }
 }
 

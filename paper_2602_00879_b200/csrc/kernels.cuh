@@ -124,6 +124,9 @@ __global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,
                                       const __grid_constant__ CUtensorMap w_c,
                                       const __grid_constant__ BoxMaps xp_maps,
                                       const __grid_constant__ BoxMaps h_maps, FfnArgs a);
+__global__ void pack_weights_kernel(const uint4* __restrict__ src, const uint4* __restrict__ src2,
+                                    uint4* __restrict__ out, int experts, int rows_per_expert,
+                                    int cols, int stacked);
 __global__ void combine_slots_kernel(const float* __restrict__ y_slot,
                                      const int* __restrict__ slot_of,
                                      const int* __restrict__ route_cnt, int n, int k, int d,
