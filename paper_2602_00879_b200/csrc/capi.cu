@@ -739,6 +739,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
                     4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
   int stages = (kSmemLimit - fixed) / stage_bytes;
   stages = std::max(2, std::min(stages, 8));
+  if (const char* sv = std::getenv("DESMOE_FFN_STAGES"))  // tuning experiments
+    stages = std::max(2, std::min(stages, std::atoi(sv)));
   a.stages = stages;
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
   if (smem > static_cast<size_t>(kSmemLimit))
