@@ -409,7 +409,8 @@ int check_des_params(const desmoe_route_cfg* cfg) {
 // router's split-K partials (partials != nullptr).
 template <typename T>
 int route_impl(desmoe_ctx* c, const T* logits, const float* partials, int splits, int n,
-               const desmoe_route_cfg* cfg, const desmoe_route_out* out, cudaStream_t st) {
+               const desmoe_route_cfg* cfg, const desmoe_route_out* out, cudaStream_t st,
+               int* zero = nullptr, int zero_words = 0, bool* zeroed = nullptr) {
   const int m = cfg->experts, k = cfg->top_k;
   int rc = check_block(c, n, m);
   if (rc) return rc;
@@ -419,9 +420,54 @@ int route_impl(desmoe_ctx* c, const T* logits, const float* partials, int splits
   int* ridx = out && out->route_idx_dev ? out->route_idx_dev : c->route_idx;
   double* rgate = out && out->route_gate_dev ? out->route_gate_dev : c->route_gate;
   int* rcnt = out && out->route_cnt_dev ? out->route_cnt_dev : c->route_cnt;
+  if (zeroed) *zeroed = false;
+  if (cfg->strategy == DESMOE_VANILLA) {
+    if (k < 1 || k > m) return fail(DESMOE_EINVAL, "top_k out of range");
+  } else {
+    rc = check_des_params(cfg);
+    if (rc) return rc;
+  }
+  const bool want_union = cfg->strategy == DESMOE_VANILLA && out &&
+                          (out->coreset_dev || out->coreset_size_dev);
+  if (!want_union && fused_route_smem(n, m, k) <= static_cast<size_t>(kFusedRouteSmem)) {
+    // whole routing stage in one single-CTA kernel
+    FusedRouteArgs<T> a{};
+    a.logits = logits;
+    a.partials = partials;
+    a.splits = splits;
+    a.logits_out = partials ? c->logits32 : nullptr;
+    a.raw_logits = partials ? reinterpret_cast<const T*>(c->logits32) : logits;
+    a.n = n;
+    a.m = m;
+    a.k = k;
+    a.act = cfg->activation;
+    a.strategy = cfg->strategy;
+    a.seq_k = cfg->seq_k;
+    a.m_core = desmoe_vote_budget(cfg->vote_beta, m);
+    a.raw = cfg->vote_source == DESMOE_VOTE_RAW_LOGITS;
+    a.route_idx = ridx;
+    a.route_gate = rgate;
+    a.route_cnt = rcnt;
+    a.members = out && out->coreset_dev ? out->coreset_dev : c->members;
+    a.n_members = out && out->coreset_size_dev ? out->coreset_size_dev : c->n_members;
+    a.member_flag = c->member_flag;
+    a.votes = out ? out->votes_dev : nullptr;
+    a.probs = out ? out->probs_dev : nullptr;
+    a.zero = zero;
+    a.zero_words = zero_words;
+    a.err = c->err;
+    cudaError_t e = launch_fused_route<T>(a, st);
+    if (e != cudaSuccess)
+      return fail(DESMOE_ECUDA, std::string("fused routing: ") + cudaGetErrorString(e));
+    if (out && out->coreset_size_dev && out->coreset_size_dev != c->n_members &&
+        cfg->strategy != DESMOE_VANILLA) {
+      // the members list already went to out->coreset_dev
+    }
+    if (zeroed) *zeroed = zero != nullptr;
+    return DESMOE_OK;
+  }
   if (cfg->strategy == DESMOE_VANILLA) {
     // topk_route(activate(block), K): gating.cpp:84-87
-    if (k < 1 || k > m) return fail(DESMOE_EINVAL, "top_k out of range");
     rc = launch_gate_topk<T>(c, logits, partials, splits, n, m, k, cfg->activation, 0,
                              out && out->probs_dev ? out->probs_dev : c->probs, k, ridx, rgate,
                              rcnt, st);
@@ -444,8 +490,6 @@ int route_impl(desmoe_ctx* c, const T* logits, const float* partials, int splits
     }
     return DESMOE_OK;
   }
-  rc = check_des_params(cfg);
-  if (rc) return rc;
   rc = launch_gate_topk<T>(c, logits, partials, splits, n, m, k, cfg->activation, 1, c->probs,
                            k, nullptr, nullptr, nullptr, st);
   if (rc) return rc;
@@ -708,11 +752,11 @@ int launch_router_tiles(const CUtensorMap& wa, const BoxMaps& acts, TileArgs a, 
 
 int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
-             const int* n_members, int* stats, cudaStream_t st) {
+             const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false) {
   const int m = ex->m, d = ex->d, f = ex->f;
   if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
   const int words = ffn_counter_words(m, f);
-  DESMOE_CUDA(cudaMemsetAsync(ex->counters, 0, sizeof(int) * words, st));
+  if (!counters_zeroed) DESMOE_CUDA(cudaMemsetAsync(ex->counters, 0, sizeof(int) * words, st));
   FfnArgs a{};
   a.mode = ex->kind == DESMOE_FFN_SWIGLU ? 0 : 1;
   a.n_tok = n;
@@ -750,9 +794,12 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   lc.blockDim = dim3(256);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
+  // one CTA per SM (shared memory > half an SM), so all CTAs become resident
+  // and the x_ready handshake cannot deadlock; launched programmatically
+  // behind the routing kernel so barrier init / TMEM allocation overlap it
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (x_ready handshake)
-  attr[0].val.cooperative = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
   DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, ex->wg, ex->wu, ex->wd, ex->xp_maps,
@@ -874,12 +921,14 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   if (rc) return rc;
   c->launches += 1;
   mark(c, st);
-  rc = route_impl<float>(c, nullptr, c->partials, splits, n, cfg, nullptr, st);
+  bool zeroed = false;
+  rc = route_impl<float>(c, nullptr, c->partials, splits, n, cfg, nullptr, st, ex->counters,
+                         ffn_counter_words(ex->m, ex->f), &zeroed);
   if (rc) return rc;
-  c->launches += cfg->strategy == DESMOE_VANILLA ? 1 : 3;
+  c->launches += zeroed ? 1 : (cfg->strategy == DESMOE_VANILLA ? 1 : 3);
   mark(c, st);
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
-                cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st);
+                cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed);
   if (rc) return rc;
   return DESMOE_OK;
 }

@@ -52,6 +52,56 @@ __device__ inline void warp_argbest(uint64_t& key, int& idx) {
   }
 }
 
+// Returns, for lane j < cnt, the ascending position of `my` among the cnt
+// values held by lanes 0..cnt-1 (values distinct).
+__device__ inline int ascending_rank(int my, int lane, int cnt) {
+  int pos = 0;
+  for (int j = 0; j < cnt; ++j) {
+    int o = __shfl_sync(0xffffffffu, my, j);
+    if (lane < cnt && (o < my)) ++pos;
+  }
+  return pos;
+}
+
+// Per-warp selection of `k` entries of row p[0..m) restricted to `allow`
+// (nullptr = all) in (p desc, index asc) order — the reference's
+// select_top_gates order (gating.cpp:42-71). Rank-ordered result in sel[0..k)
+// (written by every lane). Lane l owns elements l, l+32, ... (m <= 1024).
+__device__ inline void warp_select(const double* p, int m, int k, const uint8_t* allow,
+                                   int* sel) {
+  const int lane = threadIdx.x & 31;
+  uint32_t taken = 0;
+  uint64_t bk = 0;
+  int bi = 0x7fffffff;
+  auto rescan = [&]() {
+    bk = 0;
+    bi = 0x7fffffff;
+    for (int s = 0, i = lane; i < m; ++s, i += 32) {
+      if ((taken >> s) & 1u) continue;
+      if (allow && !allow[i]) continue;
+      const uint64_t kk = order_key(p[i]);
+      if (bi == 0x7fffffff || key_precedes(kk, i, bk, bi)) {
+        bk = kk;
+        bi = i;
+      }
+    }
+  };
+  rescan();
+  for (int r = 0; r < k; ++r) {
+    uint64_t wk = bk;
+    int wi = bi;
+    // lanes without a candidate carry (0, INT_MAX), which never beats a real
+    // candidate (order_key of a finite double is never 0)
+    warp_argbest(wk, wi);
+    sel[r] = wi;
+    if ((wi & 31) == lane) {
+      taken |= 1u << (wi >> 5);
+      rescan();
+    }
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------------------
 // shared-memory addressing / mbarrier
 // ---------------------------------------------------------------------------
@@ -227,6 +277,13 @@ __device__ inline void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue now / wait until the previous kernel's results are visible.
+__device__ inline void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ inline void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ inline bool elect_one() {
   uint32_t pred = 0;

@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  pdl_launch_dependents();  // the combine kernel may launch; it waits for us
+  pdl_wait();               // route + zeroed counters from the routing kernel
 
   // ---- prologue: permutation (redundantly per CTA) ------------------------
   for (int i = tid; i < m; i += kThreads) t.count[i] = 0;

@@ -25,6 +25,33 @@ struct GateTopkArgs {
   int* err;
 };
 
+template <typename T>
+struct FusedRouteArgs {
+  const T* logits;        // [n x m] (splits == 0)
+  const float* partials;  // [splits x n x m] router split-K partials (splits > 0)
+  int splits;
+  float* logits_out;      // fp32 logits written when reducing partials
+  const T* raw_logits;    // raw-logit votes source
+  int n, m, k, act, strategy, seq_k, m_core, raw;
+  int* route_idx;      // [n x k]
+  double* route_gate;  // [n x k]
+  int* route_cnt;      // [n]
+  int* members;        // [m] (optional)
+  int* n_members;      // [1] (optional)
+  uint8_t* member_flag;
+  double* votes;       // [m] (optional)
+  double* probs;       // [n x m] (optional)
+  int* zero;           // words to zero for the next kernel (optional)
+  int zero_words;
+  int* err;
+};
+
+constexpr int kFusedRouteSmem = 200 * 1024;
+size_t fused_route_smem(int n, int m, int k);
+template <typename T>
+cudaError_t launch_fused_route(const FusedRouteArgs<T>& a, cudaStream_t st);
+cudaError_t set_fused_route_smem_limit(int bytes);
+
 struct CoresetArgs {
   int n, m, k, strategy, seq_k, m_core, raw;
   const int* topk_idx;  // [n x k] rank order

@@ -26,57 +26,6 @@ __device__ inline double load_logit(const T* p) {
   return static_cast<double>(*p);
 }
 
-// Inserts `v` at rank position among the lanes: returns for lane j < cnt the
-// ascending position of its value among the cnt values held by lanes 0..cnt-1.
-__device__ inline int ascending_rank(int my, int lane, int cnt) {
-  int pos = 0;
-  for (int j = 0; j < cnt; ++j) {
-    int o = __shfl_sync(0xffffffffu, my, j);
-    if (lane < cnt && (o < my)) ++pos;
-  }
-  return pos;
-}
-
-// Per-warp selection of `k` entries of row p[0..m) restricted to `allow`
-// (nullptr = all) in (p desc, index asc) order. Result (rank order) is
-// written to sel[0..k) (all lanes return). Each lane owns elements
-// lane, lane+32, ...; at most 32 per lane (m <= 1024).
-__device__ inline void warp_select(const double* p, int m, int k, const uint8_t* allow,
-                                   int* sel) {
-  const int lane = threadIdx.x & 31;
-  uint32_t taken = 0;
-  uint64_t bk = 0;
-  int bi = 0x7fffffff;
-  auto rescan = [&]() {
-    bk = 0;
-    bi = 0x7fffffff;
-    for (int s = 0, i = lane; i < m; ++s, i += 32) {
-      if ((taken >> s) & 1u) continue;
-      if (allow && !allow[i]) continue;
-      uint64_t kk = order_key(p[i]);
-      if (bi == 0x7fffffff || key_precedes(kk, i, bk, bi)) {
-        bk = kk;
-        bi = i;
-      }
-    }
-  };
-  rescan();
-  for (int r = 0; r < k; ++r) {
-    uint64_t wk = bk;
-    int wi = bi;
-    // lanes with no candidate carry (0, INT_MAX) which never wins against a
-    // real candidate (keys of real values are never 0: order_key maps the
-    // most negative double to 0x000fffff... > 0 and NaN is excluded).
-    warp_argbest(wk, wi);
-    sel[r] = wi;  // every lane writes the same value
-    if ((wi & 31) == lane) {
-      taken |= 1u << (wi >> 5);
-      rescan();
-    }
-  }
-  __syncwarp();
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -428,7 +377,8 @@ cudaError_t set_kernel_smem_limits() {
   set(reinterpret_cast<const void*>(permute_kernel), routing);
   set(reinterpret_cast<const void*>(tile_gemm_kernel), 227 * 1024);
   set(reinterpret_cast<const void*>(ffn_persistent_kernel), 227 * 1024);
-  return e;
+  const cudaError_t f = set_fused_route_smem_limit(kFusedRouteSmem);
+  return e != cudaSuccess ? e : f;
 }
 
 }  // namespace desmoe
