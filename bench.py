@@ -197,7 +197,6 @@ def main():
     lc = LayerConfig(m, k, d, f, strategy="vote", seq_k=3, vote_beta=cfg["beta"])
     layer = DesMoeLayer(lc, wr, wg, wu, wd)
     L = _lib.lib()
-    L.desmoe_set_profiling(layer.ctx.h, 1)
     total = args.warmup + args.steps
     xs = [synth.hidden_states(n, d, seed=10_000 * (rank + 1) + i, rho=cfg["rho"])
           for i in range(total)]
@@ -207,8 +206,8 @@ def main():
     stream = torch.cuda.current_stream()
     ph = (C.c_float * 8)()
 
-    def run(strategy, steps_list, record=True):
-        times, phases, us = [], [], []
+    def run(strategy, steps_list, record=True, phases=True):
+        times, ph_list, us = [], [], []
         lc.seq_k = 3 if strategy != "seq2" else 2
         strat = "seq" if strategy.startswith("seq") else strategy
         for i, x in steps_list:
@@ -222,12 +221,13 @@ def main():
             e1.synchronize()
             if record:
                 times.append(e0.elapsed_time(e1) * 1e3)
-                cnt = L.desmoe_get_phase_ms(layer.ctx.h, ph, 8)
-                if cnt < 0 or cnt > 8:
-                    raise RuntimeError(L.desmoe_last_error().decode())
-                phases.append([ph[j] * 1e3 for j in range(cnt)])
+                if phases:
+                    cnt = L.desmoe_get_phase_ms(layer.ctx.h, ph, 8)
+                    if cnt < 0 or cnt > 8:
+                        raise RuntimeError(L.desmoe_last_error().decode())
+                    ph_list.append([ph[j] * 1e3 for j in range(cnt)])
                 us.append(layer.stats.cpu().numpy().copy())
-        return times, phases, us
+        return times, ph_list, us
 
     steps = list(enumerate(xs))
     warm, timed = steps[: args.warmup], steps[args.warmup:]
@@ -235,15 +235,24 @@ def main():
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
         for strategy in ("vanilla", "seq3", "seq2", "vote"):
+            # timed pass: only the outer events (no event nodes between kernels,
+            # so the programmatic launches overlap exactly as in production)
+            L.desmoe_set_profiling(layer.ctx.h, 0)
             run(strategy, warm, record=False)
             if strategy == "vote":
                 if ws > 1:
                     torch.distributed.barrier()
                 torch.cuda.synchronize()
-            t, p, s = run(strategy, timed)
+            t, _, s = run(strategy, timed, phases=False)
             torch.cuda.synchronize()
+            # phase pass: CUDA events between the layer's kernels (roofline)
+            L.desmoe_set_profiling(layer.ctx.h, 1)
+            run(strategy, warm[:1], record=False)
+            _, p, _ = run(strategy, timed)
             results[strategy] = (np.array(t), np.array(p), np.array(s))
     clocks = clk.summary()
+    L.desmoe_set_profiling(layer.ctx.h, 0)
+    run("vote", warm[:1], record=False)
     launches = L.desmoe_last_launch_count(layer.ctx.h)
 
     # e2e: host buffers through desmoe_layer_forward_host

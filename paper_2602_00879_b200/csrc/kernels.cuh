@@ -47,6 +47,7 @@ struct FusedRouteArgs {
 };
 
 constexpr int kFusedRouteSmem = 200 * 1024;
+constexpr int kMaxSplits = 32;  // router split-K factor bound
 size_t fused_route_smem(int n, int m, int k);
 template <typename T>
 cudaError_t launch_fused_route(const FusedRouteArgs<T>& a, cudaStream_t st);

@@ -50,9 +50,16 @@ __global__ void __launch_bounds__(1024, 1) fused_route_kernel(FusedRouteArgs<T> 
     for (int i = lane; i < m; i += 32) {
       double x;
       if (a.splits > 0) {
+        // all split partials in flight at once, then summed in split order
+        float v[kMaxSplits];
+#pragma unroll
+        for (int s = 0; s < kMaxSplits; ++s)
+          v[s] = s < a.splits ? __ldcg(&a.partials[(static_cast<size_t>(s) * n + t) * m + i])
+                              : 0.0f;
         float acc = 0.0f;
-        for (int s = 0; s < a.splits; ++s)
-          acc += a.partials[(static_cast<size_t>(s) * n + t) * m + i];
+#pragma unroll
+        for (int s = 0; s < kMaxSplits; ++s)
+          if (s < a.splits) acc += v[s];
         if (a.logits_out) a.logits_out[static_cast<size_t>(t) * m + i] = acc;
         x = static_cast<double>(acc);
       } else {

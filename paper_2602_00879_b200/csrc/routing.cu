@@ -55,9 +55,15 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(GateTopkArgs<T> a) {
   for (int i = lane; i < m; i += 32) {
     double x;
     if (a.splits > 0) {
+      float v[kMaxSplits];
+#pragma unroll
+      for (int s = 0; s < kMaxSplits; ++s)
+        v[s] = s < a.splits ? __ldcg(&a.partials[(static_cast<size_t>(s) * a.n + n) * a.m_pad + i])
+                            : 0.0f;
       float acc = 0.0f;
-      for (int s = 0; s < a.splits; ++s)
-        acc += a.partials[(static_cast<size_t>(s) * a.n + n) * a.m_pad + i];
+#pragma unroll
+      for (int s = 0; s < kMaxSplits; ++s)
+        if (s < a.splits) acc += v[s];
       x = static_cast<double>(acc);
       if (a.logits_out) a.logits_out[static_cast<size_t>(n) * m + i] = acc;
     } else {
