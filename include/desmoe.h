@@ -178,6 +178,10 @@ int desmoe_layer_forward(desmoe_ctx* ctx, const desmoe_experts* ex, const void* 
                          const void* x_dev, int n, const desmoe_route_cfg* cfg, float* y_dev,
                          int* stats_dev, void* stream);
 
+/* The fp32 router logits [n x experts] the last desmoe_layer_forward on this
+ * context routed with (for checking its routing against the reference). */
+int desmoe_layer_logits(desmoe_ctx* ctx, float* logits_dev, int n, int experts, void* stream);
+
 /* Same with HOST buffers: copies x (bf16) in, runs the layer, copies y
  * (fp32) and stats back; synchronises. The end-to-end entry a C/C++ caller
  * without device memory uses. */

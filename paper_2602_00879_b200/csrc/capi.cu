@@ -909,6 +909,76 @@ int desmoe_router_logits(desmoe_ctx* c, const void* x, const void* w_r, int n, i
 
 namespace {
 
+// Router GEMM + routing in one cluster launch (front.cu) when the shape fits:
+// N <= 256 tokens, M <= 256 experts, hidden a multiple of 64 * kFrontCta.
+int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const void* w_r, int n,
+               const desmoe_route_cfg* cfg, cudaStream_t st, bool* used) {
+  *used = false;
+  const int m = cfg->experts, k = cfg->top_k, d = ex->d;
+  if (std::getenv("DESMOE_NO_FRONT")) return DESMOE_OK;
+  if (n > 256 || m > 256 || (d / kBK) % kFrontCta != 0 || d % kBK) return DESMOE_OK;
+  if (cfg->strategy == DESMOE_VANILLA) {
+    if (k < 1 || k > m) return fail(DESMOE_EINVAL, "top_k out of range");
+  } else {
+    int rc = check_des_params(cfg);
+    if (rc) return rc;
+  }
+  if (cfg->activation < 0 || cfg->activation > 2)
+    return fail(DESMOE_EINVAL, "unknown gate activation");
+  const int b_rows = b_rows_for(n);
+  const int kb_cta = (d / kBK) / kFrontCta;
+  const int mt = (m + kBM - 1) / kBM;
+  int stages = std::min(kb_cta, 4);
+  size_t smem = front_smem_bytes(n, m, k, stages, b_rows);
+  while (smem > static_cast<size_t>(kSmemLimit) && stages > 1)
+    smem = front_smem_bytes(n, m, k, --stages, b_rows);
+  if (smem > static_cast<size_t>(kSmemLimit)) return DESMOE_OK;
+  if (x != c->x_map_ptr || n != c->x_map_n || d != c->x_map_d) {
+    int rc = make_box_maps(&c->x_maps, x, n, d);
+    if (rc) return rc;
+    c->x_map_ptr = x;
+    c->x_map_n = n;
+    c->x_map_d = d;
+  }
+  if (w_r != c->wr_map_ptr || m != c->wr_map_m || d != c->wr_map_d) {
+    int rc = make_map(&c->wr_map, w_r, m, d, kBM);
+    if (rc) return rc;
+    c->wr_map_ptr = w_r;
+    c->wr_map_m = m;
+    c->wr_map_d = d;
+  }
+  FrontArgs a{};
+  a.n = n;
+  a.m = m;
+  a.k = k;
+  a.act = cfg->activation;
+  a.strategy = cfg->strategy;
+  a.seq_k = cfg->seq_k;
+  a.m_core = desmoe_vote_budget(cfg->vote_beta, m);
+  a.raw = cfg->vote_source == DESMOE_VOTE_RAW_LOGITS;
+  a.b_rows = b_rows;
+  int bi = 0;
+  while ((16 << bi) < n) ++bi;
+  a.box_index = bi;
+  a.kb_per_cta = kb_cta;
+  a.stages = stages;
+  a.tmem_cols = mt * 256;
+  a.route_idx = c->route_idx;
+  a.route_gate = c->route_gate;
+  a.route_cnt = c->route_cnt;
+  a.members = c->members;
+  a.n_members = c->n_members;
+  a.logits_out = c->logits32;
+  a.zero = ex->counters;
+  a.zero_words = ffn_counter_words(ex->m, ex->f);
+  a.err = c->err;
+  cudaError_t e = launch_front(c->wr_map, c->x_maps, a, smem, st);
+  if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("front kernel: ") + cudaGetErrorString(e));
+  c->launches += 1;
+  *used = true;
+  return DESMOE_OK;
+}
+
 int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
                        int n, const desmoe_route_cfg* cfg, float* y, int* stats,
                        cudaStream_t st) {
@@ -916,16 +986,21 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   c->n_ev = 0;
   c->launches = 0;
   mark(c, st);
-  int splits = 0;
-  rc = router_impl(c, x, w_r, n, cfg->experts, ex->d, &splits, st);
-  if (rc) return rc;
-  c->launches += 1;
-  mark(c, st);
   bool zeroed = false;
-  rc = route_impl<float>(c, nullptr, c->partials, splits, n, cfg, nullptr, st, ex->counters,
-                         ffn_counter_words(ex->m, ex->f), &zeroed);
+  rc = front_impl(c, ex, x, w_r, n, cfg, st, &zeroed);
   if (rc) return rc;
-  c->launches += zeroed ? 1 : (cfg->strategy == DESMOE_VANILLA ? 1 : 3);
+  if (!zeroed) {
+    // shapes outside the cluster kernel's envelope: split-K router + routing kernels
+    int splits = 0;
+    rc = router_impl(c, x, w_r, n, cfg->experts, ex->d, &splits, st);
+    if (rc) return rc;
+    c->launches += 1;
+    mark(c, st);
+    rc = route_impl<float>(c, nullptr, c->partials, splits, n, cfg, nullptr, st, ex->counters,
+                           ffn_counter_words(ex->m, ex->f), &zeroed);
+    if (rc) return rc;
+    c->launches += zeroed ? 1 : (cfg->strategy == DESMOE_VANILLA ? 1 : 3);
+  }
   mark(c, st);
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed);
@@ -992,6 +1067,14 @@ int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_
   DESMOE_CUDA(cudaGraphLaunch(c->gexec, st));
   c->n_ev = c->g_n_ev;
   c->launches = c->g_launches;
+  return DESMOE_OK;
+}
+
+int desmoe_layer_logits(desmoe_ctx* c, float* logits_dev, int n, int experts, void* stream) {
+  int rc = check_block(c, n, experts);
+  if (rc) return rc;
+  DESMOE_CUDA(cudaMemcpyAsync(logits_dev, c->logits32, sizeof(float) * n * experts,
+                              cudaMemcpyDeviceToDevice, S(stream)));
   return DESMOE_OK;
 }
 

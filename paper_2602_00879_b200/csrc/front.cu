@@ -1,0 +1,442 @@
+// K1 + K2 fused: router GEMM and the whole DES routing stage of one block in
+// a single thread-block CLUSTER of kFrontCta CTAs (one per SM):
+//
+//   R  router GEMM, split-K over the cluster: CTA r multiplies W_r[:, K-slice r]
+//      by X[:, K-slice r] on tcgen05 (swap-AB: 128 expert rows x N tokens per
+//      M tile, TMA -> SWIZZLE_128B smem -> TMEM) and parks its fp32 partial
+//      logits [N][M] in its own shared memory;
+//   L  CTA r owns tokens [r*N/C, (r+1)*N/C): it sums each logit over the C
+//      partials in fixed CTA order through distributed shared memory (so the
+//      logits are deterministic), then activation + per-token top-K in fp64
+//      (gating.cpp:10-71), one warp per token;
+//   V  every CTA gathers all tokens' selections over DSMEM and computes the
+//      block coreset redundantly — DES-Vote votes summed over tokens in
+//      ascending order, top floor(beta*M) by (vote desc, index asc)
+//      (des.cpp:65-95), or the DES-Seq union (des.cpp:33-45) — so no further
+//      cluster round is needed;
+//   RR constrained re-route + renormalisation of its own tokens
+//      (des.cpp:97-118); VANILLA stops after L with topk_route's gates.
+// Three cluster barriers in total; every intermediate stays on chip. The
+// kernel also zeroes the expert-FFN scheduler counters and triggers the
+// programmatic launch of the FFN kernel at its start.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace desmoe {
+
+namespace {
+
+__device__ inline uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ inline void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// address of the same shared-memory location in CTA `rank` of the cluster
+__device__ inline uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+
+__device__ inline float ld_dsmem_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ inline int ld_dsmem_s32(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ inline double ld_dsmem_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kFrontThreads, 1)
+    front_kernel(const __grid_constant__ CUtensorMap wr_map, const __grid_constant__ BoxMaps x_maps,
+                 FrontArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int C = kFrontCta;
+  const int n = a.n, m = a.m, k = a.k;
+  const int mt = (m + kBM - 1) / kBM;  // expert (M) tiles
+  const int mw = (m + 31) >> 5;
+  const int b_rows = a.b_rows;        // token box rows (>= n, multiple of 16)
+  const int kb_cta = a.kb_per_cta;    // K blocks of this CTA
+  // ---- shared memory -----------------------------------------------------------
+  // [stage ring: per K block: mt weight tiles (16 KB) + token box] | barriers |
+  // partial[n][m] f32 | prow[own][m] f64 | own topk/p | all topk/p | bits | flags
+  const int stage_bytes = mt * kATile + b_rows * 128;
+  const int S = a.stages;
+  unsigned char* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(S) * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tdone = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
+  float* part = reinterpret_cast<float*>(tmem_slot + 4);                  // [n][m]
+  const int t0 = (n * static_cast<int>(rank)) / C, t1 = (n * (static_cast<int>(rank) + 1)) / C;
+  const int own = t1 - t0;
+  const int own_max = (n + C - 1) / C;  // identical layout in every CTA (DSMEM offsets)
+  double* prow = reinterpret_cast<double*>(part + static_cast<size_t>(n) * m +
+                                           ((n * m) & 1));                // [own_max][m]
+  int* otop = reinterpret_cast<int*>(prow + static_cast<size_t>(own_max) * m);
+  double* otp = reinterpret_cast<double*>(otop + n * k + ((n * k) & 1));  // [n*k] own p / raw
+  int* atop = reinterpret_cast<int*>(otp + n * k);                        // [n][k] all tokens
+  double* atp = reinterpret_cast<double*>(atop + n * k + ((n * k) & 1));  // [n][k]
+  uint32_t* ebits = reinterpret_cast<uint32_t*>(atp + n * k);             // [m][tw]
+  const int tw = (n + 31) >> 5;
+  double* votes = reinterpret_cast<double*>(ebits + m * tw + ((m * tw) & 1));  // [m]
+  uint8_t* flag = reinterpret_cast<uint8_t*>(votes + m);                       // [m]
+  int* wsel_all = reinterpret_cast<int*>(flag + ((m + 15) & ~15));             // [warps][32]
+  __shared__ int warp_tot[kFrontThreads / 32 + 1];
+  __shared__ int s_bad;
+
+  const bool vanilla = a.strategy < 0;
+  const int depth = a.strategy == 0 ? a.seq_k : k;
+
+  // ---- setup -------------------------------------------------------------------
+  if (tid == 0) {
+    tma_prefetch_desc(&wr_map);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tdone, 1);
+    fence_mbar_init();
+    s_bad = 0;
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel's outputs (x) are complete
+  for (int i = tid + static_cast<int>(rank) * kFrontThreads; i < a.zero_words;
+       i += kFrontThreads * C)
+    a.zero[i] = 0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int box = a.box_index;
+  const int n_mma = (n + 15) & ~15;
+  const int kb0 = static_cast<int>(rank) * kb_cta;
+
+  // ---- R: split-K router GEMM ---------------------------------------------------
+  if (warp == 0 && lane == 0) {
+    const uint64_t pol_w = l2_policy_evict_first();
+    const uint64_t pol_x = l2_policy_evict_last();
+    for (int i = 0; i < kb_cta; ++i) {
+      const int s = i % S;
+      mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+      unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
+      mbar_arrive_expect_tx(&full[s], mt * kATile + (16u << box) * 128u);
+      for (int tl = 0; tl < mt; ++tl)
+        tma_load_2d(st + tl * kATile, &wr_map, &full[s], (kb0 + i) * kBK, tl * kBM, pol_w);
+      tma_load_2d(st + mt * kATile, &x_maps.map[box], &full[s], (kb0 + i) * kBK, 0, pol_x);
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
+    for (int i = 0; i < kb_cta; ++i) {
+      const int s = i % S;
+      mbar_wait(&full[s], (i / S) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
+        const uint32_t b0 = a0 + mt * kATile;
+        for (int tl = 0; tl < mt; ++tl)
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            tc_mma_bf16(tmem_base + tl * 256, sw128_kmajor_desc(a0 + tl * kATile + kk * 32),
+                        sw128_kmajor_desc(b0 + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(&empty[s]);
+        if (i == kb_cta - 1) tc_commit(tdone);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // drain TMEM: partial[t][e] for this CTA's K slice
+    mbar_wait(tdone, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    for (int tl = 0; tl < mt; ++tl) {
+      const int e = tl * kBM + r;
+      const uint32_t lb = tmem_base + tl * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      for (int c0 = 0; c0 < n_mma; c0 += 16) {
+        float v[16];
+        tmem_ld16(lb + c0, v);
+        if (e < m) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < n) part[(c0 + j) * m + e] = v[j];
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+  cluster_sync();  // #1: all partials parked
+
+  // ---- L: logit reduction over the cluster + activation + top-K (own tokens) -----
+  uint32_t part_remote[kFrontCta];
+#pragma unroll
+  for (int c = 0; c < kFrontCta; ++c) part_remote[c] = dsmem_addr(part, c);
+  const int nwarps = kFrontThreads / 32;
+  int* wsel = wsel_all + warp * 32;
+  for (int lt = warp; lt < own; lt += nwarps) {
+    const int t = t0 + lt;
+    double* row = prow + static_cast<size_t>(lt) * m;
+    bool bad = false;
+    double mx = -INFINITY;
+    for (int i = lane; i < m; i += 32) {
+      float v[kFrontCta];
+      const uint32_t off = static_cast<uint32_t>((t * m + i) * 4);
+#pragma unroll
+      for (int c = 0; c < kFrontCta; ++c) v[c] = ld_dsmem_f32(part_remote[c] + off);
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kFrontCta; ++c) acc += v[c];
+      if (a.logits_out) a.logits_out[static_cast<size_t>(t) * m + i] = acc;
+      const double x = static_cast<double>(acc);
+      bad |= !isfinite(x);
+      row[i] = x;
+      mx = fmax(mx, x);
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) s_bad = 1;
+      continue;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (a.act == 0) {
+      for (int i = lane; i < m; i += 32) row[i] = exp(row[i] - mx);
+      __syncwarp();
+      double s = 0.0;
+      if (lane == 0)
+        for (int i = 0; i < m; ++i) s += row[i];
+      s = __shfl_sync(0xffffffffu, s, 0);
+      for (int i = lane; i < m; i += 32) row[i] = row[i] / s;
+    } else if (a.act == 1) {
+      for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + exp(-row[i]));
+    }
+    __syncwarp();
+    warp_select(row, m, k, nullptr, wsel);
+    if (vanilla) {
+      const int my = lane < k ? wsel[lane] : 0x7fffffff;
+      const int pos = ascending_rank(my, lane, k);
+      __syncwarp();
+      if (lane < k) wsel[pos] = my;
+      __syncwarp();
+      double ssum = 0.0;
+      if (lane == 0)
+        for (int j = 0; j < k; ++j) ssum += row[wsel[j]];
+      ssum = __shfl_sync(0xffffffffu, ssum, 0);
+      if (lane < k) {
+        const size_t o = static_cast<size_t>(t) * k + lane;
+        a.route_idx[o] = wsel[lane];
+        a.route_gate[o] = row[wsel[lane]] / ssum;
+      }
+      if (lane == 0) a.route_cnt[t] = k;
+    } else if (lane < k) {
+      const int e = wsel[lane];
+      otop[lt * k + lane] = e;
+      // vote value: activated gate, or the raw logit (re-summed in the same order)
+      double val = row[e];
+      if (a.raw) {
+        float v[kFrontCta];
+        const uint32_t off = static_cast<uint32_t>((t * m + e) * 4);
+#pragma unroll
+        for (int c = 0; c < kFrontCta; ++c) v[c] = ld_dsmem_f32(part_remote[c] + off);
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kFrontCta; ++c) acc += v[c];
+        val = static_cast<double>(acc);
+      }
+      otp[lt * k + lane] = val;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (s_bad && tid == 0) atomicOr(a.err, 1);
+  cluster_sync();  // #2: every CTA's selections are visible
+  if (vanilla) {
+    cluster_sync();  // keep partials alive until every CTA finished reading them
+    return;
+  }
+
+  // ---- V: gather all tokens' selections, block coreset (redundant per CTA) --------
+  for (int e = tid; e < n * k; e += kFrontThreads) {
+    const int t = e / k, j = e - t * k;
+    int ow = C - 1;  // owner CTA: largest r with floor(n r / C) <= t
+    while ((n * ow) / C > t) --ow;
+    const int lt = t - (n * ow) / C;
+    atop[e] = ld_dsmem_s32(dsmem_addr(otop + lt * k + j, ow));
+    atp[e] = ld_dsmem_f64(dsmem_addr(otp + lt * k + j, ow));
+  }
+  for (int i = tid; i < m * tw; i += kFrontThreads) ebits[i] = 0;
+  __syncthreads();
+  for (int e = tid; e < n * k; e += kFrontThreads) {
+    const int t = e / k, j = e - t * k;
+    if (j < depth) atomicOr(&ebits[atop[e] * tw + (t >> 5)], 1u << (t & 31));
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += kFrontThreads) {
+    const uint32_t* b = ebits + i * tw;
+    if (a.strategy == 0) {
+      int in = 0;
+      for (int w = 0; w < tw; ++w) in |= b[w] != 0;
+      flag[i] = static_cast<uint8_t>(in);
+    } else {
+      double v = 0.0;  // tokens in ascending order (des.cpp:86-91)
+      for (int w = 0; w < tw; ++w) {
+        uint32_t bits = b[w];
+        while (bits) {
+          const int t = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          for (int j = 0; j < k; ++j)
+            if (atop[t * k + j] == i) {
+              v += atp[t * k + j];
+              break;
+            }
+        }
+      }
+      votes[i] = v;
+      if (a.votes && rank == 0) a.votes[i] = v;
+    }
+  }
+  __syncthreads();
+  if (a.strategy == 1) {
+    for (int i = tid; i < m; i += kFrontThreads) {
+      const uint64_t ki = order_key(votes[i]);
+      int rk = 0;
+      for (int j = 0; j < m; ++j) {
+        const uint64_t kj = order_key(votes[j]);
+        rk += (kj > ki) | ((kj == ki) & (j < i));
+      }
+      flag[i] = static_cast<uint8_t>(rk < a.m_core);
+    }
+    __syncthreads();
+  }
+  int nm = 0;
+  {
+    // ascending member list (block scan over chunks of kFrontThreads experts)
+    int base = 0;
+    for (int c0 = 0; c0 < m; c0 += kFrontThreads) {
+      const int i = c0 + tid;
+      const int f = i < m ? flag[i] : 0;
+      const uint32_t bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) warp_tot[warp] = __popc(bal);
+      __syncthreads();
+      if (tid == 0) {
+        int acc = 0;
+        for (int w = 0; w < nwarps; ++w) {
+          const int c = warp_tot[w];
+          warp_tot[w] = acc;
+          acc += c;
+        }
+        warp_tot[nwarps] = acc;
+      }
+      __syncthreads();
+      if (f && rank == 0 && a.members)
+        a.members[base + warp_tot[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
+      base += warp_tot[nwarps];
+      __syncthreads();
+    }
+    nm = base;
+    if (rank == 0 && tid == 0 && a.n_members) *a.n_members = nm;
+  }
+  const int kk = k < nm ? k : nm;
+
+  // ---- RR: constrained re-route of own tokens -------------------------------------
+  for (int lt = warp; lt < own; lt += nwarps) {
+    const int t = t0 + lt;
+    const double* row = prow + static_cast<size_t>(lt) * m;
+    bool covered = false;
+    if (nm >= k) {
+      const int mine = lane < k ? otop[lt * k + lane] : 0;
+      covered = __all_sync(0xffffffffu, lane >= k || flag[mine]);
+      if (covered && lane < k) wsel[lane] = mine;
+      __syncwarp();
+    }
+    if (!covered) warp_select(row, m, kk, flag, wsel);
+    const int my = lane < kk ? wsel[lane] : 0x7fffffff;
+    const int pos = ascending_rank(my, lane, kk);
+    __syncwarp();
+    if (lane < kk) wsel[pos] = my;
+    __syncwarp();
+    double ssum = 0.0;
+    if (lane == 0)
+      for (int j = 0; j < kk; ++j) ssum += row[wsel[j]];
+    ssum = __shfl_sync(0xffffffffu, ssum, 0);
+    if (lane < k) {
+      const size_t o = static_cast<size_t>(t) * k + lane;
+      const bool in = lane < kk;
+      a.route_idx[o] = in ? wsel[lane] : -1;
+      a.route_gate[o] = in ? row[wsel[lane]] / ssum : 0.0;
+    }
+    if (lane == 0) a.route_cnt[t] = kk;
+    __syncwarp();
+  }
+  cluster_sync();  // #3: no CTA exits while others may still read its shared memory
+}
+
+size_t front_smem_bytes(int n, int m, int k, int stages, int b_rows) {
+  const int mt = (m + kBM - 1) / kBM;
+  const int own = (n + kFrontCta - 1) / kFrontCta;  // own_max
+  const int tw = (n + 31) / 32;
+  size_t b = 1024;                                                     // alignment slack
+  b += static_cast<size_t>(stages) * (mt * kATile + b_rows * 128);      // ring
+  b += 8 * (2 * stages + 1) + 16;                                       // barriers, tmem slot
+  b += static_cast<size_t>(n) * m * 4 + 4;                              // partials
+  b += static_cast<size_t>(own) * m * 8;                                // own p rows
+  b += static_cast<size_t>(n) * k * (4 + 8) * 2 + 16;                   // own + all selections
+  b += static_cast<size_t>(m) * tw * 4 + 4;                             // expert bitmaps
+  b += static_cast<size_t>(m) * 8 + ((m + 15) & ~15);                   // votes, flags
+  b += (kFrontThreads / 32) * 32 * 4;                                   // per-warp scratch
+  return b;
+}
+
+cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,
+                         size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(kFrontCta);
+  lc.blockDim = dim3(kFrontThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kFrontCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 2;
+  return cudaLaunchKernelEx(&lc, front_kernel, wr_map, x_maps, a);
+}
+
+cudaError_t set_front_smem_limit() {
+  return cudaFuncSetAttribute(front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024);
+}
+
+}  // namespace desmoe

@@ -53,6 +53,27 @@ template <typename T>
 cudaError_t launch_fused_route(const FusedRouteArgs<T>& a, cudaStream_t st);
 cudaError_t set_fused_route_smem_limit(int bytes);
 
+// ---- front: router GEMM + routing in one thread-block cluster (front.cu) ----
+constexpr int kFrontCta = 8;        // cluster size (portable maximum)
+constexpr int kFrontThreads = 256;
+
+struct FrontArgs {
+  int n, m, k, act, strategy, seq_k, m_core, raw;
+  int b_rows, box_index, kb_per_cta, stages, tmem_cols;
+  int* route_idx;      // [n x k]
+  double* route_gate;  // [n x k]
+  int* route_cnt;      // [n]
+  int* members;        // [m] (written by cluster rank 0)
+  int* n_members;      // [1]
+  double* votes;       // [m] optional
+  float* logits_out;   // [n x m] optional fp32 logits
+  int* zero;           // FFN counters to zero
+  int zero_words;
+  int* err;
+};
+
+size_t front_smem_bytes(int n, int m, int k, int stages, int b_rows);
+
 struct CoresetArgs {
   int n, m, k, strategy, seq_k, m_core, raw;
   const int* topk_idx;  // [n x k] rank order
@@ -159,6 +180,10 @@ __global__ void combine_slots_kernel(const float* __restrict__ y_slot,
                                      const int* __restrict__ slot_of,
                                      const int* __restrict__ route_cnt, int n, int k, int d,
                                      float* __restrict__ y);
+
+cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,
+                         size_t smem, cudaStream_t st);
+cudaError_t set_front_smem_limit();
 
 __global__ void tile_gemm_kernel(const __grid_constant__ CUtensorMap wa,
                                  const __grid_constant__ CUtensorMap wb,

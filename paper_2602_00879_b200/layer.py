@@ -65,5 +65,12 @@ class DesMoeLayer:
             _stream()))
         return y_host
 
+    def last_logits(self, n):
+        """fp32 router logits [n x M] the last forward() routed with."""
+        import torch
+        out = torch.empty((n, self.cfg.experts), dtype=torch.float32, device="cuda")
+        check(lib().desmoe_layer_logits(self.ctx.h, _ptr(out), n, self.cfg.experts, _stream()))
+        return out
+
     def check(self):
         check(lib().desmoe_check(self.ctx.h, _stream()))

@@ -105,14 +105,16 @@ def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
     y = layer.forward(x)
     torch.cuda.synchronize()
     layer.check()
-    # 1. router logits vs fp64 GEMM of the same bf16 values
+    # 1. router logits (the ones the layer routed with) vs fp64 GEMM of the same
+    #    bf16 values; the standalone router entry point agrees to fp32 rounding
+    lg = layer.last_logits(n).cpu().numpy().astype(np.float64)
+    want_logits = x.float().cpu().numpy().astype(np.float64) @ wr.float().cpu().numpy().astype(np.float64).T
+    assert np.abs(lg - want_logits).max() <= 1e-4
     logits = torch.empty((n, m), dtype=torch.float32, device="cuda")
     _lib.check(_lib.lib().desmoe_router_logits(layer.ctx.h, ds._ptr(x), ds._ptr(wr), n, m, d,
                                                ds._ptr(logits), ds._stream()))
     torch.cuda.synchronize()
-    lg = logits.cpu().numpy().astype(np.float64)
-    want_logits = x.float().cpu().numpy().astype(np.float64) @ wr.float().cpu().numpy().astype(np.float64).T
-    assert np.abs(lg - want_logits).max() <= 1e-4
+    assert np.abs(logits.cpu().numpy() - want_logits).max() <= 1e-4
     # 2. routing from the GPU's logits == reference fed the same logits
     if strategy == "vanilla":
         r = ref.topk_route(lg, 8)
