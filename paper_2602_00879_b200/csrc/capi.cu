@@ -930,9 +930,9 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   const int mt = (m + kBM - 1) / kBM;
   int stages = std::min(kb_cta, 4);
   size_t smem = front_smem_bytes(n, m, k, stages, b_rows);
-  while (smem > static_cast<size_t>(kSmemLimit) && stages > 1)
+  while (smem > static_cast<size_t>(kFrontSmemLimit) && stages > 1)
     smem = front_smem_bytes(n, m, k, --stages, b_rows);
-  if (smem > static_cast<size_t>(kSmemLimit)) return DESMOE_OK;
+  if (smem > static_cast<size_t>(kFrontSmemLimit)) return DESMOE_OK;
   if (x != c->x_map_ptr || n != c->x_map_n || d != c->x_map_d) {
     int rc = make_box_maps(&c->x_maps, x, n, d);
     if (rc) return rc;

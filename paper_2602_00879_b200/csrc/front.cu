@@ -436,7 +436,7 @@ cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const
 
 cudaError_t set_front_smem_limit() {
   return cudaFuncSetAttribute(front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+                              kFrontSmemLimit);
 }
 
 }  // namespace desmoe
