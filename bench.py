@@ -292,7 +292,9 @@ def main():
 
     def summarize(name):
         t, p, s = results[name]
-        ffn = p[:, 2]
+        names = (["router_and_routing", "expert_ffn"] if p.shape[1] == 2
+                 else ["router", "routing", "expert_ffn"])
+        ffn = p[:, -1]
         u = s[:, 0].astype(float)
         gbps = (u * wbytes_per_expert) / (ffn * 1e-6) / 1e9
         return {"us_per_block": round(float(t.mean()), 3),
@@ -300,8 +302,7 @@ def main():
                 "unique_experts": round(float(u.mean()), 2),
                 "coreset": round(float(s[:, 1].mean()), 2),
                 "expert_weight_GBps": round(float(gbps.mean()), 1),
-                "phase_us": {nm: round(float(p[:, j].mean()), 2) for j, nm in enumerate(
-                    ["router", "routing", "expert_ffn"]) if j < p.shape[1]}}
+                "phase_us": {nm: round(float(p[:, j].mean()), 2) for j, nm in enumerate(names)}}
 
     summ = {nm: summarize(nm) for nm in results}
     v, van = summ["vote"], summ["vanilla"]
