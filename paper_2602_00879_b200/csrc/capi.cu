@@ -972,6 +972,8 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.zero = ex->counters;
   a.zero_words = ffn_counter_words(ex->m, ex->f);
   a.err = c->err;
+  a.trace = c->trace;
+  a.trace_cap = c->trace_cap;
   cudaError_t e = launch_front(c->wr_map, c->x_maps, a, smem, st);
   if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("front kernel: ") + cudaGetErrorString(e));
   c->launches += 1;

@@ -278,6 +278,24 @@ __device__ inline void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ inline uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Optional timeline trace: records {unit<<32 | cta<<8 | event, globaltimer ns}.
+__device__ inline void trace(uint64_t* buf, int cap, int event, int unit) {
+  if (!buf) return;
+  unsigned long long* cur = reinterpret_cast<unsigned long long*>(buf);
+  const unsigned long long i = atomicAdd(cur, 1ull);
+  if (i < static_cast<unsigned long long>(cap)) {
+    buf[2 + 2 * i] = (static_cast<uint64_t>(static_cast<uint32_t>(unit)) << 32) |
+                     (static_cast<uint64_t>(blockIdx.x) << 8) | static_cast<uint64_t>(event);
+    buf[3 + 2 * i] = gtime();
+  }
+}
+
 // Programmatic dependent launch: let the next kernel in the stream start its
 // prologue now / wait until the previous kernel's results are visible.
 __device__ inline void pdl_launch_dependents() {

@@ -92,24 +92,6 @@ __device__ inline int box_for(int count) {
 
 __device__ inline float silu(float g) { return g / (1.0f + expf(-g)); }
 
-__device__ inline uint64_t gtime() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Optional timeline trace: records {unit<<32 | cta<<8 | event, globaltimer ns}.
-__device__ inline void trace(uint64_t* buf, int cap, int event, int unit) {
-  if (!buf) return;
-  unsigned long long* cur = reinterpret_cast<unsigned long long*>(buf);
-  const unsigned long long i = atomicAdd(cur, 1ull);
-  if (i < static_cast<unsigned long long>(cap)) {
-    buf[2 + 2 * i] = (static_cast<uint64_t>(static_cast<uint32_t>(unit)) << 32) |
-                     (static_cast<uint64_t>(blockIdx.x) << 8) | static_cast<uint64_t>(event);
-    buf[3 + 2 * i] = gtime();
-  }
-}
-
 // Block-wide exclusive scan of v[0..n) (n <= 4 * kThreads) in place; returns total.
 __device__ int block_exclusive_scan(int* v, int n, int* warp_sums) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   const int depth = a.strategy == 0 ? a.seq_k : k;
 
   // ---- setup -------------------------------------------------------------------
+  if (tid == 0) trace(a.trace, a.trace_cap, 10, static_cast<int>(rank));
   if (tid == 0) {
     tma_prefetch_desc(&wr_map);
     for (int s = 0; s < S; ++s) {
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (tid == 0) trace(a.trace, a.trace_cap, 11, static_cast<int>(rank));
   const int box = a.box_index;
   const int n_mma = (n + 15) & ~15;
   const int kb0 = static_cast<int>(rank) * kb_cta;
@@ -194,7 +196,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, a.tmem_cols);
   }
+  if (tid == 0) trace(a.trace, a.trace_cap, 12, static_cast<int>(rank));
   cluster_sync();  // #1: all partials parked
+  if (tid == 0) trace(a.trace, a.trace_cap, 13, static_cast<int>(rank));
 
   // ---- L: logit reduction over the cluster + activation + top-K (own tokens) -----
   uint32_t part_remote[kFrontCta];
@@ -277,7 +281,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   }
   __syncthreads();
   if (s_bad && tid == 0) atomicOr(a.err, 1);
+  if (tid == 0) trace(a.trace, a.trace_cap, 14, static_cast<int>(rank));
   cluster_sync();  // #2: every CTA's selections are visible
+  if (tid == 0) trace(a.trace, a.trace_cap, 15, static_cast<int>(rank));
   if (vanilla) {
     cluster_sync();  // keep partials alive until every CTA finished reading them
     return;
@@ -365,6 +371,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     if (rank == 0 && tid == 0 && a.n_members) *a.n_members = nm;
   }
   const int kk = k < nm ? k : nm;
+  if (tid == 0) trace(a.trace, a.trace_cap, 16, static_cast<int>(rank));
 
   // ---- RR: constrained re-route of own tokens -------------------------------------
   for (int lt = warp; lt < own; lt += nwarps) {
@@ -396,6 +403,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     if (lane == 0) a.route_cnt[t] = kk;
     __syncwarp();
   }
+  if (tid == 0) trace(a.trace, a.trace_cap, 17, static_cast<int>(rank));
   cluster_sync();  // #3: no CTA exits while others may still read its shared memory
 }
 

@@ -71,6 +71,8 @@ struct FrontArgs {
   int* zero;           // FFN counters to zero
   int zero_words;
   int* err;
+  uint64_t* trace;     // optional timeline (events 10-17)
+  int trace_cap;
 };
 
 size_t front_smem_bytes(int n, int m, int k, int stages, int b_rows);

@@ -57,13 +57,19 @@ def main():
     unit = (rec[:, 0] >> 32).astype(np.int64)
     unit[unit >= 2 ** 31] -= 2 ** 32
     t = rec[:, 1].astype(np.int64)
-    t0 = t[ev == 0].min()
+    t0 = t[ev == 10].min() if (ev == 10).any() else t[ev == 0].min()
     t = (t - t0) / 1e3  # µs
     stats = layer.stats.cpu().numpy()
     U = int(stats[0])
     tilesA = f // 64
     nA = U * tilesA
     out = {"U": U, "units": int((ev == 2).sum()), "records": cnt}
+    names = {10: "front_start", 11: "front_setup_done", 12: "front_router_done",
+             13: "front_sync1", 14: "front_gating_done", 15: "front_sync2",
+             16: "front_coreset_done", 17: "front_reroute_done", 0: "ffn_start"}
+    for e_, nm in names.items():
+        if (ev == e_).any():
+            out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
     out["kernel_span_us"] = float(t[ev == 5].max())
     out["cta_start_spread_us"] = float(t[ev == 0].max())
     out["gather_done_us"] = [float(t[ev == 1].min()), float(t[ev == 1].max())]
