@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ BoxMaps h_maps,    // h_perm boxes
                           FfnArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // align to 1024 B by offsetting the shared array itself, so the compiler
+  // keeps the shared address space (LDS/STS instead of generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_tok = a.n_tok, k = a.top_k, m = a.m, d = a.d, f = a.f;
   if (tid == 0) trace(a.trace, a.trace_cap, 0, -1);

@@ -70,8 +70,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     front_kernel(const __grid_constant__ CUtensorMap wr_map, const __grid_constant__ BoxMaps x_maps,
                  FrontArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // align to 1024 B by offsetting the shared array itself, so the compiler
+  // keeps the shared address space (LDS/STS instead of generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
   const int C = kFrontCta;
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   }
   for (int i = tid; i < m * tw; i += kFrontThreads) ebits[i] = 0;
   __syncthreads();
+  if (tid == 0) trace(a.trace, a.trace_cap, 20, static_cast<int>(rank));
   for (int e = tid; e < n * k; e += kFrontThreads) {
     const int t = e / k, j = e - t * k;
     if (j < depth) atomicOr(&ebits[atop[e] * tw + (t >> 5)], 1u << (t & 31));
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
   }
   __syncthreads();
+  if (tid == 0) trace(a.trace, a.trace_cap, 21, static_cast<int>(rank));
   if (a.strategy == 1) {
     for (int i = tid; i < m; i += kFrontThreads) {
       const uint64_t ki = order_key(votes[i]);
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
     __syncthreads();
   }
+  if (tid == 0) trace(a.trace, a.trace_cap, 22, static_cast<int>(rank));
   int nm = 0;
   {
     // ascending member list (block scan over chunks of kFrontThreads experts)

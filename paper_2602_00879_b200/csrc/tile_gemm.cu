@@ -58,8 +58,9 @@ __global__ void __launch_bounds__(256, 1)
                      const __grid_constant__ BoxMaps acts, TileArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B atoms
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // align to 1024 B by offsetting the shared array itself, so the compiler
+  // keeps the shared address space (LDS/STS instead of generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const Unit unit = decode_unit(a, blockIdx.x);
