@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--strategy", default="vote")
     ap.add_argument("--json", default="")
+    ap.add_argument("--no-flush", action="store_true", help="keep L2 warm before the traced call")
     args = ap.parse_args()
     import torch
     from bench import CONFIGS
@@ -44,7 +45,8 @@ def main():
     L.desmoe_set_trace(layer.ctx.h, _ptr(buf), cap)
     for _ in range(2):  # second call is the traced one (graph warm)
         buf.zero_()
-        flush.fill_(1)
+        if not args.no_flush:
+            flush.fill_(1)
         torch.cuda.synchronize()
         layer.forward(x)
         torch.cuda.synchronize()
