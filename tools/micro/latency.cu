@@ -1,0 +1,69 @@
+// Microbenchmarks (clock64 cycles, one warp) of the routing stage's building
+// blocks on sm_100a: serial fp64 sum, exp(double), fp64 division, warp
+// top-K selection, shuffles, and shared-memory round trips.
+#include <cstdio>
+#include <cstdint>
+#include "../../paper_2602_00879_b200/csrc/common.cuh"
+
+using namespace desmoe;
+
+__global__ void probe(const double* in, long long* out, int m, int k) {
+  __shared__ double row[1024];
+  __shared__ int sel[32];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < m; i += 32) row[i] = in[i];
+  __syncwarp();
+  long long t0 = clock64();
+  double s = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < m; ++i) s += row[i];
+  s = __shfl_sync(0xffffffffu, s, 0);
+  long long t1 = clock64();
+  double e = 0.0;
+  for (int i = lane; i < m; i += 32) e += exp(row[i] - 1.0);
+  e = __shfl_sync(0xffffffffu, e, 0);
+  long long t2 = clock64();
+  double q = 0.0;
+  for (int i = lane; i < m; i += 32) q += row[i] / (s + 3.0);
+  q = __shfl_sync(0xffffffffu, q, 0);
+  long long t3 = clock64();
+  warp_select(row, m, k, nullptr, sel);
+  long long t4 = clock64();
+  uint64_t kk = order_key(row[lane]);
+  int ii = lane;
+  warp_argbest(kk, ii);
+  long long t5 = clock64();
+  float f = 0.f;
+  for (int i = lane; i < m; i += 32) f += expf(static_cast<float>(row[i]));
+  f = __shfl_sync(0xffffffffu, f, 0);
+  long long t6 = clock64();
+  if (lane == 0) {
+    out[0] = t1 - t0;
+    out[1] = t2 - t1;
+    out[2] = t3 - t2;
+    out[3] = t4 - t3;
+    out[4] = t5 - t4;
+    out[5] = t6 - t5;
+    out[6] = static_cast<long long>(s + e + q + sel[0] + ii + f);
+  }
+}
+
+int main() {
+  const int ms[] = {64, 256};
+  double* in;
+  long long* out;
+  cudaMalloc(&in, 1024 * 8);
+  cudaMalloc(&out, 8 * 8);
+  double h[1024];
+  for (int i = 0; i < 1024; ++i) h[i] = 0.001 * ((i * 7919) % 1000) - 0.5;
+  cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+  for (int m : ms) {
+    for (int rep = 0; rep < 3; ++rep) probe<<<1, 32>>>(in, out, m, 8);
+    long long r[8];
+    cudaMemcpy(r, out, sizeof(r), cudaMemcpyDeviceToHost);
+    printf("m=%d cycles: serial_dadd_sum=%lld exp_f64=%lld div_f64=%lld warp_select_k8=%lld "
+           "warp_argbest=%lld expf_f32=%lld\n",
+           m, r[0], r[1], r[2], r[3], r[4], r[5]);
+  }
+  return 0;
+}
