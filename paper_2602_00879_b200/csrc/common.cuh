@@ -102,6 +102,54 @@ __device__ inline void warp_select(const double* p, int m, int k, const uint8_t*
   __syncwarp();
 }
 
+// Fast warp top-k for the routing hot path. Candidates carry a packed 64-bit
+// key: the order-preserving key of the value with its 10 lowest bits replaced
+// by (1023 - index), so ONE unsigned max picks (value desc, index asc) —
+// exactly the reference's order unless two distinct values agree in all but
+// those 10 bits (relative gap < 2^-42). Each round is two 32-bit warp
+// reductions (REDUX) instead of a 5-level 64-bit shuffle tree. Rounds run to
+// `rounds` (>= k; one past a boundary lets the caller see the next key).
+// sel[r] = index of round r (all lanes), keys[r] = its packed key.
+// m <= 1024, rounds <= 32. Lanes own elements lane, lane+32, ...
+__device__ inline uint64_t packed_key(double v, int i) {
+  return (order_key(v) & ~0x3FFull) | static_cast<uint64_t>(1023 - i);
+}
+
+__device__ inline void warp_topk_packed(const double* val, int m, int rounds,
+                                        const uint8_t* allow, int* sel, uint64_t* keys) {
+  const int lane = threadIdx.x & 31;
+  uint32_t taken = 0;
+  auto local_best = [&]() -> uint64_t {
+    uint64_t b = 0;
+    for (int s = 0, i = lane; i < m; ++s, i += 32) {
+      if (((taken >> s) & 1u) || (allow && !allow[i])) continue;
+      const uint64_t kk = packed_key(val[i], i);
+      b = kk > b ? kk : b;
+    }
+    return b;
+  };
+  uint64_t best = local_best();
+  for (int r = 0; r < rounds; ++r) {
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(best >> 32));
+    const uint32_t lo = __reduce_max_sync(
+        0xffffffffu, static_cast<uint32_t>(best >> 32) == hi ? static_cast<uint32_t>(best) : 0u);
+    const uint64_t win = (static_cast<uint64_t>(hi) << 32) | lo;
+    const int idx = 1023 - static_cast<int>(lo & 0x3FFu);
+    if (lane == 0) {
+      sel[r] = win ? idx : -1;
+      keys[r] = win;
+    }
+    if (win && (idx & 31) == lane) {
+      taken |= 1u << (idx >> 5);
+      best = local_best();
+    }
+  }
+  __syncwarp();
+}
+
+// Truncated key of a packed key (drops the index bits).
+__device__ inline uint64_t key_value_part(uint64_t pk) { return pk >> 10; }
+
 // ---------------------------------------------------------------------------
 // shared-memory addressing / mbarrier
 // ---------------------------------------------------------------------------

@@ -21,6 +21,7 @@
 // programmatic launch of the FFN kernel at its start.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "route_common.cuh"
 
 namespace desmoe {
 
@@ -95,17 +96,24 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   const int t0 = (n * static_cast<int>(rank)) / C, t1 = (n * (static_cast<int>(rank) + 1)) / C;
   const int own = t1 - t0;
   const int own_max = (n + C - 1) / C;  // identical layout in every CTA (DSMEM offsets)
+  const int nwarps = kFrontThreads / 32;
   double* prow = reinterpret_cast<double*>(part + static_cast<size_t>(n) * m +
                                            ((n * m) & 1));                // [own_max][m]
-  int* otop = reinterpret_cast<int*>(prow + static_cast<size_t>(own_max) * m);
-  double* otp = reinterpret_cast<double*>(otop + n * k + ((n * k) & 1));  // [n*k] own p / raw
-  int* atop = reinterpret_cast<int*>(otp + n * k);                        // [n][k] all tokens
-  double* atp = reinterpret_cast<double*>(atop + n * k + ((n * k) & 1));  // [n][k]
-  uint32_t* ebits = reinterpret_cast<uint32_t*>(atp + n * k);             // [m][tw]
+  double* psum = prow + static_cast<size_t>(own_max) * m;                 // [own_max] softmax s
+  double* scratch_all = psum + own_max;                                   // [warps][m]
+  double* otp = scratch_all + static_cast<size_t>(nwarps) * m;            // [own_max*k] vote vals
+  double* atp = otp + own_max * k;                                        // [n*k] gathered vals
+  double* slotv = atp + n * k;                                            // [n*k] expert-sorted
+  double* votes = slotv + n * k;                                          // [m]
+  uint64_t* wkey_all = reinterpret_cast<uint64_t*>(votes + m);            // [warps][64]
+  int* otop = reinterpret_cast<int*>(wkey_all + nwarps * 64);             // [own_max*k] rank order
+  int* atop = otop + own_max * k;                                         // [n*k] gathered ids
+  int* ecount = atop + n * k;                                             // [m]
+  int* eoff = ecount + m;                                                 // [m]
   const int tw = (n + 31) >> 5;
-  double* votes = reinterpret_cast<double*>(ebits + m * tw + ((m * tw) & 1));  // [m]
-  uint8_t* flag = reinterpret_cast<uint8_t*>(votes + m);                       // [m]
-  int* wsel_all = reinterpret_cast<int*>(flag + ((m + 15) & ~15));             // [warps][32]
+  uint32_t* ebits = reinterpret_cast<uint32_t*>(eoff + m);                // [m][tw]
+  int* wsel_all = reinterpret_cast<int*>(ebits + m * tw);                 // [warps][64]
+  uint8_t* flag = reinterpret_cast<uint8_t*>(wsel_all + nwarps * 64);     // [m]
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
   __shared__ int s_bad;
 
@@ -205,8 +213,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   uint32_t part_remote[kFrontCta];
 #pragma unroll
   for (int c = 0; c < kFrontCta; ++c) part_remote[c] = dsmem_addr(part, c);
-  const int nwarps = kFrontThreads / 32;
-  int* wsel = wsel_all + warp * 32;
+  int* wsel = wsel_all + warp * 64;
+  uint64_t* wkey = wkey_all + warp * 64;
+  double* scratch = scratch_all + static_cast<size_t>(warp) * m;
   for (int lt = warp; lt < own; lt += nwarps) {
     const int t = t0 + lt;
     double* row = prow + static_cast<size_t>(lt) * m;
@@ -217,7 +226,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       const uint32_t off = static_cast<uint32_t>((t * m + i) * 4);
 #pragma unroll
       for (int c = 0; c < kFrontCta; ++c) v[c] = ld_dsmem_f32(part_remote[c] + off);
-      float acc = 0.0f;
+      float acc = 0.0f;  // fixed cluster order: deterministic logits
 #pragma unroll
       for (int c = 0; c < kFrontCta; ++c) acc += v[c];
       if (a.logits_out) a.logits_out[static_cast<size_t>(t) * m + i] = acc;
@@ -232,51 +241,19 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if (a.act == 0) {
-      for (int i = lane; i < m; i += 32) row[i] = exp(row[i] - mx);
-      __syncwarp();
-      double s = 0.0;
-      if (lane == 0)
-        for (int i = 0; i < m; ++i) s += row[i];
-      s = __shfl_sync(0xffffffffu, s, 0);
-      for (int i = lane; i < m; i += 32) row[i] = row[i] / s;
-    } else if (a.act == 1) {
-      for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + exp(-row[i]));
-    }
-    __syncwarp();
-    warp_select(row, m, k, nullptr, wsel);
+    const double ssum = token_activate(row, m, a.act, mx);
+    if (lane == 0) psum[lt] = ssum;
+    const int cnt = token_select(row, ssum, a.act, m, k, vanilla ? 0 : depth, nullptr, m, wsel,
+                                 wkey, scratch);
     if (vanilla) {
-      const int my = lane < k ? wsel[lane] : 0x7fffffff;
-      const int pos = ascending_rank(my, lane, k);
-      __syncwarp();
-      if (lane < k) wsel[pos] = my;
-      __syncwarp();
-      double ssum = 0.0;
-      if (lane == 0)
-        for (int j = 0; j < k; ++j) ssum += row[wsel[j]];
-      ssum = __shfl_sync(0xffffffffu, ssum, 0);
-      if (lane < k) {
-        const size_t o = static_cast<size_t>(t) * k + lane;
-        a.route_idx[o] = wsel[lane];
-        a.route_gate[o] = row[wsel[lane]] / ssum;
-      }
-      if (lane == 0) a.route_cnt[t] = k;
+      token_write_route(row, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate,
+                        a.route_cnt);
     } else if (lane < k) {
       const int e = wsel[lane];
       otop[lt * k + lane] = e;
-      // vote value: activated gate, or the raw logit (re-summed in the same order)
-      double val = row[e];
-      if (a.raw) {
-        float v[kFrontCta];
-        const uint32_t off = static_cast<uint32_t>((t * m + e) * 4);
-#pragma unroll
-        for (int c = 0; c < kFrontCta; ++c) v[c] = ld_dsmem_f32(part_remote[c] + off);
-        float acc = 0.0f;
-#pragma unroll
-        for (int c = 0; c < kFrontCta; ++c) acc += v[c];
-        val = static_cast<double>(acc);
-      }
-      otp[lt * k + lane] = val;
+      // vote value: the activated gate, or the raw logit (VoteSource::raw_logits)
+      otp[lt * k + lane] = a.raw ? static_cast<double>(a.logits_out[static_cast<size_t>(t) * m + e])
+                                 : p_of(row, ssum, a.act, e);
     }
     __syncwarp();
   }
@@ -290,7 +267,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     return;
   }
 
-  // ---- V: gather all tokens' selections, block coreset (redundant per CTA) --------
+  // ---- V: block coreset, redundantly in every CTA ------------------------------------
+  // gather every token's selections (token order) over DSMEM
   for (int e = tid; e < n * k; e += kFrontThreads) {
     const int t = e / k, j = e - t * k;
     int ow = C - 1;  // owner CTA: largest r with floor(n r / C) <= t
@@ -299,41 +277,65 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     atop[e] = ld_dsmem_s32(dsmem_addr(otop + lt * k + j, ow));
     atp[e] = ld_dsmem_f64(dsmem_addr(otp + lt * k + j, ow));
   }
+  for (int i = tid; i < m; i += kFrontThreads) ecount[i] = 0;
   for (int i = tid; i < m * tw; i += kFrontThreads) ebits[i] = 0;
   __syncthreads();
   if (tid == 0) trace(a.trace, a.trace_cap, 20, static_cast<int>(rank));
+  // per-expert token sets of the first `depth` selections
   for (int e = tid; e < n * k; e += kFrontThreads) {
     const int t = e / k, j = e - t * k;
-    if (j < depth) atomicOr(&ebits[atop[e] * tw + (t >> 5)], 1u << (t & 31));
-  }
-  __syncthreads();
-  for (int i = tid; i < m; i += kFrontThreads) {
-    const uint32_t* b = ebits + i * tw;
-    if (a.strategy == 0) {
-      int in = 0;
-      for (int w = 0; w < tw; ++w) in |= b[w] != 0;
-      flag[i] = static_cast<uint8_t>(in);
-    } else {
-      double v = 0.0;  // tokens in ascending order (des.cpp:86-91)
-      for (int w = 0; w < tw; ++w) {
-        uint32_t bits = b[w];
-        while (bits) {
-          const int t = w * 32 + __ffs(bits) - 1;
-          bits &= bits - 1;
-          for (int j = 0; j < k; ++j)
-            if (atop[t * k + j] == i) {
-              v += atp[t * k + j];
-              break;
-            }
-        }
-      }
-      votes[i] = v;
-      if (a.votes && rank == 0) a.votes[i] = v;
+    if (j < depth) {
+      atomicOr(&ebits[atop[e] * tw + (t >> 5)], 1u << (t & 31));
+      atomicAdd(&ecount[atop[e]], 1);
     }
   }
   __syncthreads();
-  if (tid == 0) trace(a.trace, a.trace_cap, 21, static_cast<int>(rank));
   if (a.strategy == 1) {
+    // counting sort of the (token, expert) selections by expert, tokens kept
+    // ascending inside each expert, then one ordered sum per expert
+    for (int i = tid; i < m; i += kFrontThreads) eoff[i] = ecount[i];
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan over experts (m <= 1024: 32 per lane)
+      const int per = (m + 31) / 32;
+      int loc = 0;
+      for (int q = 0; q < per; ++q) {
+        const int i = lane * per + q;
+        if (i < m) loc += eoff[i];
+      }
+      int incl = loc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      int base = incl - loc;
+      for (int q = 0; q < per; ++q) {
+        const int i = lane * per + q;
+        if (i < m) {
+          const int c = eoff[i];
+          eoff[i] = base;
+          base += c;
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < n * k; e += kFrontThreads) {
+      const int t = e / k, x = atop[e];
+      const uint32_t* b = ebits + x * tw;
+      int before = 0;
+      for (int w = 0; w < (t >> 5); ++w) before += __popc(b[w]);
+      before += __popc(b[t >> 5] & ((1u << (t & 31)) - 1u));
+      slotv[eoff[x] + before] = atp[e];
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += kFrontThreads) {
+      double v = 0.0;  // tokens in ascending order (des.cpp:86-91)
+      for (int q = eoff[i], qe = eoff[i] + ecount[i]; q < qe; ++q) v += slotv[q];
+      votes[i] = v;
+      if (a.votes && rank == 0) a.votes[i] = v;
+    }
+    __syncthreads();
+    if (tid == 0) trace(a.trace, a.trace_cap, 21, static_cast<int>(rank));
     for (int i = tid; i < m; i += kFrontThreads) {
       const uint64_t ki = order_key(votes[i]);
       int rk = 0;
@@ -343,8 +345,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       }
       flag[i] = static_cast<uint8_t>(rk < a.m_core);
     }
-    __syncthreads();
+  } else {
+    for (int i = tid; i < m; i += kFrontThreads) flag[i] = static_cast<uint8_t>(ecount[i] > 0);
   }
+  __syncthreads();
   if (tid == 0) trace(a.trace, a.trace_cap, 22, static_cast<int>(rank));
   int nm = 0;
   {
@@ -374,13 +378,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     nm = base;
     if (rank == 0 && tid == 0 && a.n_members) *a.n_members = nm;
   }
-  const int kk = k < nm ? k : nm;
   if (tid == 0) trace(a.trace, a.trace_cap, 16, static_cast<int>(rank));
 
   // ---- RR: constrained re-route of own tokens -------------------------------------
   for (int lt = warp; lt < own; lt += nwarps) {
     const int t = t0 + lt;
     const double* row = prow + static_cast<size_t>(lt) * m;
+    const double ssum = psum[lt];
     bool covered = false;
     if (nm >= k) {
       const int mine = lane < k ? otop[lt * k + lane] : 0;
@@ -388,24 +392,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       if (covered && lane < k) wsel[lane] = mine;
       __syncwarp();
     }
-    if (!covered) warp_select(row, m, kk, flag, wsel);
-    const int my = lane < kk ? wsel[lane] : 0x7fffffff;
-    const int pos = ascending_rank(my, lane, kk);
-    __syncwarp();
-    if (lane < kk) wsel[pos] = my;
-    __syncwarp();
-    double ssum = 0.0;
-    if (lane == 0)
-      for (int j = 0; j < kk; ++j) ssum += row[wsel[j]];
-    ssum = __shfl_sync(0xffffffffu, ssum, 0);
-    if (lane < k) {
-      const size_t o = static_cast<size_t>(t) * k + lane;
-      const bool in = lane < kk;
-      a.route_idx[o] = in ? wsel[lane] : -1;
-      a.route_gate[o] = in ? row[wsel[lane]] / ssum : 0.0;
-    }
-    if (lane == 0) a.route_cnt[t] = kk;
-    __syncwarp();
+    int cnt = k < nm ? k : nm;
+    if (!covered) cnt = token_select(row, ssum, a.act, m, k, 0, flag, nm, wsel, wkey, scratch);
+    token_write_route(row, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate, a.route_cnt);
   }
   if (tid == 0) trace(a.trace, a.trace_cap, 17, static_cast<int>(rank));
   cluster_sync();  // #3: no CTA exits while others may still read its shared memory
@@ -415,15 +404,18 @@ size_t front_smem_bytes(int n, int m, int k, int stages, int b_rows) {
   const int mt = (m + kBM - 1) / kBM;
   const int own = (n + kFrontCta - 1) / kFrontCta;  // own_max
   const int tw = (n + 31) / 32;
+  const int nw = kFrontThreads / 32;
   size_t b = 1024;                                                     // alignment slack
   b += static_cast<size_t>(stages) * (mt * kATile + b_rows * 128);      // ring
   b += 8 * (2 * stages + 1) + 16;                                       // barriers, tmem slot
   b += static_cast<size_t>(n) * m * 4 + 4;                              // partials
-  b += static_cast<size_t>(own) * m * 8;                                // own p rows
-  b += static_cast<size_t>(n) * k * (4 + 8) * 2 + 16;                   // own + all selections
-  b += static_cast<size_t>(m) * tw * 4 + 4;                             // expert bitmaps
-  b += static_cast<size_t>(m) * 8 + ((m + 15) & ~15);                   // votes, flags
-  b += (kFrontThreads / 32) * 32 * 4;                                   // per-warp scratch
+  b += static_cast<size_t>(own) * m * 8 + own * 8;                      // own rows + sums
+  b += static_cast<size_t>(nw) * m * 8;                                 // per-warp scratch rows
+  b += static_cast<size_t>(own) * k * 8 + static_cast<size_t>(n) * k * 16;  // vote values
+  b += static_cast<size_t>(m) * 8 + nw * 64 * 8;                        // votes, keys
+  b += static_cast<size_t>(own) * k * 4 + static_cast<size_t>(n) * k * 4;   // selections
+  b += static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;   // counts, offsets, bitmaps
+  b += nw * 64 * 4 + static_cast<size_t>(m) + 16;                       // warp sel, flags
   return b;
 }
 
