@@ -69,7 +69,9 @@ def main():
     names = {10: "front_start", 11: "front_setup_done", 12: "front_router_done",
              13: "front_sync1", 14: "front_gating_done", 15: "front_sync2",
              16: "front_coreset_done", 17: "front_reroute_done", 0: "ffn_start",
-             20: "front_V_gathered", 21: "front_V_votes", 22: "front_V_ranked"}
+             20: "front_V_gathered", 21: "front_V_votes", 22: "front_V_ranked",
+             33: "L_tok0_start", 30: "L_tok0_loaded", 31: "L_tok0_activated",
+             32: "L_tok0_selected"}
     for e_, nm in names.items():
         if (ev == e_).any():
             out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]

@@ -48,7 +48,9 @@ __global__ void probe(const double* in, long long* out, int m, int k) {
   }
 }
 
+int main2();
 int main() {
+  main2();
   const int ms[] = {64, 256};
   double* in;
   long long* out;
@@ -65,5 +67,50 @@ int main() {
            "warp_argbest=%lld expf_f32=%lld\n",
            m, r[0], r[1], r[2], r[3], r[4], r[5]);
   }
+  return 0;
+}
+
+// CTA-level probes: barrier, smem atomics, global atomic round trip, globaltimer.
+__global__ void probe_cta(unsigned long long* gcnt, long long* out) {
+  __shared__ uint32_t words[64];
+  __shared__ int cnt[64];
+  const int tid = threadIdx.x;
+  if (tid < 64) { words[tid] = 0; cnt[tid] = 0; }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < 10; ++i) __syncthreads();
+  long long t1 = clock64();
+  atomicOr(&words[(tid * 7) & 63], 1u << (tid & 31));
+  atomicAdd(&cnt[(tid * 7) & 63], 1);
+  __syncthreads();
+  long long t2 = clock64();
+  if (tid == 0) atomicAdd(gcnt, 1ull);
+  __syncthreads();
+  long long t3 = clock64();
+  uint64_t g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  long long t4 = clock64();
+  do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1)); } while (g1 == g0);
+  long long t5 = clock64();
+  if (tid == 0) {
+    out[0] = (t1 - t0) / 10;
+    out[1] = t2 - t1;
+    out[2] = t3 - t2;
+    out[3] = t5 - t4;
+    out[4] = static_cast<long long>(g1 - g0);
+    out[5] = words[0] + cnt[0];
+  }
+}
+
+int main2() {
+  unsigned long long* g;
+  long long* out;
+  cudaMalloc(&g, 8);
+  cudaMalloc(&out, 64);
+  for (int rep = 0; rep < 3; ++rep) probe_cta<<<1, 256>>>(g, out);
+  long long r[6];
+  cudaMemcpy(r, out, sizeof(r), cudaMemcpyDeviceToHost);
+  printf("cta: syncthreads=%lld smem_atomics+sync=%lld global_atomic+sync=%lld "
+         "globaltimer_tick_cycles=%lld tick_ns=%lld\n", r[0], r[1], r[2], r[3], r[4]);
   return 0;
 }
