@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   for (int lt = warp; lt < own; lt += nwarps) {
     const int t = t0 + lt;
     double* row = prow + static_cast<size_t>(lt) * m;
-    if (lt == 0 && lane == 0) trace(a.trace, a.trace_cap, 33, static_cast<int>(rank));
+    if (lt == 0 && lane == 0)
+      trace(a.trace, a.trace_cap, 33, static_cast<int>(clock64() >> 4));
     bool bad = false;
     double mx = -INFINITY;
     for (int i = lane; i < m; i += 32) {
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     if (lane == 0) psum[lt] = ssum;
     const int cnt = token_select(row, ssum, a.act, m, k, vanilla ? 0 : depth, nullptr, m, wsel,
                                  wkey, scratch);
-    if (tr) trace(a.trace, a.trace_cap, 32, static_cast<int>(rank));
+    if (tr) trace(a.trace, a.trace_cap, 32, static_cast<int>(clock64() >> 4));
     if (vanilla) {
       token_write_route(row, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate,
                         a.route_cnt);

@@ -95,6 +95,13 @@ def main():
     out["h_ready_waits"] = len(hwait)
     per_cta = np.bincount(cta[ev == 2], minlength=int(cta.max()) + 1)
     out["units_per_cta"] = [int(per_cta.min()), float(per_cta.mean()), int(per_cta.max())]
+    # SM clock during the front kernel's gating (events 33 -> 32 carry clock64 >> 4)
+    c33 = {int(c): (int(u), tt) for c, u, tt, e in zip(cta, unit, t, ev) if e == 33}
+    c32 = {int(c): (int(u), tt) for c, u, tt, e in zip(cta, unit, t, ev) if e == 32}
+    mhz = [((c32[c][0] - c33[c][0]) * 16) / ((c32[c][1] - c33[c][1]) * 1e3) * 1e3
+           for c in c33 if c in c32 and c32[c][1] > c33[c][1]]
+    if mhz:
+        out["front_sm_mhz"] = [round(min(mhz), 1), round(max(mhz), 1)]
     print(json.dumps(out, indent=1))
     if args.json:
         json.dump(out, open(args.json, "w"), indent=1)
