@@ -79,12 +79,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   const int C = kFrontCta;
   const int n = a.n, m = a.m, k = a.k;
   const int mt = (m + kBM - 1) / kBM;  // expert (M) tiles
-  const int mw = (m + 31) >> 5;
   const int b_rows = a.b_rows;        // token box rows (>= n, multiple of 16)
   const int kb_cta = a.kb_per_cta;    // K blocks of this CTA
-  // ---- shared memory -----------------------------------------------------------
-  // [stage ring: per K block: mt weight tiles (16 KB) + token box] | barriers |
-  // partial[n][m] f32 | prow[own][m] f64 | own topk/p | all topk/p | bits | flags
+  const int nwarps = kFrontThreads / 32;
+  const int npairs = nwarps / 2;      // one (main, helper) warp pair per token
+  // ---- shared memory (identical layout in every CTA: DSMEM offsets) -------------
   const int stage_bytes = mt * kATile + b_rows * 128;
   const int S = a.stages;
   unsigned char* ring = smem;
@@ -92,35 +91,36 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tdone = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
-  float* part = reinterpret_cast<float*>(tmem_slot + 4);                  // [n][m]
+  float* part = reinterpret_cast<float*>(tmem_slot + 4);                  // [n][m] f32 partial
   const int t0 = (n * static_cast<int>(rank)) / C, t1 = (n * (static_cast<int>(rank) + 1)) / C;
   const int own = t1 - t0;
-  const int own_max = (n + C - 1) / C;  // identical layout in every CTA (DSMEM offsets)
-  const int nwarps = kFrontThreads / 32;
-  double* prow = reinterpret_cast<double*>(part + static_cast<size_t>(n) * m +
-                                           ((n * m) & 1));                // [own_max][m]
-  double* psum = prow + static_cast<size_t>(own_max) * m;                 // [own_max] softmax s
-  double* scratch_all = psum + own_max;                                   // [warps][m]
-  double* otp = scratch_all + static_cast<size_t>(nwarps) * m;            // [own_max*k] vote vals
-  double* atp = otp + own_max * k;                                        // [n*k] gathered vals
-  double* slotv = atp + n * k;                                            // [n*k] expert-sorted
-  double* votes = slotv + n * k;                                          // [m]
-  uint64_t* wkey_all = reinterpret_cast<uint64_t*>(votes + m);            // [warps][64]
-  int* otop = reinterpret_cast<int*>(wkey_all + nwarps * 64);             // [own_max*k] rank order
-  int* atop = otop + own_max * k;                                         // [n*k] gathered ids
-  int* ecount = atop + n * k;                                             // [m]
-  int* eoff = ecount + m;                                                 // [m]
-  const int tw = (n + 31) >> 5;
-  uint32_t* ebits = reinterpret_cast<uint32_t*>(eoff + m);                // [m][tw]
-  int* wsel_all = reinterpret_cast<int*>(ebits + m * tw);                 // [warps][64]
-  uint8_t* flag = reinterpret_cast<uint8_t*>(wsel_all + nwarps * 64);     // [m]
+  const int own_max = (n + C - 1) / C;
+  double* xrow = reinterpret_cast<double*>(part + static_cast<size_t>(n) * m +
+                                           ((n * m) & 1));                // [own_max][m] logits
+  double* erow = xrow + static_cast<size_t>(own_max) * m;                 // [own_max][m] e or p
+  double* psum = erow + static_cast<size_t>(own_max) * m;                 // [own_max] softmax s
+  double* pmx = psum + own_max;                                           // [own_max] row max
+  double* scratch_all = pmx + own_max;                                    // [pairs][m]
+  double* otp = scratch_all + static_cast<size_t>(npairs) * m;            // [own_max*k]
+  double* dense = otp + own_max * k;                                      // [n][m] vote values
+  double* votes = dense + static_cast<size_t>(n) * m;                     // [m]
+  uint64_t* wkey_all = reinterpret_cast<uint64_t*>(votes + m);            // [pairs][64]
+  int* otop = reinterpret_cast<int*>(wkey_all + npairs * 64);             // [own_max*k]
+  int* wsel_all = otop + own_max * k;                                     // [pairs][64]
+  int* rankp = wsel_all + npairs * 64;                                    // [4][m] partial ranks
+  uint8_t* flag = reinterpret_cast<uint8_t*>(rankp + 4 * m);              // [m]
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
   __shared__ int s_bad;
 
   const bool vanilla = a.strategy < 0;
   const int depth = a.strategy == 0 ? a.seq_k : k;
+  const int box = a.box_index;
+  const int n_mma = (n + 15) & ~15;
+  const int kb0 = static_cast<int>(rank) * kb_cta;
+  const uint32_t xbytes = (16u << box) * 128u;
 
-  // ---- setup -------------------------------------------------------------------
+  // ---- setup: barriers, TMEM, router-weight prefetch (weights are static, so
+  // they stream before the previous kernel's output is even waited for) ----------
   if (tid == 0) trace(a.trace, a.trace_cap, 10, static_cast<int>(rank));
   if (tid == 0) {
     tma_prefetch_desc(&wr_map);
@@ -131,10 +131,17 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     mbar_init(tdone, 1);
     fence_mbar_init();
     s_bad = 0;
+    const uint64_t pol_w = l2_policy_evict_first();
+    for (int i = 0; i < kb_cta && i < S; ++i) {
+      unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
+      mbar_arrive_expect_tx(&full[i], mt * kATile + xbytes);
+      for (int tl = 0; tl < mt; ++tl)
+        tma_load_2d(st + tl * kATile, &wr_map, &full[i], (kb0 + i) * kBK, tl * kBM, pol_w);
+    }
   }
   if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
   pdl_launch_dependents();
-  pdl_wait();  // the previous kernel's outputs (x) are complete
+  pdl_wait();  // x (the previous kernel's output) is complete from here on
   for (int i = tid + static_cast<int>(rank) * kFrontThreads; i < a.zero_words;
        i += kFrontThreads * C)
     a.zero[i] = 0;
@@ -143,9 +150,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (tid == 0) trace(a.trace, a.trace_cap, 11, static_cast<int>(rank));
-  const int box = a.box_index;
-  const int n_mma = (n + 15) & ~15;
-  const int kb0 = static_cast<int>(rank) * kb_cta;
 
   // ---- R: split-K router GEMM ---------------------------------------------------
   if (warp == 0 && lane == 0) {
@@ -153,11 +157,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     const uint64_t pol_x = l2_policy_evict_last();
     for (int i = 0; i < kb_cta; ++i) {
       const int s = i % S;
-      mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
       unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
-      mbar_arrive_expect_tx(&full[s], mt * kATile + (16u << box) * 128u);
-      for (int tl = 0; tl < mt; ++tl)
-        tma_load_2d(st + tl * kATile, &wr_map, &full[s], (kb0 + i) * kBK, tl * kBM, pol_w);
+      if (i >= S) {
+        mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], mt * kATile + xbytes);
+        for (int tl = 0; tl < mt; ++tl)
+          tma_load_2d(st + tl * kATile, &wr_map, &full[s], (kb0 + i) * kBK, tl * kBM, pol_w);
+      }
       tma_load_2d(st + mt * kATile, &x_maps.map[box], &full[s], (kb0 + i) * kBK, 0, pol_x);
     }
   } else if (warp == 1) {
@@ -200,6 +206,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
     tc_fence_before();
   }
+  // zero the dense vote matrix while the MMA drains (used only by DES)
+  if (!vanilla)
+    for (int i = tid; i < n * m; i += kFrontThreads) dense[i] = 0.0;
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
@@ -209,59 +218,92 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   cluster_sync();  // #1: all partials parked
   if (tid == 0) trace(a.trace, a.trace_cap, 13, static_cast<int>(rank));
 
-  // ---- L: logit reduction over the cluster + activation + top-K (own tokens) -----
+  // ---- L: logits (cluster reduction) -> activation -> top-K, own tokens ----------
+  // Warp pair per token: the main warp reduces the logits and selects on the
+  // logit order; the helper warp computes e = exp(x - max) and the ordered
+  // softmax sum at the same time. Order by logit == order by probability
+  // except for rounding ties; token_finish_selection() detects those and
+  // re-selects exactly.
+  const int pair = warp >> 1;
+  const bool main_w = (warp & 1) == 0;
+  int* wsel = wsel_all + pair * 64;
+  uint64_t* wkey = wkey_all + pair * 64;
+  double* scratch = scratch_all + static_cast<size_t>(pair) * m;
   uint32_t part_remote[kFrontCta];
 #pragma unroll
   for (int c = 0; c < kFrontCta; ++c) part_remote[c] = dsmem_addr(part, c);
-  int* wsel = wsel_all + warp * 64;
-  uint64_t* wkey = wkey_all + warp * 64;
-  double* scratch = scratch_all + static_cast<size_t>(warp) * m;
-  for (int lt = warp; lt < own; lt += nwarps) {
+  for (int lt = pair; lt < own_max; lt += npairs) {
+    const bool active = lt < own;  // uniform per pair
     const int t = t0 + lt;
-    double* row = prow + static_cast<size_t>(lt) * m;
-    if (lt == 0 && lane == 0)
-      trace(a.trace, a.trace_cap, 33, static_cast<int>(clock64() >> 4));
-    bool bad = false;
-    double mx = -INFINITY;
-    for (int i = lane; i < m; i += 32) {
-      float v[kFrontCta];
-      const uint32_t off = static_cast<uint32_t>((t * m + i) * 4);
+    double* xr = xrow + static_cast<size_t>(lt) * m;
+    double* er = erow + static_cast<size_t>(lt) * m;
+    if (active && main_w) {
+      bool bad = false;
+      double mx = -INFINITY;
+      for (int i = lane; i < m; i += 32) {
+        float v[kFrontCta];
+        const uint32_t off = static_cast<uint32_t>((t * m + i) * 4);
 #pragma unroll
-      for (int c = 0; c < kFrontCta; ++c) v[c] = ld_dsmem_f32(part_remote[c] + off);
-      float acc = 0.0f;  // fixed cluster order: deterministic logits
+        for (int c = 0; c < kFrontCta; ++c) v[c] = ld_dsmem_f32(part_remote[c] + off);
+        float acc = 0.0f;  // fixed cluster order: deterministic logits
 #pragma unroll
-      for (int c = 0; c < kFrontCta; ++c) acc += v[c];
-      if (a.logits_out) a.logits_out[static_cast<size_t>(t) * m + i] = acc;
-      const double x = static_cast<double>(acc);
-      bad |= !isfinite(x);
-      row[i] = x;
-      mx = fmax(mx, x);
-    }
-    if (__any_sync(0xffffffffu, bad)) {
-      if (lane == 0) s_bad = 1;
-      continue;
-    }
-    const bool tr = lt == 0 && lane == 0;
-    if (tr) trace(a.trace, a.trace_cap, 30, static_cast<int>(rank));
+        for (int c = 0; c < kFrontCta; ++c) acc += v[c];
+        if (a.logits_out) a.logits_out[static_cast<size_t>(t) * m + i] = acc;
+        const double x = static_cast<double>(acc);
+        bad |= !isfinite(x);
+        xr[i] = x;
+        mx = fmax(mx, x);
+      }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const double ssum = token_activate(row, m, a.act, mx);
-    if (tr) trace(a.trace, a.trace_cap, 31, static_cast<int>(rank));
-    if (lane == 0) psum[lt] = ssum;
-    const int cnt = token_select(row, ssum, a.act, m, k, vanilla ? 0 : depth, nullptr, m, wsel,
-                                 wkey, scratch);
-    if (tr) trace(a.trace, a.trace_cap, 32, static_cast<int>(clock64() >> 4));
-    if (vanilla) {
-      token_write_route(row, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate,
-                        a.route_cnt);
-    } else if (lane < k) {
-      const int e = wsel[lane];
-      otop[lt * k + lane] = e;
-      // vote value: the activated gate, or the raw logit (VoteSource::raw_logits)
-      otp[lt * k + lane] = a.raw ? static_cast<double>(a.logits_out[static_cast<size_t>(t) * m + e])
-                                 : p_of(row, ssum, a.act, e);
+      for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+      if (lane == 0) pmx[lt] = mx;
     }
-    __syncwarp();
+    named_bar_sync(1 + pair, 64);  // x row + max published to the helper
+    if (active && !main_w) {
+      const double mx = pmx[lt];
+      double ssum = 1.0;
+      if (a.act == 0) {
+        for (int i = lane; i < m; i += 32) er[i] = exp(xr[i] - mx);
+        __syncwarp();
+        ssum = 0.0;
+        if (lane == 0)
+          for (int i = 0; i < m; ++i) ssum += er[i];  // ascending index (gating.cpp:31-33)
+      } else if (a.act == 1) {
+        for (int i = lane; i < m; i += 32) er[i] = 1.0 / (1.0 + exp(-xr[i]));
+      } else {
+        for (int i = lane; i < m; i += 32) er[i] = xr[i];
+      }
+      if (lane == 0) psum[lt] = ssum;
+    } else if (active && main_w) {
+      // softmax: order by logit; sigmoid/identity: order by the probability
+      // itself (the main warp computes it — saturation ties are value ties)
+      const double* key_src = xr;
+      if (a.act != 0) {
+        for (int i = lane; i < m; i += 32)
+          scratch[i] = a.act == 1 ? 1.0 / (1.0 + exp(-xr[i])) : xr[i];
+        __syncwarp();
+        key_src = scratch;
+      }
+      const int rounds = k < m ? k + 1 : k;
+      warp_topk_fast(key_src, m, rounds, nullptr, wsel, wkey);
+    }
+    named_bar_sync(1 + pair, 64);  // e row + sum ready
+    if (active && main_w) {
+      const double ssum = psum[lt];
+      const int cnt = token_finish_selection(xr, er, ssum, pmx[lt], a.act, m, k,
+                                             vanilla ? 0 : depth, nullptr, m, wsel, scratch);
+      if (vanilla) {
+        token_write_route(er, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate,
+                          a.route_cnt);
+      } else if (lane < k) {
+        const int e = wsel[lane];
+        otop[lt * k + lane] = e;
+        // vote value: the activated gate, or the raw logit (VoteSource::raw_logits)
+        otp[lt * k + lane] = a.raw ? xr[e] : p_of(er, ssum, a.act, e);
+      }
+      __syncwarp();
+    }
   }
   __syncthreads();
   if (s_bad && tid == 0) atomicOr(a.err, 1);
@@ -274,85 +316,46 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   }
 
   // ---- V: block coreset, redundantly in every CTA ------------------------------------
-  // gather every token's selections (token order) over DSMEM
+  // scatter every token's selections into the dense [token][expert] vote matrix
   for (int e = tid; e < n * k; e += kFrontThreads) {
     const int t = e / k, j = e - t * k;
+    if (j >= depth) continue;
     int ow = C - 1;  // owner CTA: largest r with floor(n r / C) <= t
     while ((n * ow) / C > t) --ow;
     const int lt = t - (n * ow) / C;
-    atop[e] = ld_dsmem_s32(dsmem_addr(otop + lt * k + j, ow));
-    atp[e] = ld_dsmem_f64(dsmem_addr(otp + lt * k + j, ow));
+    const int x = ld_dsmem_s32(dsmem_addr(otop + lt * k + j, ow));
+    dense[t * m + x] = a.strategy == 1 ? ld_dsmem_f64(dsmem_addr(otp + lt * k + j, ow)) : 1.0;
   }
-  for (int i = tid; i < m; i += kFrontThreads) ecount[i] = 0;
-  for (int i = tid; i < m * tw; i += kFrontThreads) ebits[i] = 0;
   __syncthreads();
   if (tid == 0) trace(a.trace, a.trace_cap, 20, static_cast<int>(rank));
-  // per-expert token sets of the first `depth` selections
-  for (int e = tid; e < n * k; e += kFrontThreads) {
-    const int t = e / k, j = e - t * k;
-    if (j < depth) {
-      atomicOr(&ebits[atop[e] * tw + (t >> 5)], 1u << (t & 31));
-      atomicAdd(&ecount[atop[e]], 1);
-    }
+  for (int i = tid; i < m; i += kFrontThreads) {
+    double v = 0.0;  // every token in ascending order (des.cpp:86-91); +0 is exact
+    for (int t = 0; t < n; ++t) v += dense[t * m + i];
+    votes[i] = v;
+    if (a.votes && rank == 0 && a.strategy == 1) a.votes[i] = v;
   }
   __syncthreads();
+  if (tid == 0) trace(a.trace, a.trace_cap, 21, static_cast<int>(rank));
   if (a.strategy == 1) {
-    // counting sort of the (token, expert) selections by expert, tokens kept
-    // ascending inside each expert, then one ordered sum per expert
-    for (int i = tid; i < m; i += kFrontThreads) eoff[i] = ecount[i];
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan over experts (m <= 1024: 32 per lane)
-      const int per = (m + 31) / 32;
-      int loc = 0;
-      for (int q = 0; q < per; ++q) {
-        const int i = lane * per + q;
-        if (i < m) loc += eoff[i];
-      }
-      int incl = loc;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += o;
-      }
-      int base = incl - loc;
-      for (int q = 0; q < per; ++q) {
-        const int i = lane * per + q;
-        if (i < m) {
-          const int c = eoff[i];
-          eoff[i] = base;
-          base += c;
-        }
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < n * k; e += kFrontThreads) {
-      const int t = e / k, x = atop[e];
-      const uint32_t* b = ebits + x * tw;
-      int before = 0;
-      for (int w = 0; w < (t >> 5); ++w) before += __popc(b[w]);
-      before += __popc(b[t >> 5] & ((1u << (t & 31)) - 1u));
-      slotv[eoff[x] + before] = atp[e];
-    }
-    __syncthreads();
-    for (int i = tid; i < m; i += kFrontThreads) {
-      double v = 0.0;  // tokens in ascending order (des.cpp:86-91)
-      for (int q = eoff[i], qe = eoff[i] + ecount[i]; q < qe; ++q) v += slotv[q];
-      votes[i] = v;
-      if (a.votes && rank == 0) a.votes[i] = v;
-    }
-    __syncthreads();
-    if (tid == 0) trace(a.trace, a.trace_cap, 21, static_cast<int>(rank));
-    for (int i = tid; i < m; i += kFrontThreads) {
+    // rank of expert i = #experts before it in (vote desc, index asc); four
+    // threads per expert each count a quarter of the pool
+    for (int w = tid; w < 4 * m; w += kFrontThreads) {
+      const int i = w % m, part4 = w / m;
       const uint64_t ki = order_key(votes[i]);
       int rk = 0;
-      for (int j = 0; j < m; ++j) {
+      const int j0 = (m * part4) / 4, j1 = (m * (part4 + 1)) / 4;
+      for (int j = j0; j < j1; ++j) {
         const uint64_t kj = order_key(votes[j]);
         rk += (kj > ki) | ((kj == ki) & (j < i));
       }
-      flag[i] = static_cast<uint8_t>(rk < a.m_core);
+      rankp[part4 * m + i] = rk;
     }
+    __syncthreads();
+    for (int i = tid; i < m; i += kFrontThreads)
+      flag[i] = static_cast<uint8_t>(rankp[i] + rankp[m + i] + rankp[2 * m + i] + rankp[3 * m + i] <
+                                     a.m_core);
   } else {
-    for (int i = tid; i < m; i += kFrontThreads) flag[i] = static_cast<uint8_t>(ecount[i] > 0);
+    for (int i = tid; i < m; i += kFrontThreads) flag[i] = static_cast<uint8_t>(votes[i] > 0.0);
   }
   __syncthreads();
   if (tid == 0) trace(a.trace, a.trace_cap, 22, static_cast<int>(rank));
@@ -386,21 +389,36 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   }
   if (tid == 0) trace(a.trace, a.trace_cap, 16, static_cast<int>(rank));
 
-  // ---- RR: constrained re-route of own tokens -------------------------------------
-  for (int lt = warp; lt < own; lt += nwarps) {
-    const int t = t0 + lt;
-    const double* row = prow + static_cast<size_t>(lt) * m;
-    const double ssum = psum[lt];
-    bool covered = false;
-    if (nm >= k) {
-      const int mine = lane < k ? otop[lt * k + lane] : 0;
-      covered = __all_sync(0xffffffffu, lane >= k || flag[mine]);
-      if (covered && lane < k) wsel[lane] = mine;
-      __syncwarp();
+  // ---- RR: constrained re-route of own tokens (main warps) ------------------------
+  if (main_w) {
+    for (int lt = pair; lt < own; lt += npairs) {
+      const int t = t0 + lt;
+      const double* xr = xrow + static_cast<size_t>(lt) * m;
+      const double* er = erow + static_cast<size_t>(lt) * m;
+      const double ssum = psum[lt];
+      bool covered = false;
+      if (nm >= k) {
+        const int mine = lane < k ? otop[lt * k + lane] : 0;
+        covered = __all_sync(0xffffffffu, lane >= k || flag[mine]);
+        if (covered && lane < k) wsel[lane] = mine;
+        __syncwarp();
+      }
+      int cnt = k < nm ? k : nm;
+      if (!covered) {
+        const double* key_src = xr;
+        if (a.act != 0) {
+          for (int i = lane; i < m; i += 32) scratch[i] = er[i];
+          __syncwarp();
+          key_src = scratch;
+        }
+        const int rounds = cnt < nm ? cnt + 1 : cnt;
+        warp_topk_fast(key_src, m, rounds, flag, wsel, wkey);
+        cnt = token_finish_selection(xr, er, ssum, pmx[lt], a.act, m, k, 0, flag, nm, wsel,
+                                     scratch);
+      }
+      token_write_route(er, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate,
+                        a.route_cnt);
     }
-    int cnt = k < nm ? k : nm;
-    if (!covered) cnt = token_select(row, ssum, a.act, m, k, 0, flag, nm, wsel, wkey, scratch);
-    token_write_route(row, ssum, a.act, wsel, cnt, k, t, a.route_idx, a.route_gate, a.route_cnt);
   }
   if (tid == 0) trace(a.trace, a.trace_cap, 17, static_cast<int>(rank));
   cluster_sync();  // #3: no CTA exits while others may still read its shared memory
@@ -409,19 +427,17 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 size_t front_smem_bytes(int n, int m, int k, int stages, int b_rows) {
   const int mt = (m + kBM - 1) / kBM;
   const int own = (n + kFrontCta - 1) / kFrontCta;  // own_max
-  const int tw = (n + 31) / 32;
-  const int nw = kFrontThreads / 32;
+  const int pairs = kFrontThreads / 64;
   size_t b = 1024;                                                     // alignment slack
   b += static_cast<size_t>(stages) * (mt * kATile + b_rows * 128);      // ring
   b += 8 * (2 * stages + 1) + 16;                                       // barriers, tmem slot
   b += static_cast<size_t>(n) * m * 4 + 4;                              // partials
-  b += static_cast<size_t>(own) * m * 8 + own * 8;                      // own rows + sums
-  b += static_cast<size_t>(nw) * m * 8;                                 // per-warp scratch rows
-  b += static_cast<size_t>(own) * k * 8 + static_cast<size_t>(n) * k * 16;  // vote values
-  b += static_cast<size_t>(m) * 8 + nw * 64 * 8;                        // votes, keys
-  b += static_cast<size_t>(own) * k * 4 + static_cast<size_t>(n) * k * 4;   // selections
-  b += static_cast<size_t>(m) * 8 + static_cast<size_t>(m) * tw * 4;   // counts, offsets, bitmaps
-  b += nw * 64 * 4 + static_cast<size_t>(m) + 16;                       // warp sel, flags
+  b += static_cast<size_t>(own) * m * 16 + own * 16;                    // x/e rows, sums, max
+  b += static_cast<size_t>(pairs) * m * 8;                              // scratch rows
+  b += static_cast<size_t>(own) * k * 8;                                // own vote values
+  b += static_cast<size_t>(n) * m * 8 + static_cast<size_t>(m) * 8;    // dense votes, votes
+  b += pairs * 64 * 8 + static_cast<size_t>(own) * k * 4 + pairs * 64 * 4;  // keys, sels
+  b += static_cast<size_t>(m) * 16 + static_cast<size_t>(m) + 16;      // partial ranks, flags
   return b;
 }
 

@@ -104,4 +104,121 @@ __device__ inline void token_write_route(const double* row, double s, int act, i
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident top-k: each lane keeps its (up to P) packed candidate
+// keys sorted descending in registers, so a round is two REDUX (~28 cycles
+// each) plus predicated register shifts in the owner lane — no shared-memory
+// traffic or divergent rescans on the critical path.
+// ---------------------------------------------------------------------------
+template <int P>
+struct LaneKeys {
+  uint64_t k[P];
+};
+
+template <int P>
+__device__ inline void lane_sort_desc(LaneKeys<P>& L) {
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+#pragma unroll
+    for (int j = 0; j + 1 < P - i; ++j) {
+      const uint64_t a = L.k[j], b = L.k[j + 1];
+      const bool sw = b > a;
+      L.k[j] = sw ? b : a;
+      L.k[j + 1] = sw ? a : b;
+    }
+}
+
+// rounds <= 64; sel[r]/keys[r] written by lane 0 (sel = -1 once exhausted).
+template <int P>
+__device__ inline void warp_topk_regs(LaneKeys<P>& L, int rounds, int* sel, uint64_t* keys) {
+  const int lane = threadIdx.x & 31;
+  lane_sort_desc<P>(L);
+  for (int r = 0; r < rounds; ++r) {
+    const uint64_t best = L.k[0];
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(best >> 32));
+    const uint32_t lo = __reduce_max_sync(
+        0xffffffffu, static_cast<uint32_t>(best >> 32) == hi ? static_cast<uint32_t>(best) : 0u);
+    const uint64_t win = (static_cast<uint64_t>(hi) << 32) | lo;
+    const int idx = 1023 - static_cast<int>(lo & 0x3FFu);
+    if (lane == 0) {
+      sel[r] = win ? idx : -1;
+      keys[r] = win;
+    }
+    const bool own = win != 0 && best == win;
+#pragma unroll
+    for (int j = 0; j + 1 < P; ++j) L.k[j] = own ? L.k[j + 1] : L.k[j];
+    L.k[P - 1] = own ? 0ull : L.k[P - 1];
+  }
+  __syncwarp();
+}
+
+// Loads the lane's candidates of `val` (allow == nullptr -> all) as packed keys.
+template <int P>
+__device__ inline void lane_load_keys(LaneKeys<P>& L, const double* val, int m,
+                                      const uint8_t* allow) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int i = lane + 32 * s;
+    L.k[s] = (i < m && (!allow || allow[i])) ? packed_key(val[i], i) : 0ull;
+  }
+}
+
+// Top-`want` of `val` (restricted to allow) in (value desc, index asc) order
+// of the packed keys, for any m <= 32 * 32 (dispatches on candidates/lane).
+// Runs `rounds` >= want rounds so the caller can inspect the boundary.
+__device__ inline void warp_topk_fast(const double* val, int m, int rounds, const uint8_t* allow,
+                                      int* sel, uint64_t* keys) {
+  if (m <= 64) {
+    LaneKeys<2> L;
+    lane_load_keys<2>(L, val, m, allow);
+    warp_topk_regs<2>(L, rounds, sel, keys);
+  } else if (m <= 128) {
+    LaneKeys<4> L;
+    lane_load_keys<4>(L, val, m, allow);
+    warp_topk_regs<4>(L, rounds, sel, keys);
+  } else if (m <= 256) {
+    LaneKeys<8> L;
+    lane_load_keys<8>(L, val, m, allow);
+    warp_topk_regs<8>(L, rounds, sel, keys);
+  } else {
+    warp_topk_packed(val, m, rounds, allow, sel, keys);
+  }
+}
+
+// Completes a fast selection made on packed keys of the logits (softmax) or of
+// the probabilities (sigmoid / identity). `sel` holds the fast rounds
+// (want + 1 when a boundary element exists). The selected SET (and the prefix
+// of length k2) is exactly the reference's unless a boundary is a near-tie:
+//   softmax  x gap <= 2^-40 (exp / division could merge the two values) or the
+//            rejected e is tiny (exp underflow ties, p subnormal);
+//   else     relative p gap <= 2^-40.
+// Near-ties re-select exactly on the fp64 probabilities with the reference's
+// comparator. Returns the number selected.
+__device__ inline int token_finish_selection(const double* xr, const double* er, double s,
+                                             double mx, int act, int m, int k, int k2,
+                                             const uint8_t* allow, int navail, int* sel,
+                                             double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int want = k < navail ? k : navail;
+  auto risky = [&](int b) -> bool {  // boundary between ranks b-1 and b
+    const int hi = sel[b - 1], lo = sel[b];
+    if (act == 0) {
+      const double gap = xr[hi] - xr[lo];
+      return !(gap > 0x1.0p-40) || !(er[lo] > 0x1.0p-960);
+    }
+    return near_tie(er[hi], er[lo]);
+  };
+  bool amb = false;
+  if (want < navail) amb |= risky(want);
+  if (k2 > 0 && k2 < want) amb |= risky(k2);
+  if (amb) {
+    for (int i = lane; i < m; i += 32) scratch[i] = p_of(er, s, act, i);
+    __syncwarp();
+    warp_select(scratch, m, want, allow, sel);
+  }
+  __syncwarp();
+  return want;
+}
+
 }  // namespace desmoe

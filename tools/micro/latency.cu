@@ -9,7 +9,7 @@ using namespace desmoe;
 
 __global__ void probe(const double* in, long long* out, int m, int k) {
   __shared__ double row[1024];
-  __shared__ int sel[32];
+  __shared__ int sel[64];
   const int lane = threadIdx.x;
   for (int i = lane; i < m; i += 32) row[i] = in[i];
   __syncwarp();
@@ -37,7 +37,20 @@ __global__ void probe(const double* in, long long* out, int m, int k) {
   for (int i = lane; i < m; i += 32) f += expf(static_cast<float>(row[i]));
   f = __shfl_sync(0xffffffffu, f, 0);
   long long t6 = clock64();
+  uint64_t pk[40];
+  warp_topk_packed(row, m, 9, nullptr, sel, pk);
+  long long t7 = clock64();
+  uint32_t rv = static_cast<uint32_t>(row[lane] * 1000.0);
+  for (int r = 0; r < 8; ++r) rv = __reduce_max_sync(0xffffffffu, rv + r);
+  long long t8 = clock64();
+  uint32_t sv = rv;
+  for (int r = 0; r < 8; ++r) sv = __shfl_xor_sync(0xffffffffu, sv, 1) + r;
+  long long t9 = clock64();
   if (lane == 0) {
+    out[7] = t7 - t6;
+    out[8] = (t8 - t7) / 8;
+    out[9] = (t9 - t8) / 8;
+    out[10] = static_cast<long long>(sv + pk[0]);
     out[0] = t1 - t0;
     out[1] = t2 - t1;
     out[2] = t3 - t2;
@@ -55,17 +68,17 @@ int main() {
   double* in;
   long long* out;
   cudaMalloc(&in, 1024 * 8);
-  cudaMalloc(&out, 8 * 8);
+  cudaMalloc(&out, 16 * 8);
   double h[1024];
   for (int i = 0; i < 1024; ++i) h[i] = 0.001 * ((i * 7919) % 1000) - 0.5;
   cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
   for (int m : ms) {
     for (int rep = 0; rep < 3; ++rep) probe<<<1, 32>>>(in, out, m, 8);
-    long long r[8];
+    long long r[12];
     cudaMemcpy(r, out, sizeof(r), cudaMemcpyDeviceToHost);
     printf("m=%d cycles: serial_dadd_sum=%lld exp_f64=%lld div_f64=%lld warp_select_k8=%lld "
-           "warp_argbest=%lld expf_f32=%lld\n",
-           m, r[0], r[1], r[2], r[3], r[4], r[5]);
+           "warp_argbest=%lld expf_f32=%lld topk_packed_9=%lld redux=%lld shfl=%lld\n",
+           m, r[0], r[1], r[2], r[3], r[4], r[5], r[7], r[8], r[9]);
   }
   return 0;
 }
