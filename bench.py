@@ -170,7 +170,8 @@ def main():
     ap.add_argument("--block", type=int, default=0, help="override block size N")
     ap.add_argument("--ref-ffn-tokens", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also report N=8..256 and strategies")
+    ap.add_argument("--strategies", default="vanilla,seq3,seq2,vote",
+                    help="comma list; vote and vanilla are always timed")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
@@ -234,7 +235,10 @@ def main():
     results = {}
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
-        for strategy in ("vanilla", "seq3", "seq2", "vote"):
+        wanted = [s for s in args.strategies.split(",") if s]
+        order = [s for s in ("vanilla", "seq3", "seq2", "vote")
+                 if s in wanted or s in ("vanilla", "vote")]
+        for strategy in order:
             # timed pass: only the outer events (no event nodes between kernels,
             # so the programmatic launches overlap exactly as in production)
             L.desmoe_set_profiling(layer.ctx.h, 0)
