@@ -3,9 +3,9 @@
  * layer. Plain pointers and sizes only; no C++ or torch types.
  *
  * Every entry point replaces one function of the reference library's C++
- * operator API (dessim, /root/reference/proj/core/include/dessim/*.hpp); the
+ * operator API (dessim, /root/reference/proj/core/include/dessim/{core,gating,des}.hpp); the
  * reference interface is cited beside each declaration. The C++ facade
- * (include/dessim_gpu.hpp) and the Python mirror (paper_2602_00879_b200/dessim.py)
+ * (include/dessim/{core,gating,des}.hpp, libdessim_gpu.so) and the Python mirror (paper_2602_00879_b200/dessim.py)
  * sit on top of this header.
  *
  * Conventions
@@ -104,6 +104,10 @@ int desmoe_validate_pool(int experts, int top_k, uint64_t bytes_per_expert, int 
 /* vote_budget (des.cpp:29-31): floor(beta * experts). */
 int desmoe_vote_budget(double beta, int experts);
 
+/* validate_params (des.cpp:10-27): validate_config first, then the strategy's
+ * parameter; same order, same messages. Host only. */
+int desmoe_validate_params(const desmoe_route_cfg* cfg);
+
 /* ---- gating / routing (logits in, device pointers) ------------------------
  * logits_dev is [n x experts] row-major, fp64 (the reference's RouterBlock,
  * core.hpp:32-44) or fp32 (the router GEMM's output / MOET trace values). */
@@ -134,6 +138,18 @@ int desmoe_constrained_route(desmoe_ctx* ctx, const double* logits_dev, int n,
                              const desmoe_route_cfg* cfg, const int* members_host,
                              int n_members, const desmoe_route_out* out, void* stream);
 
+/* select_top_gates (gating.cpp:42-71), both overloads, any k <= candidates:
+ * the k largest of values_dev[0..m) by (value desc, index asc), restricted to
+ * cand_dev[0..n_cand) when cand_dev != NULL (ascending, unique, < m); writes
+ * the k selected indices in ascending order to out_dev. m <= 16384. */
+int desmoe_select_top(desmoe_ctx* ctx, const double* values_dev, int m, int k,
+                      const int* cand_dev, int n_cand, int* out_dev, void* stream);
+
+/* renormalize_over (gating.cpp:73-82): out[j] = values[sel[j]] / sum, the
+ * sum taken over sel in the given order. */
+int desmoe_renormalize(desmoe_ctx* ctx, const double* values_dev, const int* sel_dev, int count,
+                       double* out_dev, void* stream);
+
 /* ---- permutation (K3) -------------------------------------------------------
  * Per-expert counts (moe_latency's count route, analysis.cpp:16-30), ascending
  * exclusive offsets, stable (ascending token) slot lists, the ascending list of
@@ -162,6 +178,18 @@ void desmoe_experts_destroy(desmoe_experts* ex);
 int desmoe_expert_ffn(desmoe_ctx* ctx, const desmoe_experts* ex, const void* x_dev, int n,
                       int top_k, const int* route_idx_dev, const double* route_gate_dev,
                       const int* route_cnt_dev, float* y_dev, void* stream);
+
+/* moe_forward (gating.cpp:136-157) over the reference's linear experts in
+ * fp64, bit-identical to the CPU library (same operation order, no FMA
+ * contraction): y[t] = sum over the token's experts in stored order of
+ * gate * W_e x_t. w_dev [experts x hidden x hidden] ([out][in], the
+ * ExpertBank layout), x_dev [n x hidden], y_dev [n x hidden], route_* as
+ * desmoe_route writes them (row stride top_k). Expert indices must lie in
+ * [0, experts) (the caller validates, as moe_forward does). */
+int desmoe_moe_forward_f64(desmoe_ctx* ctx, const double* w_dev, const double* x_dev, int n,
+                           int hidden, int experts, int top_k, const int* route_idx_dev,
+                           const double* route_gate_dev, const int* route_cnt_dev, double* y_dev,
+                           void* stream);
 
 /* ---- router GEMM (K1) -------------------------------------------------------
  * logits[n x experts] fp32 = x[n x hidden] (bf16) . w_router[experts x hidden]^T

@@ -43,6 +43,10 @@ _SIGS = {
     "desmoe_version": (_I, []),
     "desmoe_validate_pool": (_I, [_I, _I, C.c_uint64, _I]),
     "desmoe_vote_budget": (_I, [_D, _I]),
+    "desmoe_validate_params": (_I, [C.POINTER(RouteCfg)]),
+    "desmoe_select_top": (_I, [_P, _P, _I, _I, _P, _I, _P, _P]),
+    "desmoe_renormalize": (_I, [_P, _P, _P, _I, _P, _P]),
+    "desmoe_moe_forward_f64": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "desmoe_activate": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "desmoe_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
     "desmoe_route_f32": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),

@@ -1138,3 +1138,66 @@ int desmoe_layer_forward_host(desmoe_ctx* c, const desmoe_experts* ex, const voi
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// exact fp64 gating primitives of the reference API (gating_exact.cu)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int desmoe_validate_params(const desmoe_route_cfg* cfg) {
+  if (!cfg) return fail(DESMOE_EINVAL, "null config");
+  return check_des_params(cfg);
+}
+
+int desmoe_select_top(desmoe_ctx* c, const double* values, int m, int k, const int* cand,
+                      int n_cand, int* out, void* stream) {
+  if (!c || !values || !out) return fail(DESMOE_EINVAL, "null argument");
+  if (m < 1 || m > 16384) return fail(DESMOE_EINVAL, "gate count outside [1, 16384]");
+  if (cand && (n_cand < 0 || n_cand > m))
+    return fail(DESMOE_EINVAL, "candidate count outside [0, gate count]");
+  if (k > (cand ? n_cand : m))
+    return fail(DESMOE_EINVAL, cand ? "selection count exceeds candidate count"
+                                    : "selection count exceeds gate count");
+  if (k < 1) return DESMOE_OK;
+  const size_t smem = static_cast<size_t>(m) * 9 + 33 * 4 + 16;
+  if (smem > 48 * 1024)
+    DESMOE_CUDA(cudaFuncSetAttribute(select_top_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+  const int threads = std::min(1024, round_up(std::max(cand ? n_cand : m, 32), 32));
+  select_top_kernel<<<1, threads, smem, S(stream)>>>(values, m, k, cand, n_cand, out);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+int desmoe_renormalize(desmoe_ctx* c, const double* values, const int* sel, int count,
+                       double* out, void* stream) {
+  if (!c || !values || !sel || !out) return fail(DESMOE_EINVAL, "null argument");
+  if (count < 1) return DESMOE_OK;
+  renormalize_kernel<<<1, 256, 0, S(stream)>>>(values, sel, count, out);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+int desmoe_moe_forward_f64(desmoe_ctx* c, const double* w, const double* x, int n, int d, int m,
+                           int k, const int* route_idx, const double* route_gate,
+                           const int* route_cnt, double* y, void* stream) {
+  if (!c || !w || !x || !y || !route_idx || !route_gate || !route_cnt)
+    return fail(DESMOE_EINVAL, "null argument");
+  if (n < 1) return fail(DESMOE_EINVAL, "block_size < 1");
+  if (d < 1 || d > 16384) return fail(DESMOE_EINVAL, "hidden_dim outside [1, 16384]");
+  if (m < 1 || k < 1) return fail(DESMOE_EINVAL, "experts and top_k must be >= 1");
+  const int threads = std::min(256, round_up(d, 32));
+  const size_t smem = static_cast<size_t>(d) * sizeof(double);
+  if (smem > 48 * 1024)
+    DESMOE_CUDA(cudaFuncSetAttribute(linear_expert_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+  dim3 grid((d + threads - 1) / threads, n);
+  linear_expert_kernel<<<grid, threads, smem, S(stream)>>>(w, x, d, k, route_idx, route_gate,
+                                                           route_cnt, y);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+}  // extern "C"

@@ -188,6 +188,17 @@ cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const
                          size_t smem, cudaStream_t st);
 cudaError_t set_front_smem_limit();
 
+// ---- exact fp64 gating primitives (gating_exact.cu) ----
+__global__ void select_top_kernel(const double* __restrict__ values, int m, int k,
+                                  const int* __restrict__ cand, int n_cand, int* __restrict__ out);
+__global__ void renormalize_kernel(const double* __restrict__ values,
+                                   const int* __restrict__ sel, int count,
+                                   double* __restrict__ out);
+__global__ void linear_expert_kernel(const double* __restrict__ w, const double* __restrict__ x,
+                                     int d, int k, const int* __restrict__ route_idx,
+                                     const double* __restrict__ route_gate,
+                                     const int* __restrict__ route_cnt, double* __restrict__ y);
+
 __global__ void tile_gemm_kernel(const __grid_constant__ CUtensorMap wa,
                                  const __grid_constant__ CUtensorMap wb,
                                  const __grid_constant__ BoxMaps acts, TileArgs a);

@@ -1,0 +1,625 @@
+// libdessim_gpu.so — the reference's C++ operator API (namespace dessim,
+// include/dessim/{core,gating,des}.hpp) backed by the sm_100a kernels of
+// libdesmoe.so through its C ABI (include/desmoe.h).
+//
+// Host work here is limited to what the reference itself does on the host
+// around the math: argument validation with the reference's messages, the
+// value-type plumbing (std::vector in, std::vector out), and the synthetic
+// generators (Rng, make_expert_bank). Every activation, selection, vote,
+// re-route, renormalisation, permutation and expert product runs on the GPU;
+// without a CUDA device every call throws — there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/desmoe.h"
+#include "dessim/core.hpp"
+#include "dessim/des.hpp"
+#include "dessim/gating.hpp"
+
+namespace dessim {
+
+// ===========================================================================
+// device plumbing
+// ===========================================================================
+namespace {
+
+[[noreturn]] void raise_desmoe(int rc) {
+  const std::string msg = desmoe_last_error();
+  if (rc == DESMOE_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error("desmoe: " + msg);
+}
+
+inline void ok(int rc) {
+  if (rc != DESMOE_OK) raise_desmoe(rc);
+}
+
+inline void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// grow-only device scratch
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~Scratch() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* get(size_t count) {
+    const size_t need = std::max<size_t>(count, 1) * sizeof(T);
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      cuda_ok(cudaMalloc(&p, need), "cudaMalloc");
+      bytes = need;
+    }
+    return static_cast<T*>(p);
+  }
+};
+
+// One C-ABI context per (host thread, device), grown on demand.
+struct Gpu {
+  int device = 0;
+  desmoe_ctx* ctx = nullptr;
+  int cap_n = 0, cap_m = 0, cap_k = 0;
+  cudaStream_t stream = nullptr;
+  Scratch s[8];
+
+  ~Gpu() {
+    if (ctx) desmoe_destroy(ctx);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void* st() const { return stream; }
+
+  template <typename T>
+  T* upload(int slot, const T* host, size_t count) {
+    T* d = s[slot].get<T>(count);
+    if (count)
+      cuda_ok(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, stream),
+              "cudaMemcpyAsync H2D");
+    return d;
+  }
+  template <typename T>
+  std::vector<T> download(const T* dev, size_t count) {
+    std::vector<T> out(count);
+    if (count)
+      cuda_ok(cudaMemcpyAsync(out.data(), dev, count * sizeof(T), cudaMemcpyDeviceToHost, stream),
+              "cudaMemcpyAsync D2H");
+    cuda_ok(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    return out;
+  }
+  // synchronises and surfaces the device-latched data checks
+  void finish() { ok(desmoe_check(ctx, stream)); }
+};
+
+constexpr int kMaxCtxTokens = 1024;
+constexpr int kMaxCtxExperts = 1024;
+constexpr int kMaxCtxTopK = 32;
+
+Gpu& gpu(int n, int m, int k) {
+  thread_local std::map<int, std::unique_ptr<Gpu>> per_device;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) {
+    cudaGetLastError();
+    throw std::runtime_error("no CUDA device: the DES MoE path has no CPU fallback");
+  }
+  if (n > kMaxCtxTokens || m > kMaxCtxExperts || k > kMaxCtxTopK)
+    throw std::runtime_error("block exceeds the GPU routing kernels' capacity "
+                             "(<= 1024 tokens, <= 1024 experts, top_k <= 32)");
+  int dev = 0;
+  cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+  std::unique_ptr<Gpu>& g = per_device[dev];
+  if (!g) {
+    g = std::make_unique<Gpu>();
+    g->device = dev;
+    cuda_ok(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  if (!g->ctx || n > g->cap_n || m > g->cap_m || k > g->cap_k) {
+    if (g->ctx) {
+      cuda_ok(cudaStreamSynchronize(g->stream), "cudaStreamSynchronize");
+      desmoe_destroy(g->ctx);
+      g->ctx = nullptr;
+    }
+    g->cap_n = std::min(kMaxCtxTokens, std::max({n, g->cap_n, 256}));
+    g->cap_m = std::min(kMaxCtxExperts, std::max({m, g->cap_m, 256}));
+    g->cap_k = std::min(kMaxCtxTopK, std::max({k, g->cap_k, 16}));
+    ok(desmoe_create(&g->ctx, dev, g->cap_n, g->cap_m, g->cap_k, 128));
+  }
+  return *g;
+}
+
+int act_code(GateActivation a) {
+  return a == GateActivation::sigmoid ? DESMOE_SIGMOID : DESMOE_SOFTMAX;
+}
+
+desmoe_route_cfg route_cfg(const PoolConfig& cfg, int strategy, int seq_k = 1, double beta = 1.0,
+                           VoteSource src = VoteSource::activated) {
+  desmoe_route_cfg c{};
+  c.experts = cfg.experts_total;
+  c.top_k = cfg.top_k;
+  c.activation = act_code(cfg.gate_activation);
+  c.strategy = strategy;
+  c.seq_k = seq_k;
+  c.vote_beta = beta;
+  c.vote_source = src == VoteSource::raw_logits ? DESMOE_VOTE_RAW_LOGITS : DESMOE_VOTE_ACTIVATED;
+  return c;
+}
+
+// Device route buffers [n x k] -> RoutingAssignment (experts ascending).
+RoutingAssignment read_assignment(Gpu& g, const int* idx, const double* gate, const int* cnt,
+                                  int n, int k) {
+  std::vector<int> hi = g.download(idx, static_cast<size_t>(n) * k);
+  std::vector<double> hg = g.download(gate, static_cast<size_t>(n) * k);
+  std::vector<int> hc = g.download(cnt, static_cast<size_t>(n));
+  RoutingAssignment a;
+  a.tokens.resize(n);
+  for (int t = 0; t < n; ++t) {
+    const int c = hc[t];
+    a.tokens[t].experts.assign(hi.begin() + static_cast<size_t>(t) * k,
+                               hi.begin() + static_cast<size_t>(t) * k + c);
+    a.tokens[t].gates.assign(hg.begin() + static_cast<size_t>(t) * k,
+                             hg.begin() + static_cast<size_t>(t) * k + c);
+  }
+  return a;
+}
+
+// des.cpp:49-61 (checked_budget)
+void checked_budget(double beta, int experts_total) {
+  if (!(beta > 0.0)) throw std::invalid_argument("beta <= 0");
+  const int m_core = vote_budget(beta, experts_total);
+  if (m_core < 1) throw std::invalid_argument("vote budget floor(beta*M) < 1");
+  if (m_core > experts_total) throw std::invalid_argument("beta > 1");
+}
+
+}  // namespace
+
+// ===========================================================================
+// core.hpp (host value types, as in the reference's core.cpp)
+// ===========================================================================
+
+const PoolConfig& validate_config(const PoolConfig& cfg) {
+  ok(desmoe_validate_pool(cfg.experts_total, cfg.top_k, cfg.bytes_per_expert, cfg.hidden_dim));
+  return cfg;
+}
+
+const char* to_string(GateActivation activation) {
+  return activation == GateActivation::sigmoid ? "sigmoid" : "softmax";
+}
+
+GateActivation gate_activation_from_string(const std::string& name) {
+  if (name == "sigmoid") return GateActivation::sigmoid;
+  if (name == "softmax") return GateActivation::softmax;
+  throw std::invalid_argument("unknown gate activation: " + name);
+}
+
+RouterBlock make_router_block(int block_size, int experts, std::vector<double> logits) {
+  if (block_size < 1) throw std::invalid_argument("block_size < 1");
+  if (experts < 1) throw std::invalid_argument("experts < 1");
+  if (logits.size() != static_cast<size_t>(block_size) * static_cast<size_t>(experts))
+    throw std::invalid_argument("logits size does not match block_size x experts");
+  if (std::any_of(logits.begin(), logits.end(), [](double v) { return !std::isfinite(v); }))
+    throw std::invalid_argument("non-finite logit");
+  RouterBlock b;
+  b.block_size = block_size;
+  b.experts = experts;
+  b.logits = std::move(logits);
+  return b;
+}
+
+void validate_block(const RouterBlock& block, const PoolConfig& cfg) {
+  if (block.experts != cfg.experts_total)
+    throw std::invalid_argument("block column count does not match experts_total");
+  if (block.block_size < 1) throw std::invalid_argument("block_size < 1");
+  if (block.logits.size() !=
+      static_cast<size_t>(block.block_size) * static_cast<size_t>(block.experts))
+    throw std::invalid_argument("logits size does not match block shape");
+  // finiteness: checked again by the device kernels (desmoe_check)
+  if (std::any_of(block.logits.begin(), block.logits.end(),
+                  [](double v) { return !std::isfinite(v); }))
+    throw std::invalid_argument("non-finite logit");
+}
+
+bool Coreset::contains(int expert) const {
+  auto it = std::lower_bound(members.begin(), members.end(), expert);
+  return it != members.end() && *it == expert;
+}
+
+Coreset Coreset::of(std::vector<int> indices) {
+  std::sort(indices.begin(), indices.end());
+  indices.erase(std::unique(indices.begin(), indices.end()), indices.end());
+  if (!indices.empty() && indices.front() < 0)
+    throw std::invalid_argument("negative expert index");
+  Coreset c;
+  c.members = std::move(indices);
+  return c;
+}
+
+namespace {
+inline std::uint64_t splitmix_finalize(std::uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr std::uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+}  // namespace
+
+std::uint64_t Rng::next_u64() {
+  state_ += kGolden;
+  return splitmix_finalize(state_);
+}
+
+double Rng::next_unit() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+
+double Rng::next_normal() {
+  if (has_spare_) {
+    has_spare_ = false;
+    return spare_;
+  }
+  const double u1 = static_cast<double>((next_u64() >> 11) + 1) * 0x1.0p-53;  // (0, 1]
+  const double u2 = next_unit();
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * 3.14159265358979323846 * u2;
+  spare_ = radius * std::sin(angle);
+  has_spare_ = true;
+  return radius * std::cos(angle);
+}
+
+int Rng::next_below(int bound) {
+  if (bound < 1) throw std::invalid_argument("bound < 1");
+  const std::uint64_t b = static_cast<std::uint64_t>(bound);
+  const std::uint64_t floor_ = (0ull - b) % b;  // 2^64 mod b: reject below it
+  for (;;) {
+    const std::uint64_t v = next_u64();
+    if (v >= floor_) return static_cast<int>(v % b);
+  }
+}
+
+std::uint64_t Rng::mix(std::uint64_t seed, std::uint64_t stream) {
+  return splitmix_finalize(seed + kGolden * (stream + 1));
+}
+
+// ===========================================================================
+// gating.hpp
+// ===========================================================================
+
+GateMatrix activate(const RouterBlock& block, const PoolConfig& cfg) {
+  validate_block(block, cfg);
+  const int n = block.block_size, m = block.experts;
+  Gpu& g = gpu(n, m, 1);
+  const double* x = g.upload(0, block.logits.data(), block.logits.size());
+  double* p = g.s[1].get<double>(block.logits.size());
+  ok(desmoe_activate(g.ctx, x, n, m, act_code(cfg.gate_activation), p, g.st()));
+  g.finish();
+  GateMatrix out;
+  out.rows = n;
+  out.cols = m;
+  out.probs = g.download(p, block.logits.size());
+  return out;
+}
+
+std::vector<int> select_top_gates(std::span<const double> gates, int k) {
+  const int m = static_cast<int>(gates.size());
+  if (k > m) throw std::invalid_argument("selection count exceeds gate count");
+  if (k < 1) return {};
+  Gpu& g = gpu(1, 1, 1);
+  const double* v = g.upload(0, gates.data(), gates.size());
+  int* out = g.s[1].get<int>(k);
+  ok(desmoe_select_top(g.ctx, v, m, k, nullptr, 0, out, g.st()));
+  return g.download(out, k);
+}
+
+std::vector<int> select_top_gates(std::span<const double> gates, int k,
+                                  std::span<const int> candidates) {
+  const int nc = static_cast<int>(candidates.size());
+  if (k > nc) throw std::invalid_argument("selection count exceeds candidate count");
+  if (k < 1) return {};
+  const int m = static_cast<int>(gates.size());
+  for (int c : candidates)
+    if (c < 0 || c >= m) throw std::invalid_argument("candidate index out of range");
+  Gpu& g = gpu(1, 1, 1);
+  const double* v = g.upload(0, gates.data(), gates.size());
+  const int* cand = g.upload(1, candidates.data(), candidates.size());
+  int* out = g.s[2].get<int>(k);
+  ok(desmoe_select_top(g.ctx, v, m, k, cand, nc, out, g.st()));
+  return g.download(out, k);
+}
+
+std::vector<double> renormalize_over(std::span<const double> gates,
+                                     std::span<const int> selected) {
+  const int cnt = static_cast<int>(selected.size());
+  if (cnt < 1) return {};
+  for (int s : selected)
+    if (s < 0 || s >= static_cast<int>(gates.size()))
+      throw std::invalid_argument("selected index out of range");
+  Gpu& g = gpu(1, 1, 1);
+  const double* v = g.upload(0, gates.data(), gates.size());
+  const int* sel = g.upload(1, selected.data(), selected.size());
+  double* out = g.s[2].get<double>(cnt);
+  ok(desmoe_renormalize(g.ctx, v, sel, cnt, out, g.st()));
+  return g.download(out, cnt);
+}
+
+RoutingAssignment topk_route(const GateMatrix& gates, int top_k) {
+  if (top_k < 1 || top_k > gates.cols) throw std::invalid_argument("top_k out of range");
+  const int n = gates.rows, m = gates.cols;
+  if (top_k > kMaxCtxTopK) {
+    // wider than the fused routing kernels: per-token GPU select + renormalise
+    RoutingAssignment a;
+    a.tokens.resize(n);
+    for (int t = 0; t < n; ++t) {
+      a.tokens[t].experts = select_top_gates(gates.row(t), top_k);
+      a.tokens[t].gates = renormalize_over(gates.row(t), a.tokens[t].experts);
+    }
+    return a;
+  }
+  Gpu& g = gpu(n, m, top_k);
+  const double* p = g.upload(0, gates.probs.data(), gates.probs.size());
+  int* idx = g.s[1].get<int>(static_cast<size_t>(n) * top_k);
+  double* gate = g.s[2].get<double>(static_cast<size_t>(n) * top_k);
+  int* cnt = g.s[3].get<int>(n);
+  desmoe_route_cfg c{};
+  c.experts = m;
+  c.top_k = top_k;
+  c.activation = DESMOE_IDENTITY;  // topk_route(const GateMatrix&): gates already activated
+  c.strategy = DESMOE_VANILLA;
+  desmoe_route_out o{};
+  o.route_idx_dev = idx;
+  o.route_gate_dev = gate;
+  o.route_cnt_dev = cnt;
+  ok(desmoe_route(g.ctx, p, n, &c, &o, g.st()));
+  g.finish();
+  return read_assignment(g, idx, gate, cnt, n, top_k);
+}
+
+ExpertBank make_expert_bank(const PoolConfig& cfg, int block_size, std::uint64_t seed) {
+  validate_config(cfg);
+  if (block_size < 1) throw std::invalid_argument("block_size < 1");
+  ExpertBank bank;
+  bank.experts = cfg.experts_total;
+  bank.dim = cfg.hidden_dim;
+  bank.block_size = block_size;
+  Rng rng(seed);
+  const double scale = 1.0 / std::sqrt(static_cast<double>(bank.dim));
+  bank.expert_weights.resize(static_cast<size_t>(bank.experts) * bank.dim * bank.dim);
+  for (double& w : bank.expert_weights) w = rng.next_normal() * scale;
+  bank.token_inputs.resize(static_cast<size_t>(block_size) * bank.dim);
+  for (double& x : bank.token_inputs) x = rng.next_normal();
+  return bank;
+}
+
+namespace {
+
+// moe_forward over `slots` (per token: experts in stored order, gates) with
+// only the experts actually used uploaded (compacted), fp64 on the GPU.
+std::vector<double> linear_forward(const ExpertBank& bank, const std::vector<const double*>& x_rows,
+                                   const std::vector<std::vector<int>>& experts,
+                                   const std::vector<std::vector<double>>& gates) {
+  const int n = static_cast<int>(x_rows.size()), d = bank.dim;
+  int kmax = 1;
+  std::vector<int> remap(bank.experts, -1), used;
+  for (const auto& ex : experts) {
+    kmax = std::max(kmax, static_cast<int>(ex.size()));
+    for (int e : ex)
+      if (remap[e] < 0) {
+        remap[e] = static_cast<int>(used.size());
+        used.push_back(e);
+      }
+  }
+  const size_t dd = static_cast<size_t>(d) * d;
+  std::vector<double> w(std::max<size_t>(used.size(), 1) * dd, 0.0);
+  for (size_t u = 0; u < used.size(); ++u)
+    std::memcpy(w.data() + u * dd, bank.expert_weights.data() + static_cast<size_t>(used[u]) * dd,
+                dd * sizeof(double));
+  std::vector<double> x(static_cast<size_t>(n) * d);
+  for (int t = 0; t < n; ++t) std::memcpy(x.data() + static_cast<size_t>(t) * d, x_rows[t], d * sizeof(double));
+  std::vector<int> idx(static_cast<size_t>(n) * kmax, 0), cnt(n, 0);
+  std::vector<double> gate(static_cast<size_t>(n) * kmax, 0.0);
+  for (int t = 0; t < n; ++t) {
+    cnt[t] = static_cast<int>(experts[t].size());
+    for (int j = 0; j < cnt[t]; ++j) {
+      idx[static_cast<size_t>(t) * kmax + j] = remap[experts[t][j]];
+      gate[static_cast<size_t>(t) * kmax + j] = gates[t][j];
+    }
+  }
+  Gpu& g = gpu(1, 1, 1);
+  const double* dw = g.upload(0, w.data(), w.size());
+  const double* dx = g.upload(1, x.data(), x.size());
+  const int* di = g.upload(2, idx.data(), idx.size());
+  const double* dg = g.upload(3, gate.data(), gate.size());
+  const int* dc = g.upload(4, cnt.data(), cnt.size());
+  double* dy = g.s[5].get<double>(x.size());
+  ok(desmoe_moe_forward_f64(g.ctx, dw, dx, n, d, std::max<int>(used.size(), 1), kmax, di, dg, dc,
+                            dy, g.st()));
+  return g.download(dy, x.size());
+}
+
+}  // namespace
+
+std::vector<double> expert_output(const ExpertBank& bank, int expert, int token) {
+  if (expert < 0 || expert >= bank.experts)
+    throw std::invalid_argument("expert index out of range for bank");
+  if (token < 0 || token >= bank.block_size) throw std::invalid_argument("token out of range");
+  // 0 + 1.0 * (W x) == W x exactly
+  return linear_forward(bank, {bank.token_input(token).data()}, {{expert}}, {{1.0}});
+}
+
+std::vector<double> moe_forward(const RoutingAssignment& assign, const ExpertBank& bank) {
+  if (assign.block_size() != bank.block_size)
+    throw std::invalid_argument("assignment and bank block sizes differ");
+  std::vector<const double*> rows(bank.block_size);
+  std::vector<std::vector<int>> experts(bank.block_size);
+  std::vector<std::vector<double>> gates(bank.block_size);
+  for (int t = 0; t < bank.block_size; ++t) {
+    const TokenRoute& tok = assign.tokens[t];
+    for (size_t j = 0; j < tok.experts.size(); ++j) {
+      const int e = tok.experts[j];
+      if (e < 0 || e >= bank.experts)
+        throw std::invalid_argument("expert index out of range for bank");
+    }
+    rows[t] = bank.token_input(t).data();
+    experts[t] = tok.experts;
+    gates[t] = tok.gates;
+    gates[t].resize(tok.experts.size(), 0.0);
+  }
+  return linear_forward(bank, rows, experts, gates);
+}
+
+Coreset unique_experts(const RoutingAssignment& assign) {
+  const int n = assign.block_size();
+  int kmax = 0, m = 0;
+  for (const TokenRoute& tok : assign.tokens) {
+    kmax = std::max(kmax, static_cast<int>(tok.experts.size()));
+    for (int e : tok.experts) {
+      if (e < 0) throw std::invalid_argument("negative expert index");
+      m = std::max(m, e + 1);
+    }
+  }
+  if (n < 1 || kmax < 1) return Coreset{};
+  Gpu& g = gpu(n, m, kmax);
+  std::vector<int> idx(static_cast<size_t>(n) * kmax, -1), cnt(n, 0);
+  for (int t = 0; t < n; ++t) {
+    const auto& ex = assign.tokens[t].experts;
+    cnt[t] = static_cast<int>(ex.size());
+    std::copy(ex.begin(), ex.end(), idx.begin() + static_cast<size_t>(t) * kmax);
+  }
+  const int* di = g.upload(0, idx.data(), idx.size());
+  const int* dc = g.upload(1, cnt.data(), cnt.size());
+  int* count = g.s[2].get<int>(m);
+  int* offset = g.s[3].get<int>(m);
+  int* active = g.s[4].get<int>(m);
+  int* n_active = g.s[5].get<int>(1);
+  ok(desmoe_permute(g.ctx, di, dc, n, kmax, m, count, offset, nullptr, nullptr, active, n_active,
+                    g.st()));
+  const int u = g.download(n_active, 1)[0];
+  Coreset c;
+  c.members = g.download(active, u);
+  return c;
+}
+
+// ===========================================================================
+// des.hpp
+// ===========================================================================
+
+void validate_params(const DesParams& params, const PoolConfig& cfg) {
+  validate_config(cfg);
+  desmoe_route_cfg c = route_cfg(cfg, params.strategy == DesStrategy::seq ? DESMOE_SEQ : DESMOE_VOTE,
+                                 params.seq_k, params.vote_beta);
+  ok(desmoe_validate_params(&c));
+}
+
+int vote_budget(double beta, int experts_total) { return desmoe_vote_budget(beta, experts_total); }
+
+namespace {
+
+struct CoresetOut {
+  Coreset coreset;
+  std::vector<double> votes;
+};
+
+CoresetOut run_coreset(const RouterBlock& block, const PoolConfig& cfg, int strategy, int seq_k,
+                       double beta, VoteSource src) {
+  const int n = block.block_size, m = block.experts;
+  Gpu& g = gpu(n, m, std::max(cfg.top_k, 1));
+  const double* x = g.upload(0, block.logits.data(), block.logits.size());
+  int* members = g.s[1].get<int>(m);
+  int* n_members = g.s[2].get<int>(1);
+  double* votes = g.s[3].get<double>(m);
+  desmoe_route_cfg c = route_cfg(cfg, strategy, seq_k, beta, src);
+  desmoe_route_out o{};
+  o.coreset_dev = members;
+  o.coreset_size_dev = n_members;
+  o.votes_dev = strategy == DESMOE_VOTE ? votes : nullptr;
+  ok(desmoe_coreset(g.ctx, x, n, &c, &o, g.st()));
+  g.finish();
+  CoresetOut r;
+  const int nm = g.download(n_members, 1)[0];
+  r.coreset.members = g.download(members, nm);
+  if (strategy == DESMOE_VOTE) r.votes = g.download(votes, m);
+  return r;
+}
+
+}  // namespace
+
+Coreset des_seq_coreset(const RouterBlock& block, const PoolConfig& cfg, int local_k) {
+  if (local_k < 1 || local_k > cfg.top_k)
+    throw std::invalid_argument("local_k outside [1, top_k]");
+  validate_block(block, cfg);
+  return run_coreset(block, cfg, DESMOE_SEQ, local_k, 1.0, VoteSource::activated).coreset;
+}
+
+VoteResult des_vote_coreset(const RouterBlock& block, const PoolConfig& cfg, double beta,
+                            VoteSource source) {
+  validate_block(block, cfg);
+  checked_budget(beta, cfg.experts_total);
+  CoresetOut r = run_coreset(block, cfg, DESMOE_VOTE, 1, beta, source);
+  VoteResult out;
+  out.coreset = std::move(r.coreset);
+  out.votes.votes = std::move(r.votes);
+  return out;
+}
+
+RoutingAssignment constrained_route(const RouterBlock& block, const PoolConfig& cfg,
+                                    const Coreset& coreset) {
+  validate_block(block, cfg);
+  if (coreset.members.empty()) throw std::invalid_argument("empty coreset");
+  if (coreset.members.back() >= cfg.experts_total)
+    throw std::invalid_argument("coreset member out of range");
+  const int n = block.block_size, m = block.experts, k = cfg.top_k;
+  Gpu& g = gpu(n, m, k);
+  const double* x = g.upload(0, block.logits.data(), block.logits.size());
+  int* idx = g.s[1].get<int>(static_cast<size_t>(n) * k);
+  double* gate = g.s[2].get<double>(static_cast<size_t>(n) * k);
+  int* cnt = g.s[3].get<int>(n);
+  desmoe_route_cfg c = route_cfg(cfg, DESMOE_VANILLA);
+  desmoe_route_out o{};
+  o.route_idx_dev = idx;
+  o.route_gate_dev = gate;
+  o.route_cnt_dev = cnt;
+  ok(desmoe_constrained_route(g.ctx, x, n, &c, coreset.members.data(), coreset.size(), &o,
+                              g.st()));
+  g.finish();
+  return read_assignment(g, idx, gate, cnt, n, k);
+}
+
+DesResult des_run(const RouterBlock& block, const PoolConfig& cfg, const DesParams& params) {
+  validate_params(params, cfg);
+  validate_block(block, cfg);
+  const int n = block.block_size, m = block.experts, k = cfg.top_k;
+  Gpu& g = gpu(n, m, k);
+  const double* x = g.upload(0, block.logits.data(), block.logits.size());
+  int* idx = g.s[1].get<int>(static_cast<size_t>(n) * k);
+  double* gate = g.s[2].get<double>(static_cast<size_t>(n) * k);
+  int* cnt = g.s[3].get<int>(n);
+  int* members = g.s[4].get<int>(m);
+  int* n_members = g.s[5].get<int>(1);
+  desmoe_route_cfg c = route_cfg(cfg, params.strategy == DesStrategy::seq ? DESMOE_SEQ : DESMOE_VOTE,
+                                 params.seq_k, params.vote_beta);
+  desmoe_route_out o{};
+  o.route_idx_dev = idx;
+  o.route_gate_dev = gate;
+  o.route_cnt_dev = cnt;
+  o.coreset_dev = members;
+  o.coreset_size_dev = n_members;
+  ok(desmoe_route(g.ctx, x, n, &c, &o, g.st()));
+  g.finish();
+  DesResult r;
+  const int nm = g.download(n_members, 1)[0];
+  r.coreset.members = g.download(members, nm);
+  r.assignment = read_assignment(g, idx, gate, cnt, n, k);
+  return r;
+}
+
+VoteResult fused_vote_pipeline(const RouterBlock& block, const PoolConfig& cfg, double beta) {
+  return des_vote_coreset(block, cfg, beta, VoteSource::activated);
+}
+
+}  // namespace dessim
