@@ -171,6 +171,43 @@ int desmoe_experts_create(desmoe_ctx* ctx, int kind, int experts, int hidden, in
                           desmoe_experts** out);
 void desmoe_experts_destroy(desmoe_experts* ex);
 
+/* ---- expert parallelism (EP) -------------------------------------------------
+ * A world of up to 8 ranks (one process per GPU of an NVSwitch box) shards
+ * the experts in contiguous ranges, rank r owning [expert_lo, expert_hi).
+ * Router, coreset and re-route are replicated (deterministic, so every rank
+ * derives the identical route with no exchange). Each rank streams only its
+ * experts; its FFN epilogues push every gate-scaled slot row straight into
+ * all ranks' slot buffers over NVLink peer memory and signal each rank's
+ * arrival counter; each rank's combine waits for all arrivals and sums the
+ * slots in ascending expert order — bit-identical to one GPU.
+ *
+ * desmoe_experts_create_ep: like desmoe_experts_create, but the weight
+ * pointers hold only the owned experts (expert_hi - expert_lo of them) while
+ * `experts` is the pool size M the router sees. */
+int desmoe_experts_create_ep(desmoe_ctx* ctx, int kind, int experts, int expert_lo, int expert_hi,
+                             int hidden, int ffn, const void* w_gate_dev, const void* w_up_dev,
+                             const void* w_down_dev, desmoe_experts** out);
+/* The exchange buffers this rank exposes (each the base of its own
+ * cudaMalloc, ready for cudaIpcGetMemHandle): the two-epoch slot buffer and
+ * the arrival counter. Allocates on first call; synchronises. */
+int desmoe_ep_local_buffers(desmoe_experts* ex, void** slot_buf, size_t* slot_bytes,
+                            void** flag_buf, size_t* flag_bytes);
+/* peer_*[r] = rank r's buffers as mapped in this process (cudaIpcOpenMemHandle;
+ * entry `rank` = this rank's own local buffers). world == 1 disconnects. Every
+ * rank must then call desmoe_layer_forward the same number of times with the
+ * same route configuration (the exchange is per call). */
+int desmoe_ep_connect(desmoe_experts* ex, int world, int rank, void* const* peer_slot_bufs,
+                      void* const* peer_flag_bufs);
+
+/* Cross-process wiring: desmoe_ep_export writes this rank's 128-byte handle
+ * (CUDA IPC handles of its slot buffer and arrival counter); the caller
+ * all-gathers the handles in rank order (any transport: torch.distributed,
+ * MPI, a file) and passes them to desmoe_ep_import, which maps the peers'
+ * buffers (NVLink peer memory) and connects. */
+#define DESMOE_EP_HANDLE_BYTES 128
+int desmoe_ep_export(desmoe_experts* ex, void* handle_out);
+int desmoe_ep_import(desmoe_experts* ex, int world, int rank, const void* handles);
+
 /* Expert FFN + combine for a routed block (moe_forward, gating.cpp:136-157):
  * y[t] = sum over the token's experts in ascending order of gate * expert(x_t).
  * x_dev [n x hidden] bf16, route_* as produced by desmoe_route, y_dev
@@ -201,7 +238,8 @@ int desmoe_router_logits(desmoe_ctx* ctx, const void* x_dev, const void* w_route
 /* ---- whole layer --------------------------------------------------------------
  * router -> activation/top-K -> coreset -> constrained route -> permute ->
  * expert FFN + combine. stats_dev (optional, int[4]): {U unique experts,
- * coreset size, total selections, 0}. */
+ * coreset size, total selections, experts streamed by this rank (= U unless
+ * expert-parallel)}. */
 int desmoe_layer_forward(desmoe_ctx* ctx, const desmoe_experts* ex, const void* w_router_dev,
                          const void* x_dev, int n, const desmoe_route_cfg* cfg, float* y_dev,
                          int* stats_dev, void* stream);

@@ -18,6 +18,7 @@ SOFTMAX, SIGMOID, IDENTITY = 0, 1, 2
 VANILLA, SEQ, VOTE = -1, 0, 1
 VOTE_ACTIVATED, VOTE_RAW_LOGITS = 0, 1
 FFN_SWIGLU, FFN_LINEAR = 0, 1
+EP_HANDLE_BYTES = 128
 
 
 class RouteCfg(C.Structure):
@@ -56,6 +57,13 @@ _SIGS = {
     "desmoe_permute": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "desmoe_experts_create": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, C.POINTER(C.c_void_p)]),
     "desmoe_experts_destroy": (None, [_P]),
+    "desmoe_experts_create_ep": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P,
+                                      C.POINTER(C.c_void_p)]),
+    "desmoe_ep_local_buffers": (_I, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                     C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "desmoe_ep_connect": (_I, [_P, _I, _I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "desmoe_ep_export": (_I, [_P, _P]),
+    "desmoe_ep_import": (_I, [_P, _I, _I, _P]),
     "desmoe_expert_ffn": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
     "desmoe_router_logits": (_I, [_P, _P, _P, _I, _I, _I, _P, _P]),
     "desmoe_layer_forward": (_I, [_P, _P, _P, _P, _I, C.POINTER(RouteCfg), _P, _P, _P]),

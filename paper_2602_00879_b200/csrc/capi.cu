@@ -171,6 +171,16 @@ struct desmoe_ctx {
 struct desmoe_experts {
   desmoe_ctx* ctx = nullptr;
   int kind = 0, m = 0, d = 0, f = 0;
+  int lo = 0, hi = 0;               // owned experts [lo, hi) (all unless expert-parallel)
+  // expert parallelism: exchange buffers this rank exposes to its peers, and
+  // the peers' buffers as mapped in this process
+  int world = 1, rank = 0;
+  float* ep_slot = nullptr;                 // [2][max_n*max_k][d] fp32 (parity halves)
+  unsigned long long* ep_flag = nullptr;    // arrival counter (peers add to it)
+  int* ep_state = nullptr;                  // [0] epoch, [1] combine CTAs done
+  float* peer_slot[kMaxWorld] = {};
+  unsigned long long* peer_flag[kMaxWorld] = {};
+  void* ipc_mapped[2 * kMaxWorld] = {};     // peer buffers opened by desmoe_ep_import
   CUtensorMap wg{}, wu{}, wd{};
   BoxMaps xp_maps{}, h_maps{};
   __nv_bfloat16* x_perm = nullptr;  // [max_n*max_k x d]
@@ -286,6 +296,8 @@ int desmoe_check(desmoe_ctx* c, void* stream) {
   DESMOE_CUDA(cudaMemcpy(&flag, c->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (flag) {
     DESMOE_CUDA(cudaMemset(c->err, 0, sizeof(int)));
+    if (flag == 2)
+      return fail(DESMOE_ECUDA, "expert-parallel exchange timed out (a peer rank stopped)");
     return fail(DESMOE_EINVAL, "non-finite logit");
   }
   return DESMOE_OK;
@@ -626,10 +638,17 @@ int desmoe_permute(desmoe_ctx* c, const int* route_idx, const int* route_cnt, in
 
 int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const void* wg,
                           const void* wu, const void* wd, desmoe_experts** out) {
+  return desmoe_experts_create_ep(c, kind, m, 0, m, d, f, wg, wu, wd, out);
+}
+
+int desmoe_experts_create_ep(desmoe_ctx* c, int kind, int m, int lo, int hi, int d, int f,
+                             const void* wg, const void* wu, const void* wd,
+                             desmoe_experts** out) {
   if (!c || !out) return fail(DESMOE_EINVAL, "null argument");
   if (kind != DESMOE_FFN_SWIGLU && kind != DESMOE_FFN_LINEAR)
     return fail(DESMOE_EINVAL, "unknown expert kind");
   if (m < 1 || m > c->max_m) return fail(DESMOE_EINVAL, "experts outside context capacity");
+  if (lo < 0 || hi > m || lo >= hi) return fail(DESMOE_EINVAL, "owned expert range outside [0, experts)");
   if (kind == DESMOE_FFN_LINEAR) f = d;
   if (d < 128 || d % 128 || d > c->max_d) return fail(DESMOE_EINVAL, "hidden must be a multiple of 128 within capacity");
   if (f < 128 || f % 128) return fail(DESMOE_EINVAL, "ffn must be a multiple of 128");
@@ -641,6 +660,8 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
   ex->m = m;
   ex->d = d;
   ex->f = f;
+  ex->lo = lo;
+  ex->hi = hi;
   const size_t slots = static_cast<size_t>(c->max_n) * c->max_k;
   cudaError_t e = cudaMalloc(&ex->x_perm, slots * d * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ex->h_perm, slots * f * 2);
@@ -653,7 +674,8 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
   }
   int rc = DESMOE_OK;
   // pack the weights into tile-contiguous blocks (one-time)
-  const size_t b_elems = static_cast<size_t>(m) * d * f;
+  const int m_own = hi - lo;  // only the owned experts are packed
+  const size_t b_elems = static_cast<size_t>(m_own) * d * f;
   cudaError_t pe = cudaMalloc(&ex->packed_b, b_elems * 2);
   if (pe == cudaSuccess && kind == DESMOE_FFN_SWIGLU) pe = cudaMalloc(&ex->packed_a, 2 * b_elems * 2);
   if (pe != cudaSuccess) {
@@ -669,12 +691,12 @@ int desmoe_experts_create(desmoe_ctx* c, int kind, int m, int d, int f, const vo
   if (kind == DESMOE_FFN_SWIGLU) {
     pack_weights_kernel<<<1184, 256, 0, ps>>>(static_cast<const uint4*>(wg),
                                               static_cast<const uint4*>(wu),
-                                              static_cast<uint4*>(ex->packed_a), m, f, d, 1);
+                                              static_cast<uint4*>(ex->packed_a), m_own, f, d, 1);
     pack_weights_kernel<<<1184, 256, 0, ps>>>(static_cast<const uint4*>(wd), nullptr,
-                                              static_cast<uint4*>(ex->packed_b), m, d, f, 0);
+                                              static_cast<uint4*>(ex->packed_b), m_own, d, f, 0);
   } else {
     pack_weights_kernel<<<1184, 256, 0, ps>>>(static_cast<const uint4*>(wg), nullptr,
-                                              static_cast<uint4*>(ex->packed_b), m, d, d, 0);
+                                              static_cast<uint4*>(ex->packed_b), m_own, d, d, 0);
   }
   pe = cudaGetLastError();
   if (pe == cudaSuccess) pe = cudaStreamSynchronize(ps);
@@ -710,6 +732,11 @@ void desmoe_experts_destroy(desmoe_experts* ex) {
   if (ex->counters) cudaFree(ex->counters);
   if (ex->packed_a) cudaFree(ex->packed_a);
   if (ex->packed_b) cudaFree(ex->packed_b);
+  for (void* p : ex->ipc_mapped)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (ex->ep_slot) cudaFree(ex->ep_slot);
+  if (ex->ep_flag) cudaFree(ex->ep_flag);
+  if (ex->ep_state) cudaFree(ex->ep_state);
   delete ex;
 }
 
@@ -778,6 +805,18 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.n_members = n_members;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
+  a.expert_lo = ex->lo;
+  a.expert_hi = ex->hi;
+  a.world = ex->world;
+  const size_t slot_stride = static_cast<size_t>(c->max_n) * c->max_k * d;
+  if (ex->world > 1) {
+    for (int r = 0; r < ex->world; ++r) {
+      a.peer_slot[r] = ex->peer_slot[r];
+      a.peer_flag[r] = ex->peer_flag[r];
+    }
+    a.slot_stride = slot_stride;
+    a.epoch = ex->ep_state;
+  }
   const int stage_bytes = 2 * kATile + 2 * a.b_rows * 128;
   const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
                     4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
@@ -814,8 +853,38 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cc.attrs = pdl;
   cc.numAttrs = 1;
-  DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_slots_kernel, static_cast<const float*>(ex->y_slot),
-                                 static_cast<const int*>(c->slot_of), route_cnt, n, k, d, y));
+  CombineArgs ca{};
+  ca.y_slot = ex->world > 1 ? ex->ep_slot : ex->y_slot;
+  ca.slot_of = c->slot_of;
+  ca.route_cnt = route_cnt;
+  ca.n = n;
+  ca.k = k;
+  ca.d = d;
+  ca.y = y;
+  ca.world = ex->world;
+  if (ex->world > 1) {
+    ca.flag = ex->ep_flag;
+    ca.arrivals = static_cast<unsigned long long>(ex->world) * c->num_sms;
+    ca.epoch = ex->ep_state;
+    ca.done_ctas = ex->ep_state + 1;
+    ca.slot_stride = slot_stride;
+    ca.err = c->err;
+  }
+  if (ex->world > 1) {
+    // arrival wait (1 CTA, programmatic behind the FFN), then the combine as
+    // a plain launch: no combine CTA sits resident while peers still stream
+    cudaLaunchConfig_t wc{};
+    wc.gridDim = dim3(1);
+    wc.blockDim = dim3(32);
+    wc.stream = st;
+    wc.attrs = pdl;
+    wc.numAttrs = 1;
+    DESMOE_CUDA(cudaLaunchKernelEx(&wc, ep_wait_kernel, ca));
+    cc.attrs = nullptr;
+    cc.numAttrs = 0;
+    c->launches += 1;
+  }
+  DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_slots_kernel, ca));
   c->launches += 2;
   mark(c, st);
   return DESMOE_OK;
@@ -1198,6 +1267,102 @@ int desmoe_moe_forward_f64(desmoe_ctx* c, const double* w, const double* x, int 
                                                            route_cnt, y);
   DESMOE_LAUNCHED();
   return DESMOE_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// expert parallelism (EP): buffers and peer wiring
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int desmoe_ep_local_buffers(desmoe_experts* ex, void** slot_buf, size_t* slot_bytes,
+                            void** flag_buf, size_t* flag_bytes) {
+  if (!ex || !slot_buf || !slot_bytes || !flag_buf || !flag_bytes)
+    return fail(DESMOE_EINVAL, "null argument");
+  desmoe_ctx* c = ex->ctx;
+  const size_t sb = 2 * static_cast<size_t>(c->max_n) * c->max_k * ex->d * sizeof(float);
+  if (!ex->ep_slot) {
+    // separate allocations, so each is the base of its own IPC handle
+    DESMOE_CUDA(cudaMalloc(&ex->ep_slot, sb));
+    DESMOE_CUDA(cudaMalloc(&ex->ep_flag, 256));
+    DESMOE_CUDA(cudaMalloc(&ex->ep_state, 256));
+    DESMOE_CUDA(cudaMemset(ex->ep_flag, 0, 256));
+    DESMOE_CUDA(cudaMemset(ex->ep_state, 0, 256));
+    DESMOE_CUDA(cudaDeviceSynchronize());
+  }
+  *slot_buf = ex->ep_slot;
+  *slot_bytes = sb;
+  *flag_buf = ex->ep_flag;
+  *flag_bytes = 256;
+  return DESMOE_OK;
+}
+
+int desmoe_ep_connect(desmoe_experts* ex, int world, int rank, void* const* peer_slot_bufs,
+                      void* const* peer_flag_bufs) {
+  if (!ex) return fail(DESMOE_EINVAL, "null argument");
+  if (world < 1 || world > kMaxWorld) return fail(DESMOE_EINVAL, "world outside [1, 8]");
+  if (rank < 0 || rank >= world) return fail(DESMOE_EINVAL, "rank outside [0, world)");
+  if (world > 1) {
+    if (!peer_slot_bufs || !peer_flag_bufs) return fail(DESMOE_EINVAL, "missing peer buffers");
+    if (!ex->ep_slot) return fail(DESMOE_EINVAL, "call desmoe_ep_local_buffers first");
+    for (int r = 0; r < world; ++r)
+      if (!peer_slot_bufs[r] || !peer_flag_bufs[r]) return fail(DESMOE_EINVAL, "null peer buffer");
+    if (peer_slot_bufs[rank] != ex->ep_slot || peer_flag_bufs[rank] != ex->ep_flag)
+      return fail(DESMOE_EINVAL, "own rank's entry must be the local buffers");
+    for (int r = 0; r < world; ++r) {
+      ex->peer_slot[r] = static_cast<float*>(peer_slot_bufs[r]);
+      ex->peer_flag[r] = static_cast<unsigned long long*>(peer_flag_bufs[r]);
+    }
+  }
+  ex->world = world;
+  ex->rank = rank;
+  ex->ctx->gkey.ex = nullptr;  // force a re-capture of the layer graph
+  return DESMOE_OK;
+}
+
+int desmoe_ep_export(desmoe_experts* ex, void* handle_out) {
+  if (!ex || !handle_out) return fail(DESMOE_EINVAL, "null argument");
+  void *slot, *flag;
+  size_t sb, fb;
+  int rc = desmoe_ep_local_buffers(ex, &slot, &sb, &flag, &fb);
+  if (rc) return rc;
+  static_assert(sizeof(cudaIpcMemHandle_t) * 2 <= DESMOE_EP_HANDLE_BYTES, "handle size");
+  cudaIpcMemHandle_t h[2];
+  DESMOE_CUDA(cudaIpcGetMemHandle(&h[0], slot));
+  DESMOE_CUDA(cudaIpcGetMemHandle(&h[1], flag));
+  std::memset(handle_out, 0, DESMOE_EP_HANDLE_BYTES);
+  std::memcpy(handle_out, h, sizeof(h));
+  return DESMOE_OK;
+}
+
+int desmoe_ep_import(desmoe_experts* ex, int world, int rank, const void* handles) {
+  if (!ex || !handles) return fail(DESMOE_EINVAL, "null argument");
+  if (world < 1 || world > kMaxWorld) return fail(DESMOE_EINVAL, "world outside [1, 8]");
+  if (rank < 0 || rank >= world) return fail(DESMOE_EINVAL, "rank outside [0, world)");
+  void *slot, *flag;
+  size_t sb, fb;
+  int rc = desmoe_ep_local_buffers(ex, &slot, &sb, &flag, &fb);
+  if (rc) return rc;
+  void* slots[kMaxWorld] = {};
+  void* flags[kMaxWorld] = {};
+  const unsigned char* hb = static_cast<const unsigned char*>(handles);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      slots[r] = slot;
+      flags[r] = flag;
+      continue;
+    }
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(h, hb + static_cast<size_t>(r) * DESMOE_EP_HANDLE_BYTES, sizeof(h));
+    for (int b = 0; b < 2; ++b) {
+      void* p = nullptr;
+      DESMOE_CUDA(cudaIpcOpenMemHandle(&p, h[b], cudaIpcMemLazyEnablePeerAccess));
+      ex->ipc_mapped[2 * r + b] = p;
+      (b == 0 ? slots : flags)[r] = p;
+    }
+  }
+  return desmoe_ep_connect(ex, world, rank, slots, flags);
 }
 
 }  // extern "C"

@@ -67,8 +67,8 @@ __device__ inline int ascending_rank(int my, int lane, int cnt) {
 // (nullptr = all) in (p desc, index asc) order — the reference's
 // select_top_gates order (gating.cpp:42-71). Rank-ordered result in sel[0..k)
 // (written by every lane). Lane l owns elements l, l+32, ... (m <= 1024).
-__device__ inline void warp_select(const double* p, int m, int k, const uint8_t* allow,
-                                   int* sel) {
+static __device__ __noinline__ void warp_select(const double* p, int m, int k,
+                                                const uint8_t* allow, int* sel) {
   const int lane = threadIdx.x & 31;
   uint32_t taken = 0;
   uint64_t bk = 0;
@@ -115,8 +115,9 @@ __device__ inline uint64_t packed_key(double v, int i) {
   return (order_key(v) & ~0x3FFull) | static_cast<uint64_t>(1023 - i);
 }
 
-__device__ inline void warp_topk_packed(const double* val, int m, int rounds,
-                                        const uint8_t* allow, int* sel, uint64_t* keys) {
+static __device__ __noinline__ void warp_topk_packed(const double* val, int m, int rounds,
+                                                     const uint8_t* allow, int* sel,
+                                                     uint64_t* keys) {
   const int lane = threadIdx.x & 31;
   uint32_t taken = 0;
   auto local_best = [&]() -> uint64_t {
@@ -146,6 +147,14 @@ __device__ inline void warp_topk_packed(const double* val, int m, int rounds,
   }
   __syncwarp();
 }
+
+// Out-of-line fp64 exp and division (IEEE round-to-nearest, as the reference's
+// std::exp / operator/): the routing kernels execute these once per element
+// from many sites; one shared copy keeps their code (and instruction fetch
+// after an L2 flush) small.
+static __device__ __noinline__ double exp_f64(double x) { return exp(x); }
+static __device__ __noinline__ double div_f64(double a, double b) { return a / b; }
+static __device__ __noinline__ double sigmoid_f64(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 // Truncated key of a packed key (drops the index bits).
 __device__ inline uint64_t key_value_part(uint64_t pk) { return pk >> 10; }
@@ -362,6 +371,16 @@ __device__ inline bool elect_one() {
 }
 
 // gpu-scope acquire load / release add for cross-CTA flags
+__device__ inline unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ inline void atomic_add_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ inline int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -205,10 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   pdl_launch_dependents();  // the combine kernel may launch; it waits for us
   pdl_wait();               // route + zeroed counters from the routing kernel
+  const size_t ep_half = a.world > 1 ? (static_cast<size_t>(*a.epoch) & 1u) * a.slot_stride : 0;
 
   // ---- prologue: permutation (redundantly per CTA) ------------------------
   for (int i = tid; i < m; i += kThreads) t.count[i] = 0;
   for (int i = tid; i < m * tw; i += kThreads) bits[i] = 0;
+  if (tid == 0) t.scalars[2] = 0;
   __syncthreads();
   for (int e = tid; e < n_tok * k; e += kThreads) {
     const int tok = e / k, j = e - tok * k;
@@ -218,15 +220,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     atomicOr(&bits[x * tw + (tok >> 5)], 1u << (tok & 31));
   }
   __syncthreads();
+  // active experts = the owned ones (all of them unless expert-parallel)
+  const int lo = a.expert_lo, hi = a.expert_hi;
+  int u_all = 0;
   for (int i = tid; i < m; i += kThreads) {
     t.offset[i] = t.count[i];
-    act_pos[i] = t.count[i] > 0 ? 1 : 0;
+    act_pos[i] = (t.count[i] > 0 && i >= lo && i < hi) ? 1 : 0;
+    u_all += t.count[i] > 0;
   }
+  u_all = __reduce_add_sync(0xffffffffu, u_all);
+  if (lane == 0) atomicAdd(&t.scalars[2], u_all);
   __syncthreads();
   const int total_slots = block_exclusive_scan(t.offset, m, warp_sums);
   const int U = block_exclusive_scan(act_pos, m, warp_sums);
   for (int i = tid; i < m; i += kThreads)
-    if (t.count[i] > 0) t.active[act_pos[i]] = i;
+    if (t.count[i] > 0 && i >= lo && i < hi) t.active[act_pos[i]] = i;
   for (int e = tid; e < n_tok * k; e += kThreads) {
     const int tok = e / k, j = e - tok * k;
     if (j >= a.route_cnt[tok]) {
@@ -251,10 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (blockIdx.x == 0) {  // products the combine kernel and the caller read
     for (int e = tid; e < n_tok * k; e += kThreads) a.slot_of[e] = t.slot_of[e];
     if (tid == 0 && a.stats) {
-      a.stats[0] = U;
-      a.stats[1] = a.n_members ? *a.n_members : U;
+      a.stats[0] = t.scalars[2];  // unique experts of the block (all ranks)
+      a.stats[1] = a.n_members ? *a.n_members : t.scalars[2];
       a.stats[2] = total_slots;
-      a.stats[3] = 0;
+      a.stats[3] = U;             // experts this rank streams
     }
   }
   // gather this CTA's share of token rows into x_perm: every thread issues
@@ -263,8 +271,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int vec = d / 8;
     const uint4* src = reinterpret_cast<const uint4*>(a.x);
     uint4* dst = reinterpret_cast<uint4*>(a.x_perm);
-    const int my_rows = total_slots > static_cast<int>(blockIdx.x)
-                            ? (total_slots - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1
+    // only the owned experts' slot rows (a contiguous slot range)
+    const int row0 = lo < m ? (lo > 0 ? t.offset[lo] : 0) : total_slots;
+    const int row1 = hi < m ? t.offset[hi] : total_slots;
+    const int nrows = row1 - row0;
+    const int my_rows = nrows > static_cast<int>(blockIdx.x)
+                            ? (nrows - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1
                             : 0;
     const int items = my_rows * vec;
     constexpr int kU = 4;
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kThreads;
         if (i < items) {
-          const int row = blockIdx.x + (i / vec) * gridDim.x;
+          const int row = row0 + blockIdx.x + (i / vec) * gridDim.x;
           v[u] = src[static_cast<size_t>(t.slot_token[row]) * vec + (i % vec)];
         }
       }
@@ -282,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kThreads;
         if (i < items) {
-          const int row = blockIdx.x + (i / vec) * gridDim.x;
+          const int row = row0 + blockIdx.x + (i / vec) * gridDim.x;
           dst[static_cast<size_t>(row) * vec + (i % vec)] = v[u];
         }
       }
@@ -328,8 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&full[s], 2 * kATile);
           // packed weights: tile-contiguous 16 KB blocks in (expert, row tile,
           // K block) order, so a unit streams one contiguous region
-          const int tile0 = phaseA ? (ui.expert * tilesA + ui.tile) * (2 * ksA) + 2 * ks
-                                   : (ui.expert * tilesB + ui.tile) * (2 * ksB) + 2 * ks;
+          const int el = ui.expert - lo;  // packed weights hold the owned experts only
+          const int tile0 = phaseA ? (el * tilesA + ui.tile) * (2 * ksA) + 2 * ks
+                                   : (el * tilesB + ui.tile) * (2 * ksB) + 2 * ks;
           const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
           tma_load_3d(st, wmap, &full[s], 0, 0, tile0, pol_w);
           tma_load_3d(st + kATile, wmap, &full[s], 0, 0, tile0 + 1, pol_w);
@@ -472,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           named_bar_sync(1, 128);
         }
-      } else {
+      } else if (a.world <= 1) {
         float* yrow = a.y_slot + static_cast<size_t>(ui.brow) * d + ui.tile * kBM + r;
         for (int c0 = 0; c0 < n_mma; c0 += 16) {
           float v[16];
@@ -482,6 +495,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = c0 + j;
             if (col < ui.count)
               yrow[static_cast<size_t>(col) * d] = v[j] * t.slot_gate[ui.brow + col];
+          }
+        }
+      } else {
+        // expert parallel: push the gate-scaled rows straight into every
+        // rank's slot buffer (own + NVLink peers) while later tiles stream
+        const size_t off = ep_half + static_cast<size_t>(ui.brow) * d + ui.tile * kBM + r;
+        for (int c0 = 0; c0 < n_mma; c0 += 16) {
+          float v[16];
+          tmem_ld16(lane_base + c0, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = c0 + j;
+            if (col < ui.count) {
+              const float val = v[j] * t.slot_gate[ui.brow + col];
+              for (int p = 0; p < a.world; ++p)
+                __stcg(a.peer_slot[p] + off + static_cast<size_t>(col) * d, val);
+            }
           }
         }
       }
@@ -500,6 +530,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
+  if (a.world > 1 && tid == 0) {
+    // every slot row this CTA pushed is visible system-wide before the
+    // arrival (fence cumulativity over the CTA barrier above)
+    __threadfence_system();
+    for (int p = 0; p < a.world; ++p) atomic_add_release_sys(a.peer_flag[p], 1ull);
+  }
   if (tid == 0) trace(a.trace, a.trace_cap, 5, -1);
   if (warp == 2) {
     tc_fence_after();
@@ -542,35 +578,77 @@ __global__ void pack_weights_kernel(const uint4* __restrict__ src, const uint4* 
 
 // Ordered combine (moe_forward's order, gating.cpp:141-155): y[t][c] = sum
 // over j ascending (= ascending expert) of y_slot[slot_of[t][j]][c]. Launched
-// with programmatic stream serialisation behind the FFN kernel.
-__global__ void __launch_bounds__(256)
-    combine_slots_kernel(const float* __restrict__ y_slot, const int* __restrict__ slot_of,
-                         const int* __restrict__ route_cnt, int n, int k, int d,
-                         float* __restrict__ y) {
+// with programmatic stream serialisation behind the FFN kernel. Expert
+// parallel: every rank holds every slot row (pushed by the owners), so the
+// sum is the same sequence of fp32 adds as on one GPU — bit-identical.
+// Expert-parallel arrival wait: ONE 32-thread CTA per rank spins (system-
+// scope acquire) until every rank's FFN CTAs signalled this call's epoch,
+// then lets the combine run. Kept out of the combine so a waiting rank holds
+// almost no SM resources (several simulated ranks can share one GPU).
+__global__ void __launch_bounds__(32) ep_wait_kernel(CombineArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int vec = d / 4;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n * vec) return;
-  const int tok = i / vec, c = (i - tok * vec) * 4;
-  const int cnt = route_cnt[tok];
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 v[8];
-  for (int j0 = 0; j0 < cnt; j0 += 8) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j0 + j < cnt)
-        v[j] = __ldcg(reinterpret_cast<const float4*>(
-            y_slot + static_cast<size_t>(slot_of[tok * k + j0 + j]) * d + c));
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j0 + j < cnt) {
-        acc.x += v[j].x;
-        acc.y += v[j].y;
-        acc.z += v[j].z;
-        acc.w += v[j].w;
+  if (threadIdx.x == 0) {
+    const unsigned long long want =
+        (static_cast<unsigned long long>(*a.epoch) + 1ull) * a.arrivals;
+    const uint64_t t0 = gtime();
+    while (ld_acquire_sys(a.flag) < want) {
+      if (gtime() - t0 > 4000000000ull) {  // 4 s: a peer is gone; fail, never hang
+        atomicExch(a.err, 2);
+        break;
       }
+      __nanosleep(100);
+    }
   }
-  *reinterpret_cast<float4*>(y + static_cast<size_t>(tok) * d + c) = acc;
+  __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ int s_epoch;
+  const float* y_slot = a.y_slot;
+  if (a.world > 1) {
+    // ep_wait_kernel established (acquire) that all slot rows arrived
+    if (threadIdx.x == 0) s_epoch = *a.epoch;
+    __syncthreads();
+    y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
+  }
+  const int vec = a.d / 4;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < a.n * vec) {
+    const int tok = i / vec, c = (i - tok * vec) * 4;
+    const int cnt = a.route_cnt[tok];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 v[8];
+    for (int j0 = 0; j0 < cnt; j0 += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j0 + j < cnt)
+          v[j] = __ldcg(reinterpret_cast<const float4*>(
+              y_slot + static_cast<size_t>(a.slot_of[tok * a.k + j0 + j]) * a.d + c));
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j0 + j < cnt) {
+          acc.x += v[j].x;
+          acc.y += v[j].y;
+          acc.z += v[j].z;
+          acc.w += v[j].w;
+        }
+    }
+    *reinterpret_cast<float4*>(a.y + static_cast<size_t>(tok) * a.d + c) = acc;
+  }
+  if (a.world > 1) {
+    // the last CTA to finish advances the epoch (every CTA read it above)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
+        *a.done_ctas = 0;
+        __threadfence();
+        atomicAdd(a.epoch, 1);
+      }
+    }
+  }
 }
 
 }  // namespace desmoe

@@ -264,13 +264,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       const double mx = pmx[lt];
       double ssum = 1.0;
       if (a.act == 0) {
-        for (int i = lane; i < m; i += 32) er[i] = exp(xr[i] - mx);
+        for (int i = lane; i < m; i += 32) er[i] = exp_f64(xr[i] - mx);
         __syncwarp();
         ssum = 0.0;
         if (lane == 0)
           for (int i = 0; i < m; ++i) ssum += er[i];  // ascending index (gating.cpp:31-33)
       } else if (a.act == 1) {
-        for (int i = lane; i < m; i += 32) er[i] = 1.0 / (1.0 + exp(-xr[i]));
+        for (int i = lane; i < m; i += 32) er[i] = sigmoid_f64(xr[i]);
       } else {
         for (int i = lane; i < m; i += 32) er[i] = xr[i];
       }
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       const double* key_src = xr;
       if (a.act != 0) {
         for (int i = lane; i < m; i += 32)
-          scratch[i] = a.act == 1 ? 1.0 / (1.0 + exp(-xr[i])) : xr[i];
+          scratch[i] = a.act == 1 ? sigmoid_f64(xr[i]) : xr[i];
         __syncwarp();
         key_src = scratch;
       }

@@ -151,6 +151,8 @@ struct TileArgs {  // router GEMM (tile_gemm.cu)
   float* y_out;        // partials [split][token][expert]
 };
 
+constexpr int kMaxWorld = 8;  // expert-parallel ranks (one 8-GPU NVSwitch box)
+
 struct FfnArgs {
   int mode;  // 0 = SwiGLU (phase A + B), 1 = linear expert (phase B on x)
   int n_tok, top_k, m, d, f, b_rows, stages;
@@ -167,6 +169,36 @@ struct FfnArgs {
   const int* n_members;      // optional coreset size
   uint64_t* trace;           // optional timeline buffer ([0] cursor, then pairs)
   int trace_cap;
+  // expert parallelism (world > 1): this rank owns experts [expert_lo,
+  // expert_hi); packed weights hold only those. Phase-B epilogues push every
+  // gate-scaled slot row into all ranks' slot buffers (peer_slot[r], NVLink
+  // peer memory; parity (epoch & 1) selects one of two halves of
+  // slot_stride floats) and each CTA signals every rank's arrival counter at
+  // exit (system-scope release).
+  int expert_lo, expert_hi;
+  int world;
+  float* peer_slot[kMaxWorld];
+  unsigned long long* peer_flag[kMaxWorld];
+  size_t slot_stride;        // floats per parity half
+  const int* epoch;          // device epoch of this rank's layer calls
+};
+
+// Ordered combine arguments (combine_slots_kernel).
+struct CombineArgs {
+  const float* y_slot;       // slot rows (world == 1) or the parity halves (EP)
+  const int* slot_of;        // [n x k]
+  const int* route_cnt;      // [n]
+  int n, k, d;
+  float* y;                  // [n x d]
+  // EP: wait until flag >= (epoch + 1) * arrivals, read half (epoch & 1); the
+  // last CTA to finish advances the epoch
+  int world;
+  const unsigned long long* flag;
+  unsigned long long arrivals;  // world * FFN grid
+  int* epoch;
+  int* done_ctas;
+  size_t slot_stride;
+  int* err;                  // set to 2 on an exchange timeout
 };
 
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }
@@ -179,10 +211,8 @@ __global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,
 __global__ void pack_weights_kernel(const uint4* __restrict__ src, const uint4* __restrict__ src2,
                                     uint4* __restrict__ out, int experts, int rows_per_expert,
                                     int cols, int stacked);
-__global__ void combine_slots_kernel(const float* __restrict__ y_slot,
-                                     const int* __restrict__ slot_of,
-                                     const int* __restrict__ route_cnt, int n, int k, int d,
-                                     float* __restrict__ y);
+__global__ void combine_slots_kernel(CombineArgs a);
+__global__ void ep_wait_kernel(CombineArgs a);
 
 cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,
                          size_t smem, cudaStream_t st);

@@ -23,16 +23,16 @@
 namespace desmoe {
 
 __device__ inline double p_of(const double* row, double s, int act, int i) {
-  return act == 0 ? row[i] / s : row[i];
+  return act == 0 ? div_f64(row[i], s) : row[i];
 }
 
 // Activation of one token row in place; returns the softmax sum (1 otherwise).
 __device__ inline double token_activate(double* row, int m, int act, double mx) {
   const int lane = threadIdx.x & 31;
   if (act == 0) {
-    for (int i = lane; i < m; i += 32) row[i] = exp(row[i] - mx);
+    for (int i = lane; i < m; i += 32) row[i] = exp_f64(row[i] - mx);
   } else if (act == 1) {
-    for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + exp(-row[i]));
+    for (int i = lane; i < m; i += 32) row[i] = sigmoid_f64(row[i]);
   }
   __syncwarp();
   double s = 1.0;
@@ -55,7 +55,7 @@ __device__ inline bool near_tie(double a, double b) {
 // (nullptr = all), exactly in the reference's order for the set and for the
 // prefix of length `k2` (0 = no second boundary). `navail` = number of
 // allowed candidates. scratch: m doubles. Returns the number selected.
-__device__ inline int token_select(const double* row, double s, int act, int m, int k, int k2,
+static __device__ __noinline__ int token_select(const double* row, double s, int act, int m, int k, int k2,
                                    const uint8_t* allow, int navail, int* sel, uint64_t* keys,
                                    double* scratch) {
   const int lane = threadIdx.x & 31;
@@ -85,7 +85,7 @@ __device__ inline void sort_selection(int* sel, int cnt) {
 
 // Writes the token's route: experts ascending, gates renormalised over the
 // selection in ascending index order (gating.cpp:73-82), -1/0 padding.
-__device__ inline void token_write_route(const double* row, double s, int act, int* sel, int cnt,
+static __device__ __noinline__ void token_write_route(const double* row, double s, int act, int* sel, int cnt,
                                          int k, int t, int* route_idx, double* route_gate,
                                          int* route_cnt) {
   const int lane = threadIdx.x & 31;
@@ -98,7 +98,7 @@ __device__ inline void token_write_route(const double* row, double s, int act, i
     const size_t o = static_cast<size_t>(t) * k + lane;
     const bool in = lane < cnt;
     route_idx[o] = in ? sel[lane] : -1;
-    route_gate[o] = in ? p_of(row, s, act, sel[lane]) / ssum : 0.0;
+    route_gate[o] = in ? div_f64(p_of(row, s, act, sel[lane]), ssum) : 0.0;
   }
   if (lane == 0) route_cnt[t] = cnt;
   __syncwarp();
@@ -167,7 +167,7 @@ __device__ inline void lane_load_keys(LaneKeys<P>& L, const double* val, int m,
 // Top-`want` of `val` (restricted to allow) in (value desc, index asc) order
 // of the packed keys, for any m <= 32 * 32 (dispatches on candidates/lane).
 // Runs `rounds` >= want rounds so the caller can inspect the boundary.
-__device__ inline void warp_topk_fast(const double* val, int m, int rounds, const uint8_t* allow,
+static __device__ __noinline__ void warp_topk_fast(const double* val, int m, int rounds, const uint8_t* allow,
                                       int* sel, uint64_t* keys) {
   if (m <= 64) {
     LaneKeys<2> L;
@@ -195,7 +195,7 @@ __device__ inline void warp_topk_fast(const double* val, int m, int rounds, cons
 //   else     relative p gap <= 2^-40.
 // Near-ties re-select exactly on the fp64 probabilities with the reference's
 // comparator. Returns the number selected.
-__device__ inline int token_finish_selection(const double* xr, const double* er, double s,
+static __device__ __noinline__ int token_finish_selection(const double* xr, const double* er, double s,
                                              double mx, int act, int m, int k, int k2,
                                              const uint8_t* allow, int navail, int* sel,
                                              double* scratch) {

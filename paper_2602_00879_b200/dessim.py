@@ -504,22 +504,26 @@ def moe_forward(assign: RoutingAssignment, bank: ExpertBank) -> np.ndarray:
 class ExpertWeights:
     """Registered device-resident bf16 experts (desmoe_experts_create)."""
 
-    def __init__(self, kind, experts, hidden, ffn, tensors):
+    def __init__(self, kind, experts, hidden, ffn, tensors, expert_range=None, ctx=None):
+        """experts = pool size M; expert_range = (lo, hi) owned experts whose
+        weights `tensors` hold (expert parallelism), default all M."""
         self.kind, self.experts, self.hidden, self.ffn = kind, experts, hidden, ffn
+        self.lo, self.hi = expert_range if expert_range is not None else (0, experts)
         self.tensors = tensors  # keep alive
-        self.ctx = _Ctx.get(256, experts, 32, hidden)
+        self.ctx = ctx if ctx is not None else _Ctx.get(256, experts, 32, hidden)
         h = C.c_void_p()
         ptrs = [_ptr(t) if t is not None else None for t in tensors]
         ptrs += [None] * (3 - len(ptrs))
-        check(lib().desmoe_experts_create(self.ctx.h, kind, experts, hidden, ffn, *ptrs,
-                                          C.byref(h)))
+        check(lib().desmoe_experts_create_ep(self.ctx.h, kind, experts, self.lo, self.hi, hidden,
+                                             ffn, *ptrs, C.byref(h)))
         self.h = h
 
     @classmethod
-    def swiglu(cls, w_gate, w_up, w_down):
+    def swiglu(cls, w_gate, w_up, w_down, experts=None, expert_range=None, ctx=None):
         m, f, d = w_gate.shape
-        return cls(_lib.FFN_SWIGLU, m, d, f, (w_gate.contiguous(), w_up.contiguous(),
-                                              w_down.contiguous()))
+        return cls(_lib.FFN_SWIGLU, experts or m, d, f,
+                   (w_gate.contiguous(), w_up.contiguous(), w_down.contiguous()),
+                   expert_range, ctx)
 
     @classmethod
     def linear(cls, w):

@@ -35,11 +35,21 @@ class LayerConfig:
 
 
 class DesMoeLayer:
-    def __init__(self, cfg: LayerConfig, w_router, w_gate, w_up, w_down, max_tokens=256):
+    """One DES MoE layer. With expert_range=(lo, hi), w_gate/w_up/w_down hold
+    only the owned experts of an expert-parallel rank (see ep.py); connect the
+    ranks with ep.connect_distributed / ep.connect_local before forward()."""
+
+    def __init__(self, cfg: LayerConfig, w_router, w_gate, w_up, w_down, max_tokens=256,
+                 expert_range=None, own_context=False):
         import torch
         self.cfg = cfg
         self.w_router = w_router.contiguous()
-        self.experts = ExpertWeights.swiglu(w_gate, w_up, w_down)
+        ctx = None
+        if own_context:  # a private C-ABI context (several simulated ranks per thread)
+            ctx = _Ctx(torch.cuda.current_device(), max_tokens, max(cfg.experts, 256), 32,
+                       max(cfg.hidden, 4096))
+        self.experts = ExpertWeights.swiglu(w_gate, w_up, w_down, experts=cfg.experts,
+                                            expert_range=expert_range, ctx=ctx)
         self.ctx = self.experts.ctx
         self.stats = torch.zeros(4, dtype=torch.int32, device="cuda")
 

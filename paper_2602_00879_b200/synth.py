@@ -86,19 +86,24 @@ def make_expert_bank(experts: int, dim: int, block_size: int, seed: int):
     return w, x
 
 
-def swiglu_weights(experts: int, hidden: int, ffn: int, seed: int, device="cuda"):
-    """Random-init bf16 SwiGLU expert weights: w_gate/w_up [M x F x d] ~
-    N(0,1)/sqrt(d), w_down [M x d x F] ~ N(0,1)/sqrt(F)."""
+def swiglu_weights(experts: int, hidden: int, ffn: int, seed: int, device="cuda",
+                   lo: int = 0, hi=None):
+    """Random-init bf16 SwiGLU expert weights of experts [lo, hi) of an
+    `experts`-expert pool: w_gate/w_up [hi-lo x F x d] ~ N(0,1)/sqrt(d),
+    w_down [hi-lo x d x F] ~ N(0,1)/sqrt(F). Each (expert, matrix) has its own
+    seed mix(seed, 3e + j), so a rank's shard equals the same slice of the
+    full bank (expert parallelism needs no full copy)."""
     import torch
 
+    hi = experts if hi is None else hi
     g = torch.Generator(device=device)
-    g.manual_seed(seed)
     out = []
-    for shape, fan in (((experts, ffn, hidden), hidden), ((experts, ffn, hidden), hidden),
-                       ((experts, hidden, ffn), ffn)):
-        t = torch.empty(shape, dtype=torch.bfloat16, device=device)
-        for e in range(experts):  # per expert keeps the fp32 scratch small
-            t[e] = (torch.randn(shape[1:], generator=g, device=device) / math.sqrt(fan)).to(
+    for j, (shape, fan) in enumerate((((ffn, hidden), hidden), ((ffn, hidden), hidden),
+                                      ((hidden, ffn), ffn))):
+        t = torch.empty((hi - lo,) + shape, dtype=torch.bfloat16, device=device)
+        for e in range(lo, hi):  # per expert keeps the fp32 scratch small
+            g.manual_seed(mix(seed, 3 * e + j) & ((1 << 63) - 1))
+            t[e - lo] = (torch.randn(shape, generator=g, device=device) / math.sqrt(fan)).to(
                 torch.bfloat16)
         out.append(t)
     return tuple(out)
