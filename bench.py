@@ -149,7 +149,7 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(cfg, strategy):
+def config_dict(cfg, strategy, ws=1):
     return {"workload": f"{cfg['desc']}: M={cfg['experts']} experts top-{cfg['top_k']}, "
                         f"d={cfg['hidden']}, SwiGLU F={cfg['ffn']}, block N={cfg['block']}, "
                         f"DES-Vote beta={cfg['beta']}",
@@ -157,7 +157,9 @@ def config_dict(cfg, strategy):
             "ffn": cfg["ffn"], "block_size": cfg["block"], "strategy": strategy,
             "vote_beta": cfg["beta"], "activation": "softmax", "rho": cfg["rho"],
             "l2": "flushed by a 256 MiB write before every timed step",
-            "parallelism": "ep1"}
+            "parallelism": f"ep{ws}" + (" (experts sharded in contiguous ranges; router and "
+                                        "routing replicated; slot rows pushed over NVLink "
+                                        "peer memory)" if ws > 1 else "")}
 
 
 def main():
@@ -183,23 +185,38 @@ def main():
     import ctypes as C
     import numpy as np
     import torch
-    from paper_2602_00879_b200 import _lib, synth
+    from paper_2602_00879_b200 import _lib, ep, synth
     from paper_2602_00879_b200.dessim import _ptr
     from paper_2602_00879_b200.layer import DesMoeLayer, LayerConfig
 
     ws, rank, local = dist_env()
+    # DESMOE_EP_SAME_DEVICE=1: every rank on cuda:0 with a gloo group — a
+    # functional check of the multi-process IPC path on a 1-GPU box (the
+    # processes time-share the GPU, so its timings mean nothing)
+    same_dev = os.environ.get("DESMOE_EP_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, m, k, d, f = cfg["block"], cfg["experts"], cfg["top_k"], cfg["hidden"], cfg["ffn"]
-    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000 + rank)
-    wr = synth.router_weights(m, d, seed=2000 + rank)
+    # expert parallelism: rank r owns a contiguous expert range; router and
+    # routing are replicated, so every rank sees the same weights and tokens
+    lo, hi = ep.partition(m, ws)[rank]
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000, lo=lo, hi=hi)
+    wr = synth.router_weights(m, d, seed=2000)
     lc = LayerConfig(m, k, d, f, strategy="vote", seq_k=3, vote_beta=cfg["beta"])
-    layer = DesMoeLayer(lc, wr, wg, wu, wd)
+    layer = DesMoeLayer(lc, wr, wg, wu, wd, expert_range=(lo, hi))
+    if ws > 1:
+        ep.connect_distributed(layer.experts)
+        torch.distributed.barrier()
     L = _lib.lib()
     total = args.warmup + args.steps
-    xs = [synth.hidden_states(n, d, seed=10_000 * (rank + 1) + i, rho=cfg["rho"])
+    xs = [synth.hidden_states(n, d, seed=10_000 + i, rho=cfg["rho"])
           for i in range(total)]
     y = torch.empty((n, d), dtype=torch.float32, device="cuda")
     x_in = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
@@ -282,7 +299,8 @@ def main():
     t_vote, p_vote, s_vote = results["vote"]
     tot_us = float(t_vote.sum())
     if ws > 1:
-        tt = torch.tensor([tot_us, e2e_us * len(e2e)], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([tot_us, e2e_us * len(e2e)], dtype=torch.float64,
+                          device="cpu" if same_dev else "cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         tot_us, e2e_tot = float(tt[0]), float(tt[1])
         e2e_us = e2e_tot / len(e2e)
@@ -290,20 +308,24 @@ def main():
         if ws > 1:
             torch.distributed.destroy_process_group()
         return
-    value = tot_us / (args.steps * ws)
+    # every rank serves the same block (expert parallel, strong scaling):
+    # µs/block = the slowest rank's time per step
+    value = tot_us / args.steps
     peak, peak_kind = measured_peaks()
     wbytes_per_expert = 3 * d * f * 2
 
     def summarize(name):
         t, p, s = results[name]
-        names = (["router_and_routing", "expert_ffn"] if p.shape[1] == 2
-                 else ["router", "routing", "expert_ffn"])
-        ffn = p[:, -1]
+        names = (["router_and_routing", "expert_ffn", "combine"] if p.shape[1] == 3
+                 else ["router", "routing", "expert_ffn", "combine"])
+        ffn = p[:, -2]
         u = s[:, 0].astype(float)
-        gbps = (u * wbytes_per_expert) / (ffn * 1e-6) / 1e9
+        u_own = s[:, 3].astype(float)  # experts streamed by this rank (= U on 1 GPU)
+        gbps = (u_own * wbytes_per_expert) / (ffn * 1e-6) / 1e9
         return {"us_per_block": round(float(t.mean()), 3),
                 "us_median": round(float(np.median(t)), 3),
                 "unique_experts": round(float(u.mean()), 2),
+                "experts_streamed_rank0": round(float(u_own.mean()), 2),
                 "coreset": round(float(s[:, 1].mean()), 2),
                 "expert_weight_GBps": round(float(gbps.mean()), 1),
                 "phase_us": {nm: round(float(p[:, j].mean()), 2) for j, nm in enumerate(names)}}
@@ -311,27 +333,33 @@ def main():
     summ = {nm: summarize(nm) for nm in results}
     v, van = summ["vote"], summ["vanilla"]
     ffn_us = v["phase_us"]["expert_ffn"]
-    achieved = v["unique_experts"] * wbytes_per_expert / (ffn_us * 1e-6) / 1e9
+    achieved = v["experts_streamed_rank0"] * wbytes_per_expert / (ffn_us * 1e-6) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("ffn_dram_bytes_per_block")
-        except Exception:
-            traffic = None
+    if ws == 1 and not args.block:
+        # DRAM bytes of this kernel on this workload from the committed ncu
+        # --set full capture (tools/ncu_capture.sh -> tools/ncu_summary.py)
+        import glob
+        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{args.config}_r*.json")))
+        if caps:
+            try:
+                traffic = json.load(open(caps[-1])).get("ffn_dram_bytes_per_block")
+            except Exception:
+                traffic = None
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "us/block", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1e3, 6),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, rho-correlated hidden states)",
-        "config": config_dict(cfg, "vote"),
+        "config": config_dict(cfg, "vote", ws),
         "latency_reduction_vs_vanilla": round(1.0 - v["us_per_block"] / van["us_per_block"], 4),
         "unique_expert_reduction_vs_vanilla": round(
             1.0 - v["unique_experts"] / van["unique_experts"], 4),
         "strategies": summ,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "ffn_persistent_kernel (permute + gather + gate/up + down + combine)",
+                     "kernel": "ffn_persistent_kernel (permute + gather + gate/up + down), "
+                               "CUDA events around its launch in the phase pass",
                      "algorithmic_bytes": "U*3*d*F*2 expert-weight bytes per block",
                      "peak_kind": peak_kind},
         "e2e": {"value": round(e2e_us, 3), "unit": "us/block",

@@ -265,8 +265,9 @@ int desmoe_set_graphs(desmoe_ctx* ctx, int enable);
  * When enabled, desmoe_layer_forward records CUDA events on its stream between
  * its phases: [0] router GEMM + gating + coreset + constrained re-route (one
  * cluster kernel; split into [0] router GEMM, [1] routing kernels for shapes
- * outside its envelope), [last] persistent expert FFN (permutation, gather,
- * gate/up + down GEMMs) + ordered combine. desmoe_get_phase_ms synchronises on the last event and writes up
+ * outside its envelope), then the persistent expert FFN (permutation, gather,
+ * gate/up + down GEMMs), [last] (expert-parallel arrival wait +) ordered
+ * combine. desmoe_get_phase_ms synchronises on the last event and writes up
  * to max_phases elapsed times (ms) of the LAST call; returns the number
  * written, or minus a DESMOE_E* code on failure. */
 int desmoe_set_profiling(desmoe_ctx* ctx, int enable);

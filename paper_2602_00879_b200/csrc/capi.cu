@@ -843,6 +843,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   lc.numAttrs = 1;
   DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, ex->wg, ex->wu, ex->wd, ex->xp_maps,
                                  ex->kind == DESMOE_FFN_SWIGLU ? ex->h_maps : ex->xp_maps, a));
+  mark(c, st);  // profiling only: expert FFN | (EP wait +) combine
   // ordered combine, programmatically serialised behind the FFN kernel
   cudaLaunchConfig_t cc{};
   cc.gridDim = dim3((n * (d / 4) + 255) / 256);

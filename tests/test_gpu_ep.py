@@ -71,3 +71,24 @@ def test_ep_rank_without_work():
         assert torch.equal(ys[r], y1)
         idle += layer.stats.cpu().tolist()[3] == 0
     assert idle > 0
+
+
+def test_ep_two_processes_ipc():
+    """Two processes (torchrun) on the same GPU wired through the C ABI's IPC
+    handle export/import — the multi-GPU code path with real cross-process
+    peer mappings; outputs bit-identical to the full layer."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, DESMOE_EP_SAME_DEVICE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr=127.0.0.1",
+                        f"--master-port={port}", os.path.join(root, "tools", "ep_check.py")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert r.stdout.count('"vote": true, "vanilla": true') == 2, r.stdout
