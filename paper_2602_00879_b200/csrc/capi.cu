@@ -995,14 +995,9 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   }
   if (cfg->activation < 0 || cfg->activation > 2)
     return fail(DESMOE_EINVAL, "unknown gate activation");
-  const int b_rows = b_rows_for(n);
-  const int kb_cta = (d / kBK) / kFrontCta;
-  const int mt = (m + kBM - 1) / kBM;
-  int stages = std::min(kb_cta, 4);
-  size_t smem = front_smem_bytes(n, m, k, stages, b_rows);
-  while (smem > static_cast<size_t>(kFrontSmemLimit) && stages > 1)
-    smem = front_smem_bytes(n, m, k, --stages, b_rows);
-  if (smem > static_cast<size_t>(kFrontSmemLimit)) return DESMOE_OK;
+  FrontArgs a{};
+  size_t smem = 0;
+  if (!front_plan(n, m, k, d, &a, &smem)) return DESMOE_OK;
   if (x != c->x_map_ptr || n != c->x_map_n || d != c->x_map_d) {
     int rc = make_box_maps(&c->x_maps, x, n, d);
     if (rc) return rc;
@@ -1017,7 +1012,6 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
     c->wr_map_m = m;
     c->wr_map_d = d;
   }
-  FrontArgs a{};
   a.n = n;
   a.m = m;
   a.k = k;
@@ -1026,13 +1020,6 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.seq_k = cfg->seq_k;
   a.m_core = desmoe_vote_budget(cfg->vote_beta, m);
   a.raw = cfg->vote_source == DESMOE_VOTE_RAW_LOGITS;
-  a.b_rows = b_rows;
-  int bi = 0;
-  while ((16 << bi) < n) ++bi;
-  a.box_index = bi;
-  a.kb_per_cta = kb_cta;
-  a.stages = stages;
-  a.tmem_cols = mt * 256;
   a.route_idx = c->route_idx;
   a.route_gate = c->route_gate;
   a.route_cnt = c->route_cnt;
@@ -1044,6 +1031,7 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.err = c->err;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
+  if (const char* pw = std::getenv("DESMOE_PREWARM")) a.prewarm = std::atoi(pw);
   cudaError_t e = launch_front(c->wr_map, c->x_maps, a, smem, st);
   if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("front kernel: ") + cudaGetErrorString(e));
   c->launches += 1;

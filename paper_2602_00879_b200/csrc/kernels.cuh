@@ -55,12 +55,14 @@ cudaError_t set_fused_route_smem_limit(int bytes);
 
 // ---- front: router GEMM + routing in one thread-block cluster (front.cu) ----
 constexpr int kFrontCta = 8;        // cluster size (portable maximum)
-constexpr int kFrontThreads = 256;
+constexpr int kFrontThreads = 512;
 constexpr int kFrontSmemLimit = 224 * 1024;  // dynamic; leaves room for static smem
 
 struct FrontArgs {
   int n, m, k, act, strategy, seq_k, m_core, raw;
   int b_rows, box_index, kb_per_cta, stages, tmem_cols;
+  int chunk, own_max;  // token chunk of the split-K GEMM; own tokens per CTA bound
+  int prewarm;         // instruction-prefetch walk (bits 0-2 warps, bit 3 route code)
   int* route_idx;      // [n x k]
   double* route_gate;  // [n x k]
   int* route_cnt;      // [n]
@@ -75,7 +77,9 @@ struct FrontArgs {
   int trace_cap;
 };
 
-size_t front_smem_bytes(int n, int m, int k, int stages, int b_rows);
+// Fills the plan fields of `a` (chunk, stages, boxes, TMEM) and the dynamic
+// shared memory; false if the shape is outside the cluster kernel's envelope.
+bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem);
 
 struct CoresetArgs {
   int n, m, k, strategy, seq_k, m_core, raw;

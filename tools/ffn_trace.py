@@ -59,7 +59,7 @@ def main():
     unit = (rec[:, 0] >> 32).astype(np.int64)
     unit[unit >= 2 ** 31] -= 2 ** 32
     t = rec[:, 1].astype(np.int64)
-    t0 = t[ev == 10].min() if (ev == 10).any() else t[ev == 0].min()
+    t0 = t[ev == 40].min() if (ev == 40).any() else t[ev == 0].min()
     t = (t - t0) / 1e3  # µs
     stats = layer.stats.cpu().numpy()
     U = int(stats[0])
@@ -72,6 +72,13 @@ def main():
              20: "front_V_gathered", 21: "front_V_votes", 22: "front_V_ranked",
              33: "L_tok0_start", 30: "L_tok0_loaded", 31: "L_tok0_activated",
              32: "L_tok0_selected"}
+    fnames = ["start", "setup", "drained", "partials_synced", "logits", "rowmax", "activated",
+              "sums_topk", "selected", "sync2", "v_zeroed", "v_gathered", "coreset", "rerouted",
+              "exit"]
+    for i, nm in enumerate(fnames):
+        e_ = 40 + i
+        if (ev == e_).any():
+            out["front_" + nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
     for e_, nm in names.items():
         if (ev == e_).any():
             out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
