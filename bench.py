@@ -14,8 +14,11 @@ grouped SwiGLU expert FFN -> combine.
                   [--config c1|c2|c3|c4] [--block N]
 
 `value` = device-timed µs/block of the DES-Vote layer (inputs resident in HBM,
-L2 flushed by a 256 MiB write before every timed step, CUDA events on the
-layer's stream); `e2e` = the same through the host-buffer C-ABI entry
+CUDA events on the layer's stream); consecutive blocks run through different
+layers of a rotated set with distinct weights (>= 1 GiB of experts), as in a
+real stack, so every expert weight a block streams comes from HBM;
+`value_l2_flushed` repeats the measurement with a 256 MiB L2 flush before
+every block. `e2e` = the same through the host-buffer C-ABI entry
 (desmoe_layer_forward_host: pinned H2D of X, layer, D2H of Y, synchronise).
 `--impl reference` times the reference library's own CPU layer
 (oracle/_ref: des_run + moe_forward with its linear dim x dim experts) on the
@@ -156,7 +159,10 @@ def config_dict(cfg, strategy, ws=1):
             "experts": cfg["experts"], "top_k": cfg["top_k"], "hidden": cfg["hidden"],
             "ffn": cfg["ffn"], "block_size": cfg["block"], "strategy": strategy,
             "vote_beta": cfg["beta"], "activation": "softmax", "rho": cfg["rho"],
-            "l2": "flushed by a 256 MiB write before every timed step",
+            "l2": "not flushed: each block runs the next of several layers with distinct "
+                  "weights (>= 1 GiB of experts rotated; every streamed expert weight comes "
+                  "from HBM); value_l2_flushed repeats vanilla/vote with a 256 MiB L2 flush "
+                  "before every block",
             "parallelism": f"ep{ws}" + (" (experts sharded in contiguous ranges; router and "
                                         "routing replicated; slot rows pushed over NVLink "
                                         "peer memory)" if ws > 1 else "")}
@@ -172,6 +178,8 @@ def main():
     ap.add_argument("--block", type=int, default=0, help="override block size N")
     ap.add_argument("--ref-ffn-tokens", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="distinct layers rotated per block (default: >= 1 GiB of experts)")
     ap.add_argument("--strategies", default="vanilla,seq3,seq2,vote",
                     help="comma list; vote and vanilla are always timed")
     args = ap.parse_args()
@@ -207,30 +215,50 @@ def main():
     # expert parallelism: rank r owns a contiguous expert range; router and
     # routing are replicated, so every rank sees the same weights and tokens
     lo, hi = ep.partition(m, ws)[rank]
-    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000, lo=lo, hi=hi)
-    wr = synth.router_weights(m, d, seed=2000)
     lc = LayerConfig(m, k, d, f, strategy="vote", seq_k=3, vote_beta=cfg["beta"])
-    layer = DesMoeLayer(lc, wr, wg, wu, wd, expert_range=(lo, hi))
+    # A block runs through the next of `nl` layers with distinct weights
+    # (rotation as in a real stack): every expert weight it streams was last
+    # touched nl-1 blocks (>= 0.9 GB of streaming) ago, so it comes from HBM
+    # without flushing L2 between blocks. The flushed variant is timed too.
+    bytes_per_expert = 3 * d * f * 2
+    nl = max(4, min(16, -(-(1 << 30) // (m * bytes_per_expert))))
+    if args.layers:
+        nl = args.layers
+    layers = []
+    for li in range(nl):
+        wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000 + 17 * li, lo=lo, hi=hi)
+        wr = synth.router_weights(m, d, seed=2000 + 17 * li)
+        layers.append(DesMoeLayer(lc, wr, wg, wu, wd, expert_range=(lo, hi), own_context=True))
+        del wg, wu, wd
+        if ws > 1:
+            ep.connect_distributed(layers[-1].experts)
+    torch.cuda.empty_cache()
     if ws > 1:
-        ep.connect_distributed(layer.experts)
         torch.distributed.barrier()
     L = _lib.lib()
     total = args.warmup + args.steps
     xs = [synth.hidden_states(n, d, seed=10_000 + i, rho=cfg["rho"])
           for i in range(total)]
     y = torch.empty((n, d), dtype=torch.float32, device="cuda")
-    x_in = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+    x_ins = [torch.empty((n, d), dtype=torch.bfloat16, device="cuda") for _ in layers]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     ph = (C.c_float * 8)()
 
-    def run(strategy, steps_list, record=True, phases=True):
+    def set_prof(on):
+        for lay in layers:
+            L.desmoe_set_profiling(lay.ctx.h, on)
+
+    def run(strategy, steps_list, record=True, phases=True, l2_flush=False):
         times, ph_list, us = [], [], []
         lc.seq_k = 3 if strategy != "seq2" else 2
         strat = "seq" if strategy.startswith("seq") else strategy
         for i, x in steps_list:
+            layer = layers[i % nl]
+            x_in = x_ins[i % nl]
             x_in.copy_(x)  # the layer's static input buffer (graph replay)
-            flush.fill_(i & 0xFF)
+            if l2_flush:
+                flush.fill_(i & 0xFF)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -258,7 +286,7 @@ def main():
         for strategy in order:
             # timed pass: only the outer events (no event nodes between kernels,
             # so the programmatic launches overlap exactly as in production)
-            L.desmoe_set_profiling(layer.ctx.h, 0)
+            set_prof(0)
             run(strategy, warm, record=False)
             if strategy == "vote":
                 if ws > 1:
@@ -267,29 +295,37 @@ def main():
             t, _, s = run(strategy, timed, phases=False)
             torch.cuda.synchronize()
             # phase pass: CUDA events between the layer's kernels (roofline)
-            L.desmoe_set_profiling(layer.ctx.h, 1)
-            run(strategy, warm[:1], record=False)
+            set_prof(1)
+            run(strategy, warm[:nl], record=False)
             _, p, _ = run(strategy, timed)
             results[strategy] = (np.array(t), np.array(p), np.array(s))
+        # the same with L2 flushed by a 256 MiB write before every block
+        set_prof(0)
+        flushed = {}
+        for strategy in ("vanilla", "vote"):
+            run(strategy, warm, record=False, l2_flush=True)
+            if ws > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            tf, _, _ = run(strategy, timed, phases=False, l2_flush=True)
+            flushed[strategy] = float(np.mean(tf))
     clocks = clk.summary()
-    L.desmoe_set_profiling(layer.ctx.h, 0)
+    set_prof(0)
     run("vote", warm[:1], record=False)
-    launches = L.desmoe_last_launch_count(layer.ctx.h)
+    launches = L.desmoe_last_launch_count(layers[0].ctx.h)
 
     # e2e: host buffers through desmoe_layer_forward_host
     xh = [x.cpu().pin_memory() for _, x in timed]
     yh = torch.empty((n, d), dtype=torch.float32).pin_memory()
     sh = torch.empty(4, dtype=torch.int32).pin_memory()
-    L.desmoe_set_profiling(layer.ctx.h, 0)
-    for _, x in warm:
-        layer.forward_host(x.cpu().pin_memory(), yh, sh, strategy="vote")
+    for i, x in warm:
+        layers[i % nl].forward_host(x.cpu().pin_memory(), yh, sh, strategy="vote")
     e2e = []
     for i, x in enumerate(xh):
-        flush.fill_(i & 0xFF)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        layer.forward_host(x, yh, sh, strategy="vote")
+        layers[i % nl].forward_host(x, yh, sh, strategy="vote")
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e3)
@@ -299,10 +335,11 @@ def main():
     t_vote, p_vote, s_vote = results["vote"]
     tot_us = float(t_vote.sum())
     if ws > 1:
-        tt = torch.tensor([tot_us, e2e_us * len(e2e)], dtype=torch.float64,
-                          device="cpu" if same_dev else "cuda")
+        tt = torch.tensor([tot_us, e2e_us * len(e2e), flushed["vanilla"], flushed["vote"]],
+                          dtype=torch.float64, device="cpu" if same_dev else "cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         tot_us, e2e_tot = float(tt[0]), float(tt[1])
+        flushed = {"vanilla": float(tt[2]), "vote": float(tt[3])}
         e2e_us = e2e_tot / len(e2e)
     if rank != 0:
         if ws > 1:
@@ -353,6 +390,10 @@ def main():
         "dtype": "bf16", "data": "synthetic (random-init weights, rho-correlated hidden states)",
         "config": config_dict(cfg, "vote", ws),
         "latency_reduction_vs_vanilla": round(1.0 - v["us_per_block"] / van["us_per_block"], 4),
+        "layers_rotated": nl,
+        "value_l2_flushed": round(flushed["vote"], 3),
+        "vanilla_l2_flushed": round(flushed["vanilla"], 3),
+        "latency_reduction_vs_vanilla_l2_flushed": round(1.0 - flushed["vote"] / flushed["vanilla"], 4),
         "unique_expert_reduction_vs_vanilla": round(
             1.0 - v["unique_experts"] / van["unique_experts"], 4),
         "strategies": summ,

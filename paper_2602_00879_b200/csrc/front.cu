@@ -49,6 +49,18 @@ __device__ inline void cluster_sync() {
                "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// split cluster barrier: arrive (release: this thread's shared writes become
+// visible cluster-wide; relaxed: nothing to publish) ... wait (acquire)
+__device__ inline void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ inline void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ inline void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // address of the same shared-memory location in CTA `rank` of the cluster
 __device__ inline uint32_t dsmem_addr(const void* local, uint32_t rank) {
   uint32_t r;
@@ -76,6 +88,56 @@ __device__ inline double ld_dsmem_f64(uint32_t addr) {
   return v;
 }
 
+// Asynchronous remote shared-memory stores that complete_tx on the
+// destination CTA's mbarrier: data is pushed to its consumer and signalled
+// without any cluster-scope release fence (those compile to a gpu-scope
+// MEMBAR, measured at ~2.5 us right after the router GEMM's bulk copies).
+__device__ inline void st_async_b32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "r"(v), "r"(rbar)
+               : "memory");
+}
+__device__ inline void st_async_b64(uint32_t raddr, uint64_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "l"(v), "r"(rbar)
+               : "memory");
+}
+// bulk copy of `bytes` (multiple of 16) from this CTA's shared memory to
+// another CTA's (TMA engine), completing tx on that CTA's mbarrier
+__device__ inline void bulk_s2cluster(uint32_t rdst, uint32_t src, uint32_t bytes, uint32_t rbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(rdst),
+      "r"(src), "r"(bytes), "r"(rbar)
+      : "memory");
+}
+
+__device__ inline uint32_t mapa_u32(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ inline void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+// chunk-local token t's owner CTA (largest r with floor(nc r / C) <= t)
+__device__ inline int token_owner(int t, int nc) {
+  int r = kFrontCta - 1;
+#pragma unroll 1
+  while ((nc * r) / kFrontCta > t) --r;
+  return r;
+}
+
 // order-preserving u32 key of an fp32 value (-0 folded onto +0)
 __device__ inline uint32_t fkey(float f) {
   uint32_t u = __float_as_uint(f);
@@ -92,41 +154,52 @@ __device__ __noinline__ double f_exp(double x) { return exp(x); }
 __device__ __noinline__ double f_div(double a, double b) { return a / b; }
 
 // ---------------------------------------------------------------------------
-// Warp selection: the first `rounds` entries of (value desc, index asc) order
-// among i < m (m <= 256) allowed by `allow` (nullptr = all). Softmax keys
-// are (fp32 logit, index) — exact; sigmoid/identity keys pack the fp64
-// activation with the index in its 10 low bits (near-ties re-checked by the
-// caller). Each lane keeps its 8 keys in registers; a round is a local max,
-// two REDUX and a predicated clear of the winner. sel[r] (shared) = index,
-// or -1 once the candidates run out.
+// Warp selection: the first `rounds` entries of (logit desc, index asc) order
+// among i < m (m <= 256) allowed by `allow` (nullptr = all). Every
+// activation is monotone in the logit, so the logit order is the order of
+// the reference's gate values except where rounding makes gates tie — the
+// caller's boundary check (risky_boundary) sends those to the exact path.
+// One 32-bit key per candidate: the order key of the fp32 logit with its 8
+// low bits replaced by (255 - index), so ONE REDUX per round picks (logit
+// desc, index asc) — exact unless two logits agree in their top 24 key bits,
+// which the boundary check also catches. P keys per lane (m <= 32 P).
+// sel[r] (shared) = index, or -1 once the candidates run out.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void warp_rank_select(const float* x, const double* e, int m, int act,
-                                              int rounds, const uint8_t* allow, int* sel) {
+__device__ inline uint32_t sel_key(float x, int i) {
+  return (fkey(x) & 0xFFFFFF00u) | static_cast<uint32_t>(255 - i);
+}
+
+template <int P>
+__device__ __noinline__ void warp_rank_select_p(const float* x, int m, int rounds,
+                                                const uint8_t* allow, int* sel) {
   const int lane = threadIdx.x & 31;
-  uint64_t k[8];
+  uint32_t k[P];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < P; ++s) {
     const int i = lane + 32 * s;
-    uint64_t key = 0;
-    if (i < m && (!allow || allow[i]))
-      key = act == 0 ? ((static_cast<uint64_t>(fkey(x[i])) << 32) | static_cast<uint64_t>(1023 - i))
-                     : packed_key(e[i], i);
-    k[s] = key;
+    k[s] = (i < m && (!allow || allow[i])) ? sel_key(x[i], i) : 0u;
   }
 #pragma unroll 1
   for (int r = 0; r < rounds; ++r) {
-    uint64_t best = k[0];
+    uint32_t best = k[0];
 #pragma unroll
-    for (int s = 1; s < 8; ++s) best = k[s] > best ? k[s] : best;
-    const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(best >> 32));
-    const uint32_t lo = __reduce_max_sync(
-        0xffffffffu, static_cast<uint32_t>(best >> 32) == hi ? static_cast<uint32_t>(best) : 0u);
-    const uint64_t win = (static_cast<uint64_t>(hi) << 32) | lo;
-    if (lane == 0) sel[r] = win ? 1023 - static_cast<int>(lo & 0x3FFu) : -1;
+    for (int s = 1; s < P; ++s) best = k[s] > best ? k[s] : best;
+    const uint32_t win = __reduce_max_sync(0xffffffffu, best);
+    if (lane == 0) sel[r] = win ? 255 - static_cast<int>(win & 0xFFu) : -1;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) k[s] = k[s] == win ? 0ull : k[s];
+    for (int s = 0; s < P; ++s) k[s] = k[s] == win ? 0u : k[s];
   }
   __syncwarp();
+}
+
+__device__ inline void warp_rank_select(const float* x, int m, int rounds, const uint8_t* allow,
+                                        int* sel) {
+  if (m <= 64)
+    warp_rank_select_p<2>(x, m, rounds, allow, sel);
+  else if (m <= 128)
+    warp_rank_select_p<4>(x, m, rounds, allow, sel);
+  else
+    warp_rank_select_p<8>(x, m, rounds, allow, sel);
 }
 
 // Writes a token's route from a rank-ordered selection: experts ascending,
@@ -139,8 +212,8 @@ __device__ __noinline__ void write_route(const double* e, double s, int act, con
   const int lane = threadIdx.x & 31;
   const int my = lane < cnt ? selr[lane] : 0x7fffffff;
   int pos = 0;  // ascending position among the selected (indices are distinct)
-#pragma unroll 1
-  for (int j = 0; j < cnt; ++j) pos += __shfl_sync(0xffffffffu, my, j) < my;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) pos += __shfl_sync(0xffffffffu, my, j) < my;  // pads are INT_MAX
   if (lane >= cnt) pos = lane;  // padding slots cnt .. k-1
   double p = 0.0;
   if (lane < cnt) {
@@ -164,10 +237,14 @@ __device__ __noinline__ void write_route(const double* e, double s, int act, con
 }
 
 // True if the boundary between ranks b-1 and b of `sel` could order
-// differently on the reference's fp64 probabilities (gating.cpp:49-52).
+// differently on the reference's fp64 gate values (gating.cpp:49-52): equal
+// truncated keys (index-ordered by the fast path), a logit gap exp/division
+// rounding could close (<= 2^-40) or an underflowing rejected gate (softmax),
+// or gates within 2^-40 relative of each other (sigmoid/identity).
 __device__ inline bool risky_boundary(const float* x, const double* e, int act, const int* sel,
                                       int b) {
   const int hi = sel[b - 1], lo = sel[b];
+  if ((sel_key(x[hi], hi) >> 8) == (sel_key(x[lo], lo) >> 8)) return true;
   if (act == 0) {
     const double gap = static_cast<double>(x[hi]) - static_cast<double>(x[lo]);
     return !(gap > 0x1.0p-40) || !(e[lo] > 0x1.0p-960);
@@ -187,17 +264,34 @@ __device__ __noinline__ void exact_reselect(const double* e, double s, int act, 
 }
 
 // timeline marks 0..count-1 of this CTA -> trace buffer as events 40 + i
-__device__ __noinline__ void front_dump_marks(const FrontArgs& a, const uint64_t* ts, int tid,
-                                              int count) {
-  if (!a.trace || tid != 0) return;
-  unsigned long long* cur = reinterpret_cast<unsigned long long*>(a.trace);
+__device__ __noinline__ void front_dump_marks(uint64_t* trace, int cap, const uint64_t* ts,
+                                              int tid, int count) {
+  if (!trace || tid != 0) return;
+  unsigned long long* cur = reinterpret_cast<unsigned long long*>(trace);
   const unsigned long long i0 = atomicAdd(cur, static_cast<unsigned long long>(count));
-#pragma unroll 1
   for (int i = 0; i < count; ++i)
-    if (i0 + i < static_cast<unsigned long long>(a.trace_cap)) {
-      a.trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (40 + i);
-      a.trace[3 + 2 * (i0 + i)] = ts[i];
+    if (i0 + i < static_cast<unsigned long long>(cap)) {
+      trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (40 + i);
+      trace[3 + 2 * (i0 + i)] = ts[i];
     }
+}
+
+// Global writes nobody in the cluster reads, issued after the last cluster
+// barrier so no release has to wait for them: the fp32 logits (for
+// desmoe_layer_logits) and the zeroed expert-FFN counters.
+__device__ __noinline__ void front_tail(float* logits_out, int* zero, int zero_words,
+                                        const float* xrow, const int* own_tok, int own, int m,
+                                        int rk, int tid) {
+  if (logits_out) {
+#pragma unroll 1
+    for (int w = tid; w < own * m; w += kFrontThreads) {
+      const int j = w / m, e = w - j * m;
+      logits_out[static_cast<size_t>(own_tok[j]) * m + e] = xrow[w];
+    }
+  }
+#pragma unroll 1
+  for (int i = tid + rk * kFrontThreads; i < zero_words; i += kFrontThreads * kFrontCta)
+    zero[i] = 0;
 }
 
 }  // namespace
@@ -205,33 +299,43 @@ __device__ __noinline__ void front_dump_marks(const FrontArgs& a, const uint64_t
 // Shared-memory plan (host and device agree on it).
 struct FrontSmem {
   size_t ring, erow, dreg, scratch, partial, xrow, mx, ssum, sel, psel, wsel, wp, own_tok, flag,
-      total;
+      allsel, allp, stage, total;
 };
 
 __host__ __device__ inline size_t fr_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int chunk, int own_max,
-                                                      int stages, int b_rows) {
+                                                      int stages, int b_rows, int vote_rows) {
   FrontSmem p{};
   const int mt = (m + kBM - 1) / kBM;
   const size_t ring = static_cast<size_t>(stages) * (mt * kATile + b_rows * 128);
-  const int words = (n + 31) / 32;
   // region A: GEMM ring, later the fp64 activations + the vote workspace
   p.ring = 0;
   p.erow = 0;
   const size_t erow_b = fr_align(static_cast<size_t>(own_max) * (m + 1) * 8, 16);
   p.dreg = erow_b;
-  const size_t nk = static_cast<size_t>(n) * k;
-  size_t dreg_b = nk * 4 + nk * 8 + static_cast<size_t>(m) * words * 4 + 2 * m * 4 + 8 + nk * 8 +
-                  m * 8 + 4 * m * 4 + 64;
+  // vote matrix chunk [vote_rows][m] f64, later votes + keys + rank parts
+  size_t dreg_b = static_cast<size_t>(vote_rows) * m * 8;
+  const size_t rank_b = static_cast<size_t>(m) * (8 + 8 + 16 * 4) + 64;
+  if (rank_b > dreg_b) dreg_b = rank_b;
   p.scratch = p.dreg;  // per-warp fallback scratch aliases the vote workspace
   const size_t scr_b = static_cast<size_t>(kFrontThreads / 32) * m * 8;
   if (scr_b > dreg_b) dreg_b = scr_b;
   size_t a_end = erow_b + fr_align(dreg_b, 16);
   if (ring > a_end) a_end = ring;
-  // region B: partial logits of the current chunk (read remotely)
+  // region B: the partial logits pushed to this CTA for its own tokens of the
+  // current chunk: [sender][own][m]
   p.partial = fr_align(a_end, 1024);
-  size_t o = p.partial + fr_align(static_cast<size_t>(chunk) * m * 4, 16);
+  const int ocm = (chunk + kFrontCta - 1) / kFrontCta;
+  const int m4 = (m + 3) & ~3;
+  size_t o = p.partial + fr_align(static_cast<size_t>(kFrontCta) * ocm * m4 * 4, 16);
+  p.stage = o;  // this CTA's own partial [chunk][m4], copied out in owner blocks
+  o += fr_align(static_cast<size_t>(chunk) * m4 * 4, 16);
+  // every token's selection pushed by its owner: [n][k] ids + weights
+  p.allsel = o;
+  o += fr_align(static_cast<size_t>(n) * k * 4, 16);
+  p.allp = o;
+  o += fr_align(static_cast<size_t>(n) * k * 8, 16);
   // region C: own tokens' rows and selections (read remotely after L)
   p.xrow = o;
   o += fr_align(static_cast<size_t>(own_max) * m * 4, 16);
@@ -262,13 +366,14 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // align to 1024 B by offsetting the shared array itself, so the compiler
   // keeps the shared address space (LDS/STS instead of generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t bars[2 * 4 + 1];
+  __shared__ uint64_t bars[2 * 4 + 3];  // full[4], empty[4], tdone, recv, selx
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
-  __shared__ uint64_t s_ts[16];  // timeline marks (trace buffer only)
+  __shared__ uint64_t s_ts[24];  // timeline marks (trace buffer only)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool tracing = a.trace != nullptr;
+  if (tracing && tid == 0) s_ts[24] = clock64();
 #define FRONT_MARK(ev)                          \
   do {                                          \
     if (tracing && tid == 0) s_ts[ev] = gtime(); \
@@ -280,10 +385,12 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   const int mt = (m + kBM - 1) / kBM;
   const int Tc = a.chunk, nch = (n + Tc - 1) / Tc;
   const int opc = (Tc * (rk + 1)) / C - (Tc * rk) / C;  // own tokens per full chunk
-  const FrontSmem P = front_smem_plan(n, m, k, Tc, a.own_max, a.stages, a.b_rows);
+  const FrontSmem P = front_smem_plan(n, m, k, Tc, a.own_max, a.stages, a.b_rows, a.vote_rows);
   unsigned char* ring = smem + P.ring;
   double* erow = reinterpret_cast<double*>(smem + P.erow);  // [own][m + 1]
-  float* part = reinterpret_cast<float*>(smem + P.partial);  // [Tc][m]
+  float* recv = reinterpret_cast<float*>(smem + P.partial);  // [C][ocm][m4]
+  float* stage = reinterpret_cast<float*>(smem + P.stage);   // [Tc][m4]
+  const int m4 = (m + 3) & ~3;
   float* xrow = reinterpret_cast<float*>(smem + P.xrow);     // [own][m]
   float* mxv = reinterpret_cast<float*>(smem + P.mx);
   double* ssum = reinterpret_cast<double*>(smem + P.ssum);
@@ -297,6 +404,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + 4;
   uint64_t* tdone = bars + 8;
+  uint64_t* bar_recv = bars + 9;  // partials pushed to this CTA (one phase per chunk)
+  uint64_t* bar_selx = bars + 10; // every token's selection pushed to this CTA
+  int* allsel = reinterpret_cast<int*>(smem + P.allsel);       // [n][k]
+  double* allp = reinterpret_cast<double*>(smem + P.allp);     // [n][k]
+  const int ocm = (Tc + C - 1) / C;                            // recv rows per sender
   const int S = a.stages;
   const int stage_bytes = mt * kATile + a.b_rows * 128;
   const int kb_cta = a.kb_per_cta;
@@ -315,9 +427,19 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tdone, 1);
+    mbar_init(bar_recv, 1);
+    mbar_init(bar_selx, 1);
     fence_mbar_init();
     s_bad = 0;
-    const uint64_t pol = l2_policy_evict_first();
+    // arm: chunk 0's partials for this CTA's own tokens from all C senders,
+    // and (DES) every token's top-`depth` selection
+    const int nc0 = n < Tc ? n : Tc;
+    const int own0 = (nc0 * (rk + 1)) / C - (nc0 * rk) / C;
+    mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
+    if (a.strategy >= 0)
+      mbar_arrive_expect_tx(bar_selx,
+                            static_cast<uint32_t>(n * depth * (a.strategy == 1 ? 12 : 4)));
+    const uint64_t pol = l2_policy_evict_last();  // W_r: small, read every call
 #pragma unroll 1
     for (int i = 0; i < kb_cta && i < S; ++i) {
       unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
@@ -328,14 +450,15 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
   }
   if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
-  pdl_launch_dependents();
+  if (!(a.prewarm & 16)) pdl_launch_dependents();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
-#pragma unroll 1
-  for (int i = tid + rk * kFrontThreads; i < a.zero_words; i += kFrontThreads * C) a.zero[i] = 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot[0];
+  // every CTA's barriers are initialised and armed before anyone pushes
+  cluster_arrive_relaxed();
+  cluster_wait();
   FRONT_MARK(1);
 
   // ---- R + L1: per token chunk, split-K GEMM, then the owners' logit sums ----------
@@ -346,7 +469,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     const int nc = n - c0 < Tc ? n - c0 : Tc;
     const int n_mma = (nc + 15) & ~15;
     if (warp == 0 && lane == 0) {
-      const uint64_t pol_w = l2_policy_evict_first();
+      const uint64_t pol_w = l2_policy_evict_last();
       const uint64_t pol_x = l2_policy_evict_last();
 #pragma unroll 1
       for (int i = 0; i < kb_cta; ++i) {
@@ -387,6 +510,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       // drain TMEM: partial[t][e] of this CTA's K slice
       mbar_wait(tdone, c & 1);
       tc_fence_after();
+      if (tracing && warp == 4 && lane == 0 && c == 0) s_ts[18] = gtime();
       const int q = warp & 3;
       const int r = q * 32 + lane;
 #pragma unroll 1
@@ -400,41 +524,56 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           if (e < m) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              if (cc + j < nc) part[(cc + j) * m + e] = v[j];
+              if (cc + j < nc) stage[(cc + j) * m4 + e] = v[j];
           }
         }
       }
       tc_fence_before();
+      if (tracing && warp == 4 && lane == 0 && c == 0) s_ts[19] = gtime();
+      // generic-proxy writes -> visible to the bulk-copy (async) proxy
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar_sync(1, 128);
+      if (warp == 4 && lane < C) {
+        // one bulk copy per owner: its contiguous token rows -> recv[rk] there
+        const int ow = lane;
+        const int lo_q = (nc * ow) / C, hi_q = (nc * (ow + 1)) / C;
+        const uint32_t bytes = static_cast<uint32_t>((hi_q - lo_q) * m4 * 4);
+        if (bytes)
+          bulk_s2cluster(mapa_u32(smem_u32(recv + rk * ocm * m4), ow),
+                         smem_u32(stage + lo_q * m4), bytes, mapa_u32(smem_u32(bar_recv), ow));
+        if (tracing && lane == 0 && c == 0) s_ts[20] = gtime();
+      }
     }
-    __syncthreads();
     FRONT_MARK(2);
-    cluster_sync();  // this chunk's partials are parked in every CTA
+    mbar_wait_cluster(bar_recv, c & 1);  // all C partials of this CTA's tokens arrived
     FRONT_MARK(3);
-    // owners: logits = sum of the 8 partials in fixed CTA order (deterministic)
+    // owners: logits = sum of the C partials in fixed CTA order (deterministic)
     const int lo = (nc * rk) / C, hi = (nc * (rk + 1)) / C;
     const int ob = c * opc;
     const int cnt = (hi - lo) * m;
-    const uint32_t pbase = smem_u32(part);
 #pragma unroll 1
     for (int w = tid; w < cnt; w += kFrontThreads) {
       const int j = w / m, e = w - j * m;
-      const uint32_t off = pbase + static_cast<uint32_t>(((lo + j) * m + e) * 4);
-      float v[C];
-#pragma unroll
-      for (int r = 0; r < C; ++r) {
-        uint32_t ad;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad) : "r"(off), "r"(r));
-        v[r] = ld_dsmem_f32(ad);
-      }
       float acc = 0.0f;
 #pragma unroll
-      for (int r = 0; r < C; ++r) acc += v[r];
+      for (int r = 0; r < C; ++r) acc += recv[(r * ocm + j) * m4 + e];
       xrow[(ob + j) * m + e] = acc;
-      if (a.logits_out) a.logits_out[static_cast<size_t>(c0 + lo + j) * m + e] = acc;
     }
     if (tid < hi - lo) own_tok[ob + tid] = c0 + lo + tid;
     own = ob + (hi - lo);
-    if (c + 1 < nch) cluster_sync();  // partials consumed before the next chunk's drain
+    if (c + 1 < nch) {
+      // re-arm for the next chunk, then a (relaxed) cluster barrier: every
+      // owner consumed this chunk before anyone pushes the next one
+      __syncthreads();
+      if (tid == 0) {
+        const int c1 = c + 1;
+        const int nc1 = n - c1 * Tc < Tc ? n - c1 * Tc : Tc;
+        const int own1 = (nc1 * (rk + 1)) / C - (nc1 * rk) / C;
+        mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own1 * m4 * 4));
+      }
+      cluster_arrive_relaxed();
+      cluster_wait();
+    }
   }
   __syncthreads();
   FRONT_MARK(4);
@@ -483,11 +622,21 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       if (act == 0) {
         s = 0.0;
         const double* er = erow + j * ew;
+        int i = 0;
 #pragma unroll 1
-        for (int i = 0; i < m; ++i) s += er[i];  // ascending index (gating.cpp:31-33)
+        for (; i + 8 <= m; i += 8) {  // ascending index (gating.cpp:31-33)
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = er[i + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) s += v[q];
+        }
+#pragma unroll 1
+        for (; i < m; ++i) s += er[i];
       }
       ssum[j] = s;
     }
+    if (tracing && lane == 0) s_ts[21] = gtime();
   } else {
     const int want = k < m ? k : m;
     const int rounds = want < m ? want + 1 : want;
@@ -496,13 +645,16 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       int* sj = sel + j * 33;
       const float* xr = xrow + j * m;
       const double* er = erow + j * ew;
-      warp_rank_select(xr, er, m, act, rounds, nullptr, sj);
+      long long c0 = clock64();
+      warp_rank_select(xr, m, rounds, nullptr, sj);
+      if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[23] = clock64() - c0;
       if (lane == 0) {
         bool r = want < m && risky_boundary(xr, er, act, sj, want);
         if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
         risky[j] = r;
       }
     }
+    if (tracing && warp == 0 && lane == 0) s_ts[22] = gtime();
   }
   __syncthreads();
   FRONT_MARK(7);
@@ -524,158 +676,124 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
                     a.route_cnt);
       } else if (lane < want) {
         const int e = sj[lane];
-        psel[j * 32 + lane] = a.raw ? static_cast<double>(xrow[j * m + e])
-                                    : (act == 0 ? f_div(er[e], s) : er[e]);
+        const double pv = a.raw ? static_cast<double>(xrow[j * m + e])
+                                : (act == 0 ? f_div(er[e], s) : er[e]);
+        psel[j * 32 + lane] = pv;
+        if (lane < depth) {
+          // broadcast the token's top-`depth` (ids, weights) to every CTA
+          const int t = own_tok[j];
+          const uint32_t ea = smem_u32(allsel + t * k + lane);
+          const uint32_t pa = smem_u32(allp + t * k + lane);
+          const uint32_t ba = smem_u32(bar_selx);
+#pragma unroll 1
+          for (int r = 0; r < C; ++r) {
+            const uint32_t rb = mapa_u32(ba, r);
+            st_async_b32(mapa_u32(ea, r), static_cast<uint32_t>(e), rb);
+            if (a.strategy == 1)
+              st_async_b64(mapa_u32(pa, r), static_cast<uint64_t>(__double_as_longlong(pv)), rb);
+          }
+        }
       }
       __syncwarp();
     }
   }
   __syncthreads();
   FRONT_MARK(8);
-  cluster_sync();  // #2: every CTA's selections are visible
-  FRONT_MARK(9);
-  if (vanilla) {  // every remote read (partials) happened before #2
-    front_dump_marks(a, s_ts, tid, 10);
+  if (vanilla) {
+    // every remote read (partials) is done once all CTAs reach this barrier
+    cluster_arrive_relaxed();
+    cluster_wait();
+    FRONT_MARK(9);
+    front_tail(a.logits_out, a.zero, a.zero_words, xrow, own_tok, own, m, rk, tid);
+    front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 26);
     return;
   }
+  mbar_wait_cluster(bar_selx, 0);       // every token's selection has arrived
+  cluster_arrive_relaxed();             // exit barrier (#3): all pushes landed; wait at the end
+  FRONT_MARK(9);
 
   // ---- V: block coreset, redundantly in every CTA ------------------------------------
-  const int words = (n + 31) / 32;
-  const int nk = n * k;
-  int* tri_e = reinterpret_cast<int*>(smem + P.dreg);                          // [n][k]
-  double* tri_p = reinterpret_cast<double*>(smem + P.dreg + fr_align(nk * 4, 8));  // [n][k]
-  uint32_t* bits = reinterpret_cast<uint32_t*>(tri_p + nk);                    // [m][words]
-  int* ecnt = reinterpret_cast<int*>(bits + m * words);                        // [m]
-  int* eoff = ecnt + m;                                                        // [m]
-  double* val = reinterpret_cast<double*>(
-      smem + fr_align(static_cast<size_t>(reinterpret_cast<unsigned char*>(eoff + m) - smem), 8));
-  double* votes = val + nk;                                                    // [m]
-  int* rankp = reinterpret_cast<int*>(votes + m);                              // [4][m]
+  // DES-Vote: the reference's masked matrix (des.cpp:73-84) in token chunks
+  // of tv rows in shared memory; thread i adds column i over the tokens in
+  // ascending order, zeros included (des.cpp:86-91) — the same fp64 sums.
+  double* dense = reinterpret_cast<double*>(smem + P.dreg);  // [tv][m]
+  const int tv = a.vote_rows;
+  double vsum = 0.0;
 #pragma unroll 1
-  for (int i = tid; i < m; i += kFrontThreads) {
-    flag[i] = 0;
-    ecnt[i] = 0;
-  }
-#pragma unroll 1
-  for (int i = tid; i < m * words; i += kFrontThreads) bits[i] = 0;
-  __syncthreads();
+  for (int i = tid; i < m; i += kFrontThreads) flag[i] = 0;
   FRONT_MARK(10);
-  // gather every token's top-`depth` from its owner CTA (DSMEM)
 #pragma unroll 1
-  for (int w = tid; w < n * depth; w += kFrontThreads) {
-    const int t = w / depth, j = w - t * depth;
-    const int c = t / Tc, l = t - c * Tc;
-    const int nc = n - c * Tc < Tc ? n - c * Tc : Tc;
-    int ow = C - 1;  // owner: largest r with floor(nc r / C) <= l
-    while ((nc * ow) / C > l) --ow;
-    const int lt = c * ((Tc * (ow + 1)) / C - (Tc * ow) / C) + (l - (nc * ow) / C);
-    const int e = ld_dsmem_s32(dsmem_addr(sel + lt * 33 + j, ow));
+  for (int t0 = 0; t0 < n; t0 += (a.strategy == 1 ? tv : n)) {
+    const int nt = a.strategy == 1 ? (n - t0 < tv ? n - t0 : tv) : n;
     if (a.strategy == 1) {
-      tri_e[t * k + j] = e;
-      tri_p[t * k + j] = ld_dsmem_f64(dsmem_addr(psel + lt * 32 + j, ow));
-      atomicAdd(&ecnt[e], 1);
-      atomicOr(&bits[e * words + (t >> 5)], 1u << (t & 31));
-    } else {
-      flag[e] = 1;  // DES-Seq: union of the top-seq_k
+#pragma unroll 1
+      for (int i = tid; i < nt * m; i += kFrontThreads) dense[i] = 0.0;
+      __syncthreads();
     }
+    // scatter the tokens' top-`depth` (pushed by their owners) into the matrix
+#pragma unroll 1
+    for (int w = tid; w < nt * depth; w += kFrontThreads) {
+      const int t = t0 + w / depth, j = w - (w / depth) * depth;
+      const int e = allsel[t * k + j];
+      if (a.strategy == 1)
+        dense[(t - t0) * m + e] = allp[t * k + j];
+      else
+        flag[e] = 1;  // DES-Seq: union of the top-seq_k
+    }
+    __syncthreads();
+    if (a.strategy == 1 && tid < m) {
+      const double* col = dense + tid;
+      int t = 0;
+#pragma unroll 1
+      for (; t + 8 <= nt; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = col[(t + q) * m];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) vsum += v[q];
+      }
+#pragma unroll 1
+      for (; t < nt; ++t) vsum += col[t * m];
+    }
+    if (a.strategy == 1) __syncthreads();  // column reads done before the next chunk
   }
-  __syncthreads();
   FRONT_MARK(11);
   if (a.strategy == 1) {
-    // stable counting sort by expert (ascending token within an expert)
-    if (warp == 0) {
-      int base = 0;
-#pragma unroll 1
-      for (int b0 = 0; b0 < m; b0 += 32) {
-        const int i = b0 + lane;
-        const int v = i < m ? ecnt[i] : 0;
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        if (i < m) eoff[i] = base + incl - v;
-        base += __shfl_sync(0xffffffffu, incl, 31);
-      }
+    double* votes = dense;                                          // [m] (aliases chunk 0)
+    uint64_t* vkey = reinterpret_cast<uint64_t*>(votes + m);        // [m]
+    int* rankp = reinterpret_cast<int*>(vkey + m);                  // [parts][m]
+    if (tid < m) {
+      votes[tid] = vsum;
+      vkey[tid] = order_key(vsum);
+      if (a.votes && rk == 0) a.votes[tid] = vsum;
     }
     __syncthreads();
-#pragma unroll 1
-    for (int w = tid; w < nk; w += kFrontThreads) {
-      const int t = w / k;
-      const int e = tri_e[w];
-      const uint32_t* b = bits + e * words;
-      int before = 0;
-#pragma unroll 1
-      for (int q = 0; q < (t >> 5); ++q) before += __popc(b[q]);
-      before += __popc(b[t >> 5] & ((1u << (t & 31)) - 1u));
-      val[eoff[e] + before] = tri_p[w];
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int i = tid; i < m; i += kFrontThreads) {
-      double v = 0.0;  // every token in ascending order (des.cpp:86-91)
-      const double* vv = val + eoff[i];
-#pragma unroll 1
-      for (int q = 0; q < ecnt[i]; ++q) v += vv[q];
-      votes[i] = v;
-      if (a.votes && rk == 0) a.votes[i] = v;
-    }
-    __syncthreads();
-    // rank of expert i = #experts before it in (vote desc, index asc)
-#pragma unroll 1
-    for (int w = tid; w < 4 * m; w += kFrontThreads) {
-      const int i = w % m, part4 = w / m;
-      const uint64_t ki = order_key(votes[i]);
+    FRONT_MARK(15);
+    // rank of expert i = #experts before it in (vote desc, index asc), the
+    // pool split into `parts` ranges counted by different threads
+    const int parts = kFrontThreads / m < 16 ? kFrontThreads / m : 16;
+    if (tid < parts * m) {
+      const int i = tid % m, part = tid / m;
+      const uint64_t ki = vkey[i];
       int r = 0;
-      const int j0 = (m * part4) / 4, j1 = (m * (part4 + 1)) / 4;
-#pragma unroll 1
+      const int j0 = (m * part) / parts, j1 = (m * (part + 1)) / parts;
+#pragma unroll 4
       for (int j = j0; j < j1; ++j) {
-        const uint64_t kj = order_key(votes[j]);
+        const uint64_t kj = vkey[j];
         r += (kj > ki) | ((kj == ki) & (j < i));
       }
-      rankp[part4 * m + i] = r;
+      rankp[part * m + i] = r;
     }
     __syncthreads();
+    FRONT_MARK(16);
+    if (tid < m) {
+      int r = 0;
 #pragma unroll 1
-    for (int i = tid; i < m; i += kFrontThreads)
-      flag[i] = static_cast<uint8_t>(rankp[i] + rankp[m + i] + rankp[2 * m + i] + rankp[3 * m + i] <
-                                     a.m_core);
-    __syncthreads();
+      for (int q = 0; q < parts; ++q) r += rankp[q * m + tid];
+      flag[tid] = static_cast<uint8_t>(r < a.m_core);
+    }
   }
-  // ascending member list (block scan over chunks of kFrontThreads experts)
-  {
-    int base = 0;
-#pragma unroll 1
-    for (int b0 = 0; b0 < m; b0 += kFrontThreads) {
-      const int i = b0 + tid;
-      const int f = i < m ? flag[i] : 0;
-      const uint32_t bal = __ballot_sync(0xffffffffu, f);
-      if (lane == 0) warp_tot[warp] = __popc(bal);
-      __syncthreads();
-      if (tid == 0) {
-        int acc = 0;
-#pragma unroll 1
-        for (int w = 0; w < NW; ++w) {
-          const int cc = warp_tot[w];
-          warp_tot[w] = acc;
-          acc += cc;
-        }
-        warp_tot[NW] = acc;
-      }
-      __syncthreads();
-      if (f && rk == 0 && a.members)
-        a.members[base + warp_tot[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
-      base += warp_tot[NW];
-      __syncthreads();
-    }
-    if (tid == 0) {
-      s_nm = base;
-      if (rk == 0 && a.n_members) *a.n_members = base;
-    }
-    __syncthreads();
-  }
-  const int nm = s_nm;
+  const int nm = __syncthreads_count(tid < m && flag[tid]);  // m <= 256 < kFrontThreads
   FRONT_MARK(12);
 
   // ---- RR: constrained re-route of own tokens (warp per token) ----------------------
@@ -699,7 +817,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       const int cnt = k < nm ? k : nm;
       if (!covered) {
         const int rounds = cnt < nm ? cnt + 1 : cnt;
-        warp_rank_select(xr, er, m, act, rounds, flag, wsel);  // rank order
+        warp_rank_select(xr, m, rounds, flag, wsel);  // rank order
         const bool r = cnt < nm && risky_boundary(xr, er, act, wsel, cnt);
         if (r) exact_reselect(er, s, act, m, cnt, flag, scratch, wsel);  // rare
       }
@@ -708,9 +826,24 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
   }
   FRONT_MARK(13);
-  cluster_sync();  // #3: no CTA exits while others may still read its shared memory
+  if (tracing && tid == 0) s_ts[25] = clock64();
+  cluster_wait();  // #3: no CTA exits while others may still read its shared memory
   FRONT_MARK(14);
-  front_dump_marks(a, s_ts, tid, 15);
+  if (rk == 0 && a.members && warp == 0) {
+    // ascending coreset members (Coreset::members)
+    int base = 0;
+#pragma unroll 1
+    for (int b0 = 0; b0 < m; b0 += 32) {
+      const int i = b0 + lane;
+      const bool f = i < m && flag[i];
+      const uint32_t bal = __ballot_sync(0xffffffffu, f);
+      if (f) a.members[base + __popc(bal & ((1u << lane) - 1u))] = i;
+      base += __popc(bal);
+    }
+    if (lane == 0 && a.n_members) *a.n_members = base;
+  }
+  front_tail(a.logits_out, a.zero, a.zero_words, xrow, own_tok, own, m, rk, tid);
+  front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 26);
 #undef FRONT_MARK
 }
 
@@ -721,31 +854,33 @@ bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem) {
   if (d % (kBK * kFrontCta)) return false;
   const int mt = (m + kBM - 1) / kBM;
   const int kb_cta = (d / kBK) / kFrontCta;
-  int chunk = n;
-  for (;;) {
+  const int max_stages = kb_cta < 4 ? kb_cta : 4;
+  // prefer: whole block in one GEMM chunk, >= 2 pipeline stages, the whole
+  // vote matrix on chip; shrink the vote chunk first, then the token chunk
+  for (int chunk = n;;) {
     int b_rows = 16;
     while (b_rows < chunk) b_rows <<= 1;
     const int nch = (n + chunk - 1) / chunk;
     const int own_max = nch * ((chunk + kFrontCta - 1) / kFrontCta);
-    int stages = kb_cta < 4 ? kb_cta : 4;
-    FrontSmem p{};
-    for (; stages >= 1; --stages) {
-      p = front_smem_plan(n, m, k, chunk, own_max, stages, b_rows);
-      if (p.total <= static_cast<size_t>(kFrontSmemLimit)) break;
-    }
-    const bool deep_enough = stages >= 2 || kb_cta == 1;
-    if (stages >= 1 && p.total <= static_cast<size_t>(kFrontSmemLimit) && deep_enough) {
-      int bi = 0;
-      while ((16 << bi) < b_rows) ++bi;
-      a->chunk = chunk;
-      a->own_max = own_max;
-      a->stages = stages;
-      a->b_rows = b_rows;
-      a->box_index = bi;
-      a->kb_per_cta = kb_cta;
-      a->tmem_cols = mt * 256;
-      *smem = p.total;
-      return true;
+    for (int vr = n;; vr = vr > 16 ? (vr + 1) / 2 : 0) {
+      if (vr == 0) break;
+      for (int stages = max_stages; stages >= 1; --stages) {
+        if (stages < 2 && kb_cta > 1) break;
+        const FrontSmem p = front_smem_plan(n, m, k, chunk, own_max, stages, b_rows, vr);
+        if (p.total > static_cast<size_t>(kFrontSmemLimit)) continue;
+        int bi = 0;
+        while ((16 << bi) < b_rows) ++bi;
+        a->chunk = chunk;
+        a->own_max = own_max;
+        a->stages = stages;
+        a->b_rows = b_rows;
+        a->box_index = bi;
+        a->kb_per_cta = kb_cta;
+        a->tmem_cols = mt * 256;
+        a->vote_rows = vr;
+        *smem = p.total;
+        return true;
+      }
     }
     if (chunk <= 16) return false;
     chunk = ((chunk / 2) + 15) & ~15;

@@ -62,7 +62,8 @@ struct FrontArgs {
   int n, m, k, act, strategy, seq_k, m_core, raw;
   int b_rows, box_index, kb_per_cta, stages, tmem_cols;
   int chunk, own_max;  // token chunk of the split-K GEMM; own tokens per CTA bound
-  int prewarm;         // instruction-prefetch walk (bits 0-2 warps, bit 3 route code)
+  int vote_rows;       // token rows of the shared-memory vote matrix chunk
+  int prewarm;         // experiment bits (16: trigger the FFN launch at the end)
   int* route_idx;      // [n x k]
   double* route_gate;  // [n x k]
   int* route_cnt;      // [n]

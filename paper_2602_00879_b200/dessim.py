@@ -509,7 +509,8 @@ class ExpertWeights:
         weights `tensors` hold (expert parallelism), default all M."""
         self.kind, self.experts, self.hidden, self.ffn = kind, experts, hidden, ffn
         self.lo, self.hi = expert_range if expert_range is not None else (0, experts)
-        self.tensors = tensors  # keep alive
+        # the caller's tensors are only read while registering (the context
+        # keeps its own tile-packed copy), so they are not retained here
         self.ctx = ctx if ctx is not None else _Ctx.get(256, experts, 32, hidden)
         h = C.c_void_p()
         ptrs = [_ptr(t) if t is not None else None for t in tensors]

@@ -74,7 +74,13 @@ def main():
              32: "L_tok0_selected"}
     fnames = ["start", "setup", "drained", "partials_synced", "logits", "rowmax", "activated",
               "sums_topk", "selected", "sync2", "v_zeroed", "v_gathered", "coreset", "rerouted",
-              "exit"]
+              "exit", "votes", "ranked", "arrived", "mma_done", "drain_done", "copies_issued", "sums_done", "topk_done"]
+    if (ev == 63).any():
+        out["select_cycles"] = int(rec[ev == 63][:, 1].max())
+    if (ev == 64).any() and (ev == 65).any() and (ev == 40).any() and (ev == 53).any():
+        cyc = rec[ev == 65][:, 1].astype(np.int64) - rec[ev == 64][:, 1].astype(np.int64)
+        ns = rec[ev == 53][:, 1].astype(np.int64) - rec[ev == 40][:, 1].astype(np.int64)
+        out["front_sm_mhz"] = [round(float(c) / float(t) * 1e3, 1) for c, t in zip(cyc, ns)]
     for i, nm in enumerate(fnames):
         e_ = 40 + i
         if (ev == e_).any():
