@@ -177,7 +177,10 @@ struct desmoe_experts {
   int world = 1, rank = 0;
   float* ep_slot = nullptr;                 // [2][max_n*max_k][d] fp32 (parity halves)
   unsigned long long* ep_flag = nullptr;    // arrival counter (peers add to it)
-  int* ep_state = nullptr;                  // [0] epoch, [1] combine CTAs done
+  int* ep_state = nullptr;                  // [0] call seq (EP epoch), [1] combine CTAs done
+  // front -> FFN hand-off words (tagged with the call seq, see kernels.cuh)
+  uint64_t* route_words = nullptr;          // [max_n * max_k]
+  uint32_t* pub = nullptr;                  // [1 + max_m]
   float* peer_slot[kMaxWorld] = {};
   unsigned long long* peer_flag[kMaxWorld] = {};
   void* ipc_mapped[2 * kMaxWorld] = {};     // peer buffers opened by desmoe_ep_import
@@ -668,6 +671,13 @@ int desmoe_experts_create_ep(desmoe_ctx* c, int kind, int m, int lo, int hi, int
   if (e == cudaSuccess) e = cudaMalloc(&ex->y_slot, slots * d * 4);
   if (e == cudaSuccess)
     e = cudaMalloc(&ex->counters, sizeof(int) * ffn_counter_words(m, f));
+  if (e == cudaSuccess) e = cudaMemset(ex->counters, 0, sizeof(int) * ffn_counter_words(m, f));
+  if (e == cudaSuccess) e = cudaMalloc(&ex->ep_state, 256);
+  if (e == cudaSuccess) e = cudaMemset(ex->ep_state, 0, 256);
+  if (e == cudaSuccess) e = cudaMalloc(&ex->route_words, slots * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMemset(ex->route_words, 0xFF, slots * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&ex->pub, (static_cast<size_t>(c->max_m) + 1) * 4);
+  if (e == cudaSuccess) e = cudaMemset(ex->pub, 0xFF, (static_cast<size_t>(c->max_m) + 1) * 4);
   if (e != cudaSuccess) {
     desmoe_experts_destroy(ex);
     return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
@@ -737,6 +747,8 @@ void desmoe_experts_destroy(desmoe_experts* ex) {
   if (ex->ep_slot) cudaFree(ex->ep_slot);
   if (ex->ep_flag) cudaFree(ex->ep_flag);
   if (ex->ep_state) cudaFree(ex->ep_state);
+  if (ex->route_words) cudaFree(ex->route_words);
+  if (ex->pub) cudaFree(ex->pub);
   delete ex;
 }
 
@@ -779,7 +791,8 @@ int launch_router_tiles(const CUtensorMap& wa, const BoxMaps& acts, TileArgs a, 
 
 int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
-             const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false) {
+             const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false,
+             bool after_front = false) {
   const int m = ex->m, d = ex->d, f = ex->f;
   if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
   const int words = ffn_counter_words(m, f);
@@ -808,6 +821,13 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.expert_lo = ex->lo;
   a.expert_hi = ex->hi;
   a.world = ex->world;
+  a.epoch = ex->ep_state;
+  a.early = after_front && !std::getenv("DESMOE_NO_EARLY") ? 1 : 0;
+  if (std::getenv("DESMOE_NO_L2PF")) a.flags |= 1;
+  a.pub = ex->pub;
+  a.route_words = ex->route_words;
+  a.wa_base = ex->packed_a;
+  a.wc_base = ex->packed_b;
   const size_t slot_stride = static_cast<size_t>(c->max_n) * c->max_k * d;
   if (ex->world > 1) {
     for (int r = 0; r < ex->world; ++r) {
@@ -815,21 +835,29 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
       a.peer_flag[r] = ex->peer_flag[r];
     }
     a.slot_stride = slot_stride;
-    a.epoch = ex->ep_state;
   }
   const int stage_bytes = 2 * kATile + 2 * a.b_rows * 128;
   const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
                     4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
-  int stages = (kSmemLimit - fixed) / stage_bytes;
+  int stages = (kSmemLimit - 256 - fixed) / stage_bytes;  // 256 B: the kernel's static smem
   stages = std::max(2, std::min(stages, 8));
   if (const char* sv = std::getenv("DESMOE_FFN_STAGES"))  // tuning experiments
     stages = std::max(2, std::min(stages, std::atoi(sv)));
   a.stages = stages;
+  if (4 * (m * ((n + 31) / 32) + 2 * m + n * k) > stage_bytes)
+    return fail(DESMOE_EINVAL, "expert FFN prologue scratch exceeds a pipeline stage");
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
-  if (smem > static_cast<size_t>(kSmemLimit))
+  if (smem > static_cast<size_t>(kSmemLimit - 256))
     return fail(DESMOE_EINVAL, "expert FFN shared-memory plan exceeds 227 KB");
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(c->num_sms);
+  // One CTA per SM. Behind the front kernel (PDL) the FFN CTAs become
+  // resident while it runs — except on the front cluster's SMs, where the
+  // last kFrontCta CTAs start only after it exits: they stream weights but
+  // take no part in the gather handshake.
+  int grid = c->num_sms;
+  if (const char* g = std::getenv("DESMOE_FFN_GRID")) grid = std::max(1, std::atoi(g));
+  lc.gridDim = dim3(grid);
+  a.gather_ctas = after_front && grid > 2 * kFrontCta ? grid - kFrontCta : grid;
   lc.blockDim = dim3(256);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
@@ -863,11 +891,13 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.d = d;
   ca.y = y;
   ca.world = ex->world;
+  ca.epoch = ex->ep_state;
+  ca.done_ctas = ex->ep_state + 1;
+  ca.zero = ex->counters;
+  ca.zero_words = words;
   if (ex->world > 1) {
     ca.flag = ex->ep_flag;
-    ca.arrivals = static_cast<unsigned long long>(ex->world) * c->num_sms;
-    ca.epoch = ex->ep_state;
-    ca.done_ctas = ex->ep_state + 1;
+    ca.arrivals = static_cast<unsigned long long>(ex->world) * grid;
     ca.slot_stride = slot_stride;
     ca.err = c->err;
   }
@@ -1026,8 +1056,9 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.members = c->members;
   a.n_members = c->n_members;
   a.logits_out = c->logits32;
-  a.zero = ex->counters;
-  a.zero_words = ffn_counter_words(ex->m, ex->f);
+  a.seq = ex->ep_state;
+  a.pub = ex->pub;
+  a.route_words = ex->route_words;
   a.err = c->err;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
@@ -1049,6 +1080,7 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   bool zeroed = false;
   rc = front_impl(c, ex, x, w_r, n, cfg, st, &zeroed);
   if (rc) return rc;
+  const bool front_used = zeroed;
   if (!zeroed) {
     // shapes outside the cluster kernel's envelope: split-K router + routing kernels
     int splits = 0;
@@ -1063,7 +1095,8 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   }
   mark(c, st);
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
-                cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed);
+                cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
+                front_used);
   if (rc) return rc;
   return DESMOE_OK;
 }
@@ -1275,9 +1308,7 @@ int desmoe_ep_local_buffers(desmoe_experts* ex, void** slot_buf, size_t* slot_by
     // separate allocations, so each is the base of its own IPC handle
     DESMOE_CUDA(cudaMalloc(&ex->ep_slot, sb));
     DESMOE_CUDA(cudaMalloc(&ex->ep_flag, 256));
-    DESMOE_CUDA(cudaMalloc(&ex->ep_state, 256));
     DESMOE_CUDA(cudaMemset(ex->ep_flag, 0, 256));
-    DESMOE_CUDA(cudaMemset(ex->ep_state, 0, 256));
     DESMOE_CUDA(cudaDeviceSynchronize());
   }
   *slot_buf = ex->ep_slot;

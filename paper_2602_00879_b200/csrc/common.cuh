@@ -242,6 +242,19 @@ __device__ inline void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint6
       : "memory");
 }
 
+// L2 prefetch of a contiguous global range (one bulk instruction)
+__device__ inline void bulk_prefetch_l2(const void* gaddr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gaddr), "r"(bytes) : "memory");
+}
+
+// L2 prefetch of a 3-D tile (no shared memory, no completion tracking)
+__device__ inline void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 // Orders this thread's generic-proxy view (e.g. an acquire of a flag set by a
 // producer CTA) before its subsequent async-proxy (TMA) global reads.
 __device__ inline void fence_proxy_async_global() {
@@ -379,6 +392,18 @@ __device__ inline unsigned long long ld_acquire_sys(const unsigned long long* p)
 
 __device__ inline void atomic_add_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ inline uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ inline uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ inline int ld_acquire(const int* p) {

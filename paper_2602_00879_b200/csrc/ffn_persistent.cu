@@ -174,14 +174,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   t.slot_of = t.active + m;
   t.slot_token = t.slot_of + n_tok * k;
   t.slot_gate = reinterpret_cast<float*>(t.slot_token + n_tok * k);
-  // prologue scratch aliases the ring (unused until the roles start)
+  float* xchg = reinterpret_cast<float*>(t.slot_gate + n_tok * k);  // [16][64] U exchange
+  // prologue scratch in the LAST ring stage: the early weight prefetch fills
+  // at most stages 0..S-2 before the prologue is done
   const int tw = (n_tok + 31) >> 5;
-  uint32_t* bits = reinterpret_cast<uint32_t*>(ring);      // [m][tw]
-  int* act_pos = reinterpret_cast<int*>(bits + m * tw);    // [m]
+  uint32_t* bits = reinterpret_cast<uint32_t*>(ring + static_cast<size_t>(S - 1) * stage_bytes);
+  int* act_pos = reinterpret_cast<int*>(bits + m * tw);             // [m]
+  int* pubm = act_pos + m;                                          // [m] published experts
+  float* gate_tmp = reinterpret_cast<float*>(pubm + m);             // [n*k] staged gates
 
   int* sched = a.counters;
   int* x_ready = a.counters + 1;
-  const int tilesA = f / kHalf, tilesB = d / kBM;
   int* h_ready = a.counters + 2;  // [m][tilesA]
 
   // ---- barrier init / TMEM allocation (independent of the route) ----------
@@ -202,26 +205,148 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
+  __shared__ uint64_t s_pts[8];  // prologue timeline (trace buffer only)
+  __shared__ int s_upub;         // early mode: owned published experts
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   pdl_launch_dependents();  // the combine kernel may launch; it waits for us
-  pdl_wait();               // route + zeroed counters from the routing kernel
-  const size_t ep_half = a.world > 1 ? (static_cast<size_t>(*a.epoch) & 1u) * a.slot_stride : 0;
+  // standalone: route + zeroed counters from the previous kernel. Behind the
+  // front kernel (early mode) nothing waits for its completion: the expert
+  // list and the route arrive as tagged words (see kernels.cuh).
+  if (!a.early) pdl_wait();
+  const int seq = *a.epoch;
+  const uint32_t tag = hand_tag(seq);
+  const int lo = a.expert_lo, hi = a.expert_hi;
+  const int tilesA = f / kHalf, tilesB = d / kBM;
+  const int ksA = d / (2 * kBK);                 // k-steps: 2 K blocks each
+  const int ksB = (swiglu ? f : d) / (2 * kBK);
+  int pre_u = -1, pre_ks = 0;  // early mode: unit claimed and k-steps issued before the prologue
+  if (a.early && warp == 0) {
+    // the published expert list (coreset / union) -> the unit list; claim
+    // the first unit and start streaming its weights while the route is
+    // still being computed (one warp polls the list in parallel)
+    uint32_t w0 = 0;
+    if (lane == 0) {
+      do {
+        w0 = ld_relaxed_u32(a.pub);
+      } while ((w0 >> 10) != tag);
+    }
+    const int cnt = static_cast<int>(__shfl_sync(0xffffffffu, w0, 0) & 1023u);
+    int u = 0;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      int e = -1;
+      if (i < cnt) {
+        uint32_t w;
+        do {
+          w = ld_relaxed_u32(a.pub + 1 + i);
+        } while ((w >> 10) != tag);
+        e = static_cast<int>(w & 1023u);
+      }
+      const bool own = e >= lo && e < hi;
+      const uint32_t bal = __ballot_sync(0xffffffffu, own);
+      if (own) pubm[u + __popc(bal & ((1u << lane) - 1u))] = e;
+      u += __popc(bal);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      s_upub = u;
+      const int n_units0 = (swiglu ? u * tilesA : 0) + u * tilesB;
+      const int u0 = atomicAdd(sched, 1);
+      if (u0 < n_units0) {
+        pre_u = u0;
+        const int nA0 = swiglu ? u * tilesA : 0;
+        const bool phaseA = u0 < nA0;
+        const int ei = phaseA ? u0 / tilesA : (u0 - nA0) / tilesB;
+        const int tile = phaseA ? u0 - ei * tilesA : (u0 - nA0) - ei * tilesB;
+        const int el = pubm[ei] - lo;
+        const int ksteps = phaseA ? ksA : ksB;
+        const uint64_t pol_w = l2_policy_evict_first();
+        const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
+        for (; pre_ks < ksteps && pre_ks < S - 1; ++pre_ks) {
+          unsigned char* st = ring + static_cast<size_t>(pre_ks) * stage_bytes;
+          mbar_arrive_expect_tx(&full[pre_ks], 2 * kATile);
+          const int tile0 = phaseA ? (el * tilesA + tile) * (2 * ksA) + 2 * pre_ks
+                                   : (el * tilesB + tile) * (2 * ksB) + 2 * pre_ks;
+          tma_load_3d(st, wmap, &full[pre_ks], 0, 0, tile0, pol_w);
+          tma_load_3d(st + kATile, wmap, &full[pre_ks], 0, 0, tile0 + 1, pol_w);
+        }
+        // the rest of the unit (one contiguous packed region) goes to L2 now,
+        // so HBM keeps streaming while the prologue waits for the route
+        if (pre_ks < ksteps && !(a.flags & 1)) {
+          const int tile0 = phaseA ? (el * tilesA + tile) * (2 * ksA) + 2 * pre_ks
+                                   : (el * tilesB + tile) * (2 * ksB) + 2 * pre_ks;
+          const unsigned char* base =
+              static_cast<const unsigned char*>(phaseA ? a.wa_base : a.wc_base);
+          bulk_prefetch_l2(base + static_cast<size_t>(tile0) * kATile,
+                           static_cast<uint32_t>((ksteps - pre_ks) * 2 * kATile));
+        }
+      }
+    }
+  }
+  if (a.trace && tid == 0) s_pts[0] = gtime();
+  const size_t ep_half = a.world > 1 ? (static_cast<size_t>(seq) & 1u) * a.slot_stride : 0;
 
   // ---- prologue: permutation (redundantly per CTA) ------------------------
   for (int i = tid; i < m; i += kThreads) t.count[i] = 0;
   for (int i = tid; i < m * tw; i += kThreads) bits[i] = 0;
   if (tid == 0) t.scalars[2] = 0;
   __syncthreads();
+  // route slot e: expert (-1 = none) and gate, staged in shared memory; early
+  // mode: ONE warp per CTA polls the tagged words (all threads polling would
+  // flood L2 while the front is still writing them and the weights stream)
+  int* rexp = t.slot_of;           // staged here until the slot pass rewrites it
+  if (a.early) {
+    if (warp == 1) {
+      // batches of 8 words per lane with every load of a batch in flight at
+      // once; re-poll until the whole batch carries this call's tag
+      const int total = n_tok * k;
+      for (int b0 = 0; b0 < total; b0 += 32 * 8) {
+        uint64_t w[8];
+        bool ok;
+        do {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int e = b0 + j * 32 + lane;
+            w[j] = e < total ? ld_relaxed_u64(a.route_words + e) : 0ull;
+          }
+          ok = true;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int e = b0 + j * 32 + lane;
+            ok &= e >= total || ((static_cast<uint32_t>(w[j]) >> 10) & kTagMask) == tag;
+          }
+          ok = __all_sync(0xffffffffu, ok);
+        } while (!ok);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int e = b0 + j * 32 + lane;
+          if (e < total) {
+            const int x = static_cast<int>(w[j] & 1023u);
+            rexp[e] = x == kPadExpert ? -1 : x;
+            gate_tmp[e] = __uint_as_float(static_cast<uint32_t>(w[j] >> 32));
+          }
+        }
+      }
+    }
+  } else {
+    for (int e = tid; e < n_tok * k; e += kThreads) {
+      const int tok = e / k, j = e - tok * k;
+      const int x = j < a.route_cnt[tok] ? a.route_idx[e] : -1;
+      rexp[e] = x;
+      gate_tmp[e] = x >= 0 ? static_cast<float>(a.route_gate[e]) : 0.0f;
+    }
+  }
+  __syncthreads();
   for (int e = tid; e < n_tok * k; e += kThreads) {
-    const int tok = e / k, j = e - tok * k;
-    if (j >= a.route_cnt[tok]) continue;
-    const int x = a.route_idx[e];
+    const int x = rexp[e];
+    if (x < 0) continue;
+    const int tok = e / k;
     atomicAdd(&t.count[x], 1);
     atomicOr(&bits[x * tw + (tok >> 5)], 1u << (tok & 31));
   }
   __syncthreads();
+  if (a.trace && tid == 0) s_pts[1] = gtime();
   // active experts = the owned ones (all of them unless expert-parallel)
-  const int lo = a.expert_lo, hi = a.expert_hi;
   int u_all = 0;
   for (int i = tid; i < m; i += kThreads) {
     t.offset[i] = t.count[i];
@@ -232,16 +357,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (lane == 0) atomicAdd(&t.scalars[2], u_all);
   __syncthreads();
   const int total_slots = block_exclusive_scan(t.offset, m, warp_sums);
-  const int U = block_exclusive_scan(act_pos, m, warp_sums);
-  for (int i = tid; i < m; i += kThreads)
-    if (t.count[i] > 0 && i >= lo && i < hi) t.active[act_pos[i]] = i;
+  int U = block_exclusive_scan(act_pos, m, warp_sums);
+  if (a.early) {
+    // units run over the published list (a listed expert may get no token
+    // after re-routing: its units stream nothing useful but stay consistent
+    // with the weights already in flight)
+    U = s_upub;
+    for (int i = tid; i < U; i += kThreads) t.active[i] = pubm[i];
+  } else {
+    for (int i = tid; i < m; i += kThreads)
+      if (t.count[i] > 0 && i >= lo && i < hi) t.active[act_pos[i]] = i;
+  }
+  // (each thread rewrites only its own entries e of rexp / slot_of)
   for (int e = tid; e < n_tok * k; e += kThreads) {
-    const int tok = e / k, j = e - tok * k;
-    if (j >= a.route_cnt[tok]) {
+    const int tok = e / k;
+    const int x = rexp[e];
+    if (x < 0) {
       t.slot_of[e] = -1;
       continue;
     }
-    const int x = a.route_idx[e];
     const uint32_t* b = bits + x * tw;
     int before = 0;
     for (int w = 0; w < (tok >> 5); ++w) before += __popc(b[w]);
@@ -249,13 +383,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int slot = t.offset[x] + before;
     t.slot_of[e] = slot;
     t.slot_token[slot] = tok;
-    t.slot_gate[slot] = static_cast<float>(a.route_gate[e]);
+    t.slot_gate[slot] = gate_tmp[e];
   }
   if (tid == 0) {
     t.scalars[0] = U;
     t.scalars[1] = total_slots;
   }
   __syncthreads();
+  if (a.trace && tid == 0) s_pts[2] = gtime();
   if (blockIdx.x == 0) {  // products the combine kernel and the caller read
     for (int e = tid; e < n_tok * k; e += kThreads) a.slot_of[e] = t.slot_of[e];
     if (tid == 0 && a.stats) {
@@ -275,8 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row0 = lo < m ? (lo > 0 ? t.offset[lo] : 0) : total_slots;
     const int row1 = hi < m ? t.offset[hi] : total_slots;
     const int nrows = row1 - row0;
-    const int my_rows = nrows > static_cast<int>(blockIdx.x)
-                            ? (nrows - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1
+    // gather duty: the first a.gather_ctas CTAs (behind the front kernel the
+    // last ones start only when its SMs free up)
+    const int gcta = a.gather_ctas;
+    const int my_rows = static_cast<int>(blockIdx.x) < gcta && nrows > static_cast<int>(blockIdx.x)
+                            ? (nrows - 1 - static_cast<int>(blockIdx.x)) / gcta + 1
                             : 0;
     const int items = my_rows * vec;
     constexpr int kU = 4;
@@ -286,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kThreads;
         if (i < items) {
-          const int row = row0 + blockIdx.x + (i / vec) * gridDim.x;
+          const int row = row0 + blockIdx.x + (i / vec) * gcta;
           v[u] = src[static_cast<size_t>(t.slot_token[row]) * vec + (i % vec)];
         }
       }
@@ -294,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kThreads;
         if (i < items) {
-          const int row = row0 + blockIdx.x + (i / vec) * gridDim.x;
+          const int row = row0 + blockIdx.x + (i / vec) * gcta;
           dst[static_cast<size_t>(row) * vec + (i % vec)] = v[u];
         }
       }
@@ -303,18 +441,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (tid == 0) {
+  if (tid == 0 && static_cast<int>(blockIdx.x) < a.gather_ctas) {
+    if (a.trace) s_pts[3] = gtime();
     __threadfence();
     atomic_add_release(x_ready, 1);
+    if (a.trace) s_pts[4] = gtime();
     trace(a.trace, a.trace_cap, 1, -1);
   }
   const uint32_t tmem_base = *tmem_slot;
 
   const int nA = swiglu ? U * tilesA : 0;
   const int n_units = nA + U * tilesB;
-  const int ksA = d / (2 * kBK);                 // k-steps: 2 K blocks each
-  const int ksB = (swiglu ? f : d) / (2 * kBK);
-  float* xchg = reinterpret_cast<float*>(t.slot_gate + n_tok * k);  // [16][64] U exchange
 
   if (warp == 0) {
     // ============ scheduler + weight producer ============
@@ -323,7 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t it = 0;
       for (int qi = 0;; ++qi) {
         const int q = qi % kQ;
-        const int u = atomicAdd(sched, 1);
+        const bool pre = qi == 0 && a.early;  // claimed (and started) before the prologue
+        const int u = pre ? (pre_u >= 0 ? pre_u : n_units) : atomicAdd(sched, 1);
         const int uu = u < n_units ? u : -1;
         mbar_wait(&qempty[q], ((qi / kQ) & 1) ^ 1);
         unit_q[q] = uu;
@@ -333,7 +471,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
         const bool phaseA = ui.phase == 0;
         const int ksteps = phaseA ? ksA : ksB;
-        for (int ks = 0; ks < ksteps; ++ks, ++it) {
+        const int ks0 = pre ? pre_ks : 0;
+        it += ks0;
+        for (int ks = ks0; ks < ksteps; ++ks, ++it) {
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
@@ -368,8 +508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t box_bytes = (16u << bi) * 128u;
         const BoxMaps& acts = from_x ? xp_maps : h_maps;
         const int ksteps = phaseA ? ksA : ksB;
-        if (from_x && !x_seen) {
-          while (ld_acquire(x_ready) < static_cast<int>(gridDim.x)) {
+        if (from_x && !x_seen && ui.count > 0) {
+          while (ld_acquire(x_ready) < a.gather_ctas) {
           }
           fence_proxy_async_global();
           x_seen = true;
@@ -378,6 +518,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          if (ui.count == 0) {  // a published expert without tokens: no activations
+            mbar_arrive(&full[s]);
+            continue;
+          }
           if (!from_x) {
             // H columns [128 ks, 128 ks + 128) = phase-A tiles 2ks, 2ks+1
             for (int h = 0; h < 2; ++h) {
@@ -422,7 +566,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
         tc_fence_after();
-        if (elect_one()) {
+        if (n_mma == 0) {  // no tokens: release the stage (and the accumulator)
+          if (lane == 0) {
+            mbar_arrive(&empty[s]);
+            if (ks == ksteps - 1) mbar_arrive(&tfull[buf]);
+          }
+        } else if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
           const uint32_t b0 = a0 + 2 * kATile;
 #pragma unroll
@@ -530,6 +679,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
+  if (a.trace && tid == 0) {
+    unsigned long long* cur = reinterpret_cast<unsigned long long*>(a.trace);
+    const unsigned long long i0 = atomicAdd(cur, 5ull);
+    for (int i = 0; i < 5; ++i)
+      if (i0 + i < static_cast<unsigned long long>(a.trace_cap)) {
+        a.trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (70 + i);
+        a.trace[3 + 2 * (i0 + i)] = s_pts[i];
+      }
+  }
   if (a.world > 1 && tid == 0) {
     // every slot row this CTA pushed is visible system-wide before the
     // arrival (fence cumulativity over the CTA barrier above)
@@ -537,6 +695,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int p = 0; p < a.world; ++p) atomic_add_release_sys(a.peer_flag[p], 1ull);
   }
   if (tid == 0) trace(a.trace, a.trace_cap, 5, -1);
+  // early mode never waited for the front kernel: do it before completing, so
+  // the FFN's completion (which the combine waits for) implies the front's
+  if (a.early && tid == 0) pdl_wait();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
@@ -606,29 +767,29 @@ __global__ void __launch_bounds__(32) ep_wait_kernel(CombineArgs a) {
 __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ int s_epoch;
+  if (threadIdx.x == 0) s_epoch = *a.epoch;
+  __syncthreads();
   const float* y_slot = a.y_slot;
-  if (a.world > 1) {
-    // ep_wait_kernel established (acquire) that all slot rows arrived
-    if (threadIdx.x == 0) s_epoch = *a.epoch;
-    __syncthreads();
-    y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
-  }
+  // expert parallel: ep_wait_kernel established (acquire) that every slot row arrived
+  if (a.world > 1) y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
   const int vec = a.d / 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < a.n * vec) {
     const int tok = i / vec, c = (i - tok * vec) * 4;
-    const int cnt = a.route_cnt[tok];
+    const int* so = a.slot_of + tok * a.k;  // ascending experts, -1 padded
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 v[8];
-    for (int j0 = 0; j0 < cnt; j0 += 8) {
+    for (int j0 = 0; j0 < a.k; j0 += 8) {
+      int sl[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sl[j] = j0 + j < a.k ? so[j0 + j] : -1;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j0 + j < cnt)
-          v[j] = __ldcg(reinterpret_cast<const float4*>(
-              y_slot + static_cast<size_t>(a.slot_of[tok * a.k + j0 + j]) * a.d + c));
+        if (sl[j] >= 0)
+          v[j] = __ldcg(reinterpret_cast<const float4*>(y_slot + static_cast<size_t>(sl[j]) * a.d + c));
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j0 + j < cnt) {
+        if (sl[j] >= 0) {
           acc.x += v[j].x;
           acc.y += v[j].y;
           acc.z += v[j].z;
@@ -637,17 +798,15 @@ __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
     }
     *reinterpret_cast<float4*>(a.y + static_cast<size_t>(tok) * a.d + c) = acc;
   }
-  if (a.world > 1) {
-    // the last CTA to finish advances the epoch (every CTA read it above)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      if (atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
-        *a.done_ctas = 0;
-        __threadfence();
-        atomicAdd(a.epoch, 1);
-      }
-    }
+  // the FFN is complete: zero its counters for the next call
+  for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;
+  // the last CTA to finish advances the call sequence number (every CTA read it above)
+  __syncthreads();
+  // (relaxed atomics suffice: each CTA's epoch read completed before its
+  // increment; the bump is published by the kernel's completion)
+  if (threadIdx.x == 0 && atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
+    *a.done_ctas = 0;
+    atomicAdd(a.epoch, 1);
   }
 }
 

@@ -208,7 +208,8 @@ __device__ inline void warp_rank_select(const float* x, int m, int rounds, const
 // wp: 32 doubles of per-warp scratch.
 __device__ __noinline__ void write_route(const double* e, double s, int act, const int* selr,
                                          int cnt, int k, int t, double* wp, int* route_idx,
-                                         double* route_gate, int* route_cnt) {
+                                         double* route_gate, int* route_cnt,
+                                         uint64_t* route_words, uint32_t tag) {
   const int lane = threadIdx.x & 31;
   const int my = lane < cnt ? selr[lane] : 0x7fffffff;
   int pos = 0;  // ascending position among the selected (indices are distinct)
@@ -229,8 +230,13 @@ __device__ __noinline__ void write_route(const double* e, double s, int act, con
   tot = __shfl_sync(0xffffffffu, tot, 0);
   if (lane < k) {
     const size_t o = static_cast<size_t>(t) * k + pos;
+    const double g = lane < cnt ? f_div(p, tot) : 0.0;
     route_idx[o] = lane < cnt ? my : -1;
-    route_gate[o] = lane < cnt ? f_div(p, tot) : 0.0;
+    route_gate[o] = g;
+    // the FFN kernel polls these (tagged with the call number) instead of
+    // waiting for this kernel to complete
+    if (route_words)
+      route_words[o] = route_word(tag, lane < cnt ? my : kPadExpert, static_cast<float>(g));
   }
   if (lane == 0) route_cnt[t] = cnt;
   __syncwarp();
@@ -276,22 +282,43 @@ __device__ __noinline__ void front_dump_marks(uint64_t* trace, int cap, const ui
     }
 }
 
+// Publishes the ascending list of flagged experts (coreset / union): the
+// tagged words the expert-FFN kernel polls to start streaming weights, plus
+// the C-ABI outputs members / n_members. One warp.
+__device__ __noinline__ void publish_list(const uint8_t* flag, int m, uint32_t tag, uint32_t* pub,
+                                          int* members, int* n_members) {
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+#pragma unroll 1
+  for (int b0 = 0; b0 < m; b0 += 32) {
+    const int i = b0 + lane;
+    const bool f = i < m && flag[i];
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    const int pos = base + __popc(bal & ((1u << lane) - 1u));
+    if (f) {
+      if (pub) pub[1 + pos] = pub_word(tag, i);
+      if (members) members[pos] = i;
+    }
+    base += __popc(bal);
+  }
+  if (lane == 0) {
+    if (pub) pub[0] = pub_word(tag, base);
+    if (n_members) *n_members = base;
+  }
+  __syncwarp();
+}
+
 // Global writes nobody in the cluster reads, issued after the last cluster
 // barrier so no release has to wait for them: the fp32 logits (for
 // desmoe_layer_logits) and the zeroed expert-FFN counters.
-__device__ __noinline__ void front_tail(float* logits_out, int* zero, int zero_words,
-                                        const float* xrow, const int* own_tok, int own, int m,
-                                        int rk, int tid) {
-  if (logits_out) {
+__device__ __noinline__ void front_tail(float* logits_out, const float* xrow, const int* own_tok,
+                                        int own, int m, int tid) {
+  if (!logits_out) return;
 #pragma unroll 1
-    for (int w = tid; w < own * m; w += kFrontThreads) {
-      const int j = w / m, e = w - j * m;
-      logits_out[static_cast<size_t>(own_tok[j]) * m + e] = xrow[w];
-    }
+  for (int w = tid; w < own * m; w += kFrontThreads) {
+    const int j = w / m, e = w - j * m;
+    logits_out[static_cast<size_t>(own_tok[j]) * m + e] = xrow[w];
   }
-#pragma unroll 1
-  for (int i = tid + rk * kFrontThreads; i < zero_words; i += kFrontThreads * kFrontCta)
-    zero[i] = 0;
 }
 
 }  // namespace
@@ -439,6 +466,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     if (a.strategy >= 0)
       mbar_arrive_expect_tx(bar_selx,
                             static_cast<uint32_t>(n * depth * (a.strategy == 1 ? 12 : 4)));
+    else if (rk == 0 && a.pub)
+      mbar_arrive_expect_tx(bar_selx, static_cast<uint32_t>(n * k * 4));  // union of top-K
     const uint64_t pol = l2_policy_evict_last();  // W_r: small, read every call
 #pragma unroll 1
     for (int i = 0; i < kb_cta && i < S; ++i) {
@@ -452,6 +481,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
   if (!(a.prewarm & 16)) pdl_launch_dependents();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
+  const uint32_t tag = a.seq ? hand_tag(*a.seq) : 0u;  // this call's hand-off tag
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -673,7 +703,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       if (risky[j]) exact_reselect(er, s, act, m, want, nullptr, scratch, sj);  // rare
       if (vanilla) {
         write_route(er, s, act, sj, want, k, own_tok[j], wp, a.route_idx, a.route_gate,
-                    a.route_cnt);
+                    a.route_cnt, a.route_words, tag);
+        if (a.pub && lane < k)  // the union (unique experts) is published by rank 0
+          st_async_b32(mapa_u32(smem_u32(allsel + own_tok[j] * k + lane), 0),
+                       static_cast<uint32_t>(sj[lane]), mapa_u32(smem_u32(bar_selx), 0));
       } else if (lane < want) {
         const int e = sj[lane];
         const double pv = a.raw ? static_cast<double>(xrow[j * m + e])
@@ -700,11 +733,22 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __syncthreads();
   FRONT_MARK(8);
   if (vanilla) {
-    // every remote read (partials) is done once all CTAs reach this barrier
+    if (rk == 0 && a.pub) {
+      // union of every token's top-K = the experts the FFN will stream
+      mbar_wait_cluster(bar_selx, 0);
+#pragma unroll 1
+      for (int i = tid; i < m; i += kFrontThreads) flag[i] = 0;
+      __syncthreads();
+#pragma unroll 1
+      for (int i = tid; i < n * k; i += kFrontThreads) flag[allsel[i]] = 1;
+      __syncthreads();
+      if (warp == 0) publish_list(flag, m, tag, a.pub, nullptr, nullptr);
+    }
+    // every remote access (partials, ids) is done once all CTAs reach this barrier
     cluster_arrive_relaxed();
     cluster_wait();
     FRONT_MARK(9);
-    front_tail(a.logits_out, a.zero, a.zero_words, xrow, own_tok, own, m, rk, tid);
+    front_tail(a.logits_out, xrow, own_tok, own, m, tid);
     front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 26);
     return;
   }
@@ -794,6 +838,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
   }
   const int nm = __syncthreads_count(tid < m && flag[tid]);  // m <= 256 < kFrontThreads
+  if (rk == 0 && warp == 0) publish_list(flag, m, tag, a.pub, a.members, a.n_members);
   FRONT_MARK(12);
 
   // ---- RR: constrained re-route of own tokens (warp per token) ----------------------
@@ -822,27 +867,14 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
         if (r) exact_reselect(er, s, act, m, cnt, flag, scratch, wsel);  // rare
       }
       write_route(er, s, act, wsel, cnt, k, own_tok[j], wp, a.route_idx, a.route_gate,
-                  a.route_cnt);
+                  a.route_cnt, a.route_words, tag);
     }
   }
   FRONT_MARK(13);
   if (tracing && tid == 0) s_ts[25] = clock64();
   cluster_wait();  // #3: no CTA exits while others may still read its shared memory
   FRONT_MARK(14);
-  if (rk == 0 && a.members && warp == 0) {
-    // ascending coreset members (Coreset::members)
-    int base = 0;
-#pragma unroll 1
-    for (int b0 = 0; b0 < m; b0 += 32) {
-      const int i = b0 + lane;
-      const bool f = i < m && flag[i];
-      const uint32_t bal = __ballot_sync(0xffffffffu, f);
-      if (f) a.members[base + __popc(bal & ((1u << lane) - 1u))] = i;
-      base += __popc(bal);
-    }
-    if (lane == 0 && a.n_members) *a.n_members = base;
-  }
-  front_tail(a.logits_out, a.zero, a.zero_words, xrow, own_tok, own, m, rk, tid);
+  front_tail(a.logits_out, xrow, own_tok, own, m, tid);
   front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 26);
 #undef FRONT_MARK
 }

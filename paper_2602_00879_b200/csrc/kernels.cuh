@@ -71,12 +71,39 @@ struct FrontArgs {
   int* n_members;      // [1]
   double* votes;       // [m] optional
   float* logits_out;   // [n x m] optional fp32 logits
-  int* zero;           // FFN counters to zero
-  int zero_words;
   int* err;
-  uint64_t* trace;     // optional timeline (events 10-17)
+  uint64_t* trace;     // optional timeline (events 40+)
   int trace_cap;
+  // early hand-off to the expert-FFN kernel (no grid-completion wait): the
+  // call sequence number, the published expert list and tagged route words
+  const int* seq;          // [1] bumped by the combine kernel after every call
+  uint32_t* pub;           // [1 + m] {tag | count}, {tag | expert} ...
+  uint64_t* route_words;   // [n x k] {gate f32 | tag | expert}, expert kPadExpert = none
 };
+
+// Tagged hand-off words (front -> FFN). A word is valid for the current call
+// when its 22-bit tag equals the call sequence number (mod 2^22); every word
+// the FFN polls is rewritten by every call, so no flag, fence or reset is
+// needed: the front's stores and the FFN's polling loads meet in L2.
+constexpr uint32_t kTagBits = 22;
+constexpr uint32_t kTagMask = (1u << kTagBits) - 1u;
+constexpr int kPadExpert = 1023;
+__host__ __device__ inline uint32_t hand_tag(int seq) {
+  return static_cast<uint32_t>(seq) & kTagMask;
+}
+__host__ __device__ inline uint32_t pub_word(uint32_t tag, int v) {
+  return (tag << 10) | static_cast<uint32_t>(v & 1023);
+}
+__host__ __device__ inline uint64_t route_word(uint32_t tag, int expert, float gate) {
+  uint32_t g;
+#ifdef __CUDA_ARCH__
+  g = __float_as_uint(gate);
+#else
+  __builtin_memcpy(&g, &gate, 4);
+#endif
+  return (static_cast<uint64_t>(g) << 32) | (static_cast<uint64_t>(tag) << 10) |
+         static_cast<uint64_t>(expert & 1023);
+}
 
 // Fills the plan fields of `a` (chunk, stages, boxes, TMEM) and the dynamic
 // shared memory; false if the shape is outside the cluster kernel's envelope.
@@ -185,7 +212,17 @@ struct FfnArgs {
   float* peer_slot[kMaxWorld];
   unsigned long long* peer_flag[kMaxWorld];
   size_t slot_stride;        // floats per parity half
-  const int* epoch;          // device epoch of this rank's layer calls
+  const int* epoch;          // device call sequence number (= the hand-off seq)
+  // early mode (behind the front kernel): the weight producer starts on the
+  // published expert list and the prologue polls the tagged route words;
+  // otherwise (standalone FFN) the route arrays after griddepcontrol.wait
+  int early;
+  const uint32_t* pub;
+  const uint64_t* route_words;
+  const void* wa_base;       // packed gate/up tiles (L2 prefetch of the first unit)
+  const void* wc_base;       // packed W_d / W_lin tiles
+  int flags;                 // experiments: 1 = no L2 prefetch of the first unit
+  int gather_ctas;           // CTAs that gather x rows (and the x_ready target)
 };
 
 // Ordered combine arguments (combine_slots_kernel).
@@ -200,10 +237,12 @@ struct CombineArgs {
   int world;
   const unsigned long long* flag;
   unsigned long long arrivals;  // world * FFN grid
-  int* epoch;
+  int* epoch;                // call sequence number: bumped by the last CTA
   int* done_ctas;
   size_t slot_stride;
   int* err;                  // set to 2 on an exchange timeout
+  int* zero;                 // FFN counters, zeroed for the next call
+  int zero_words;
 };
 
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }

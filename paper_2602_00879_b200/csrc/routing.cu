@@ -372,7 +372,13 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
 cudaError_t set_kernel_smem_limits() {
   cudaError_t e = cudaSuccess;
   auto set = [&](const void* fn, int bytes) {
-    cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    // dynamic + the kernel's static shared memory must stay within 227 KB
+    cudaFuncAttributes fa{};
+    cudaError_t r = cudaFuncGetAttributes(&fa, fn);
+    const int cap = 227 * 1024 - static_cast<int>(fa.sharedSizeBytes);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               bytes < cap ? bytes : cap);
     if (e == cudaSuccess) e = r;
   };
   const int routing = 200 * 1024;  // leaves room for the kernels' static shared memory

@@ -88,6 +88,10 @@ def main():
     for e_, nm in names.items():
         if (ev == e_).any():
             out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
+    for i, nm in enumerate(["pdl_released", "counted", "slotted", "gathered", "x_ready_added"]):
+        if (ev == 70 + i).any():
+            out["ffn_" + nm] = [round(float(t[ev == 70 + i].min()), 2),
+                                round(float(t[ev == 70 + i].max()), 2)]
     out["kernel_span_us"] = float(t[ev == 5].max())
     out["cta_start_spread_us"] = float(t[ev == 0].max())
     out["gather_done_us"] = [float(t[ev == 1].min()), float(t[ev == 1].max())]
