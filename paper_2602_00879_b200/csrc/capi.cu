@@ -823,6 +823,13 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.world = ex->world;
   a.epoch = ex->ep_state;
   a.early = after_front && !std::getenv("DESMOE_NO_EARLY") ? 1 : 0;
+  // dense: small blocks compute every published expert for every token (the
+  // tensor pipe is nearly idle in this memory-bound layer), so the FFN needs
+  // only the published expert list — no route, permutation or gather
+  const bool dense = a.early && n <= kDenseMaxTokens &&
+                     static_cast<size_t>(m) * n <= static_cast<size_t>(c->max_n) * c->max_k &&
+                     !std::getenv("DESMOE_NO_DENSE");
+  a.dense = dense ? 1 : 0;
   if (std::getenv("DESMOE_NO_L2PF")) a.flags |= 1;
   a.pub = ex->pub;
   a.route_words = ex->route_words;
@@ -844,7 +851,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   if (const char* sv = std::getenv("DESMOE_FFN_STAGES"))  // tuning experiments
     stages = std::max(2, std::min(stages, std::atoi(sv)));
   a.stages = stages;
-  if (4 * (m * ((n + 31) / 32) + 2 * m + n * k) > stage_bytes)
+  if (4 * (m * ((n + 31) / 32) + 3 * m + n * k) > stage_bytes)
     return fail(DESMOE_EINVAL, "expert FFN prologue scratch exceeds a pipeline stage");
   const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
   if (smem > static_cast<size_t>(kSmemLimit - 256))
@@ -869,8 +876,10 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, ex->wg, ex->wu, ex->wd, ex->xp_maps,
-                                 ex->kind == DESMOE_FFN_SWIGLU ? ex->h_maps : ex->xp_maps, a));
+  // dense phase A reads X itself (the front built its box maps for this x)
+  const BoxMaps& xmaps = dense ? c->x_maps : ex->xp_maps;
+  DESMOE_CUDA(cudaLaunchKernelEx(&lc, ffn_persistent_kernel, ex->wg, ex->wu, ex->wd, xmaps,
+                                 ex->kind == DESMOE_FFN_SWIGLU ? ex->h_maps : xmaps, a));
   mark(c, st);  // profiling only: expert FFN | (EP wait +) combine
   // ordered combine, programmatically serialised behind the FFN kernel
   cudaLaunchConfig_t cc{};
@@ -895,6 +904,13 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.done_ctas = ex->ep_state + 1;
   ca.zero = ex->counters;
   ca.zero_words = words;
+  ca.route_idx = route_idx;
+  ca.route_gate = route_gate;
+  ca.pub = ex->pub;
+  ca.m = m;
+  ca.expert_lo = ex->lo;
+  ca.expert_hi = ex->hi;
+  ca.stats = stats;
   if (ex->world > 1) {
     ca.flag = ex->ep_flag;
     ca.arrivals = static_cast<unsigned long long>(ex->world) * grid;
@@ -915,7 +931,12 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
     cc.numAttrs = 0;
     c->launches += 1;
   }
-  DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_slots_kernel, ca));
+  if (dense) {
+    cc.dynamicSmemBytes = static_cast<size_t>(m) * sizeof(int);
+    DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_dense_kernel, ca));
+  } else {
+    DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_slots_kernel, ca));
+  }
   c->launches += 2;
   mark(c, st);
   return DESMOE_OK;

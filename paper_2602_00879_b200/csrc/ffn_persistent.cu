@@ -65,22 +65,30 @@ struct UnitInfo {
   int expert, tile, brow, count;
 };
 
-__device__ inline UnitInfo decode(int u, int nA, int tilesA, int tilesB, const Tables& t) {
+// dense: every unit covers all n_tok tokens; row block = the expert's index
+// in the published list (t.offset holds it) x n_tok
+__device__ inline UnitInfo decode(int u, int nA, int tilesA, int tilesB, const Tables& t,
+                                  bool dense, int n_tok) {
   UnitInfo r;
+  int ei;
   if (u < nA) {
     r.phase = 0;
-    int ei = u / tilesA;
+    ei = u / tilesA;
     r.tile = u - ei * tilesA;
-    r.expert = t.active[ei];
   } else {
     u -= nA;
     r.phase = 1;
-    int ei = u / tilesB;
+    ei = u / tilesB;
     r.tile = u - ei * tilesB;
-    r.expert = t.active[ei];
   }
-  r.brow = t.offset[r.expert];
-  r.count = t.count[r.expert];
+  r.expert = t.active[ei];
+  if (dense) {
+    r.brow = t.offset[ei] * n_tok;
+    r.count = n_tok;
+  } else {
+    r.brow = t.offset[r.expert];
+    r.count = t.count[r.expert];
+  }
   return r;
 }
 
@@ -150,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_tok = a.n_tok, k = a.top_k, m = a.m, d = a.d, f = a.f;
   if (tid == 0) trace(a.trace, a.trace_cap, 0, -1);
   const bool swiglu = a.mode == 0;
+  const bool dense = a.dense != 0;
   const int S = a.stages;
   const int b_box_bytes = a.b_rows * 128;
   const int stage_bytes = 2 * kATile + 2 * b_box_bytes;
@@ -181,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* bits = reinterpret_cast<uint32_t*>(ring + static_cast<size_t>(S - 1) * stage_bytes);
   int* act_pos = reinterpret_cast<int*>(bits + m * tw);             // [m]
   int* pubm = act_pos + m;                                          // [m] published experts
-  float* gate_tmp = reinterpret_cast<float*>(pubm + m);             // [n*k] staged gates
+  int* pubidx = pubm + m;                                           // [m] their list index
+  float* gate_tmp = reinterpret_cast<float*>(pubidx + m);           // [n*k] staged gates
 
   int* sched = a.counters;
   int* x_ready = a.counters + 1;
@@ -207,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __shared__ uint64_t s_pts[8];  // prologue timeline (trace buffer only)
   __shared__ int s_upub;         // early mode: owned published experts
+  __shared__ int s_pcnt;         // early mode: published list length
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   pdl_launch_dependents();  // the combine kernel may launch; it waits for us
   // standalone: route + zeroed counters from the previous kernel. Behind the
@@ -231,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } while ((w0 >> 10) != tag);
     }
     const int cnt = static_cast<int>(__shfl_sync(0xffffffffu, w0, 0) & 1023u);
+    if (lane == 0) s_pcnt = cnt;
     int u = 0;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
       const int i = i0 + lane;
@@ -244,7 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const bool own = e >= lo && e < hi;
       const uint32_t bal = __ballot_sync(0xffffffffu, own);
-      if (own) pubm[u + __popc(bal & ((1u << lane) - 1u))] = e;
+      if (own) {
+        const int pos = u + __popc(bal & ((1u << lane) - 1u));
+        pubm[pos] = e;
+        pubidx[pos] = i;  // global list index: the dense row block (same on every rank)
+      }
       u += __popc(bal);
     }
     __syncwarp();
@@ -286,6 +302,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (a.trace && tid == 0) s_pts[0] = gtime();
   const size_t ep_half = a.world > 1 ? (static_cast<size_t>(seq) & 1u) * a.slot_stride : 0;
 
+  int U = 0, total_slots = 0;
+  if (dense) {
+    // dense mode: units over the published list, all tokens each; no route,
+    // permutation, gather or handshake (X itself is the activation source)
+    __syncthreads();  // s_upub / pubm from the early block
+    U = s_upub;
+    for (int i = tid; i < U; i += kThreads) {
+      t.active[i] = pubm[i];
+      t.offset[i] = pubidx[i];
+    }
+    __syncthreads();
+  } else {
   // ---- prologue: permutation (redundantly per CTA) ------------------------
   for (int i = tid; i < m; i += kThreads) t.count[i] = 0;
   for (int i = tid; i < m * tw; i += kThreads) bits[i] = 0;
@@ -356,8 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   u_all = __reduce_add_sync(0xffffffffu, u_all);
   if (lane == 0) atomicAdd(&t.scalars[2], u_all);
   __syncthreads();
-  const int total_slots = block_exclusive_scan(t.offset, m, warp_sums);
-  int U = block_exclusive_scan(act_pos, m, warp_sums);
+  total_slots = block_exclusive_scan(t.offset, m, warp_sums);
+  U = block_exclusive_scan(act_pos, m, warp_sums);
   if (a.early) {
     // units run over the published list (a listed expert may get no token
     // after re-routing: its units stream nothing useful but stay consistent
@@ -395,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int e = tid; e < n_tok * k; e += kThreads) a.slot_of[e] = t.slot_of[e];
     if (tid == 0 && a.stats) {
       a.stats[0] = t.scalars[2];  // unique experts of the block (all ranks)
-      a.stats[1] = a.n_members ? *a.n_members : t.scalars[2];
+      a.stats[1] = a.early ? s_pcnt : (a.n_members ? *a.n_members : t.scalars[2]);
       a.stats[2] = total_slots;
       a.stats[3] = U;             // experts this rank streams
     }
@@ -438,10 +466,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  }  // !dense
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (tid == 0 && static_cast<int>(blockIdx.x) < a.gather_ctas) {
+  if (!dense && tid == 0 && static_cast<int>(blockIdx.x) < a.gather_ctas) {
     if (a.trace) s_pts[3] = gtime();
     __threadfence();
     atomic_add_release(x_ready, 1);
@@ -468,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&qfull[q]);
         if (uu < 0) break;
         trace(a.trace, a.trace_cap, 2, uu);
-        const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
+        const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
         const int ksteps = phaseA ? ksA : ksB;
         const int ks0 = pre ? pre_ks : 0;
@@ -501,14 +530,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int uu = unit_q[q];
         mbar_arrive(&qempty[q]);
         if (uu < 0) break;
-        const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
+        const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
         const bool from_x = phaseA || !swiglu;
         const int bi = box_for(ui.count);
         const uint32_t box_bytes = (16u << bi) * 128u;
         const BoxMaps& acts = from_x ? xp_maps : h_maps;
         const int ksteps = phaseA ? ksA : ksB;
-        if (from_x && !x_seen && ui.count > 0) {
+        if (from_x && !x_seen && ui.count > 0 && !dense) {
           while (ld_acquire(x_ready) < a.gather_ctas) {
           }
           fence_proxy_async_global();
@@ -536,8 +565,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes + 2 * kATile;
           mbar_arrive_expect_tx(&full[s], 2 * box_bytes);
-          tma_load_2d(st, &acts.map[bi], &full[s], 2 * ks * kBK, ui.brow, pol_x);
-          tma_load_2d(st + b_box_bytes, &acts.map[bi], &full[s], (2 * ks + 1) * kBK, ui.brow,
+          const int row = dense && from_x ? 0 : ui.brow;  // dense: X itself (all tokens)
+          tma_load_2d(st, &acts.map[bi], &full[s], 2 * ks * kBK, row, pol_x);
+          tma_load_2d(st + b_box_bytes, &acts.map[bi], &full[s], (2 * ks + 1) * kBK, row,
                       pol_x);
         }
       }
@@ -552,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[q]);
       if (uu < 0) break;
-      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
+      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
@@ -601,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       if (etid == 0) mbar_arrive(&qempty[q]);
       if (uu < 0) break;
-      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t);
+      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t buf = nunit & 1u;
@@ -643,7 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) {
             const int col = c0 + j;
             if (col < ui.count)
-              yrow[static_cast<size_t>(col) * d] = v[j] * t.slot_gate[ui.brow + col];
+              yrow[static_cast<size_t>(col) * d] =
+                  dense ? v[j] : v[j] * t.slot_gate[ui.brow + col];
           }
         }
       } else {
@@ -657,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) {
             const int col = c0 + j;
             if (col < ui.count) {
-              const float val = v[j] * t.slot_gate[ui.brow + col];
+              const float val = dense ? v[j] : v[j] * t.slot_gate[ui.brow + col];
               for (int p = 0; p < a.world; ++p)
                 __stcg(a.peer_slot[p] + off + static_cast<size_t>(col) * d, val);
             }
@@ -762,6 +793,89 @@ __global__ void __launch_bounds__(32) ep_wait_kernel(CombineArgs a) {
   }
   __syncwarp();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Dense-mode combine: the FFN computed every published expert for every
+// token (rows [list index][token]); y[t] = sum over the token's routed
+// experts in ascending order of gate * row (gating.cpp:141-155) — the same
+// fp32 products and sums as the routed path. CTA 0 also writes the block's
+// stats (unique experts of the route, published list length, selections,
+// experts this rank streamed).
+__global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  extern __shared__ int inv[];  // [m] expert -> published list index
+  __shared__ int s_epoch, s_cnt;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_epoch = *a.epoch;
+    s_cnt = static_cast<int>(a.pub[0] & 1023u);
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  for (int i = tid; i < cnt; i += blockDim.x) inv[a.pub[1 + i] & 1023u] = i;
+  __syncthreads();
+  const float* y_slot = a.y_slot;
+  if (a.world > 1) y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
+  const int vec = a.d / 4;
+  const int i = blockIdx.x * blockDim.x + tid;
+  if (i < a.n * vec) {
+    const int tok = i / vec, c = (i - tok * vec) * 4;
+    const int rc = a.route_cnt[tok];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < rc; ++j) {
+      const size_t o = static_cast<size_t>(tok) * a.k + j;
+      const int e = a.route_idx[o];
+      const float g = static_cast<float>(a.route_gate[o]);
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(
+          y_slot + (static_cast<size_t>(inv[e]) * a.n + tok) * a.d + c));
+      // product then add (no contraction): the routed path's epilogue product
+      // followed by the combine's add
+      acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, g));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, g));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, g));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, g));
+    }
+    *reinterpret_cast<float4*>(a.y + static_cast<size_t>(tok) * a.d + c) = acc;
+  }
+  if (blockIdx.x == 0 && a.stats) {
+    // unique experts of the route (moe_latency's count route, analysis.cpp:16-30)
+    __syncthreads();
+    for (int e = tid; e < a.m; e += blockDim.x) inv[e] = 0;
+    __syncthreads();
+    int sel = 0;
+    for (int o = tid; o < a.n * a.k; o += blockDim.x) {
+      const int tok = o / a.k, j = o - tok * a.k;
+      if (j < a.route_cnt[tok]) {
+        inv[a.route_idx[o]] = 1;
+        ++sel;
+      }
+    }
+    __shared__ int s_sel, s_u, s_own;
+    if (tid == 0) s_sel = s_u = s_own = 0;
+    __syncthreads();
+    atomicAdd(&s_sel, sel);
+    int u = 0, own = 0;
+    for (int e = tid; e < a.m; e += blockDim.x) u += inv[e];
+    for (int q = tid; q < cnt; q += blockDim.x) {
+      const int e = static_cast<int>(a.pub[1 + q] & 1023u);
+      own += e >= a.expert_lo && e < a.expert_hi;
+    }
+    atomicAdd(&s_u, u);
+    atomicAdd(&s_own, own);
+    __syncthreads();
+    if (tid == 0) {
+      a.stats[0] = s_u;
+      a.stats[1] = cnt;
+      a.stats[2] = s_sel;
+      a.stats[3] = s_own;
+    }
+  }
+  for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;
+  __syncthreads();
+  if (tid == 0 && atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
+    *a.done_ctas = 0;
+    atomicAdd(a.epoch, 1);
+  }
 }
 
 __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {

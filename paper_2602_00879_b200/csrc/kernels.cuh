@@ -184,6 +184,7 @@ struct TileArgs {  // router GEMM (tile_gemm.cu)
 };
 
 constexpr int kMaxWorld = 8;  // expert-parallel ranks (one 8-GPU NVSwitch box)
+constexpr int kDenseMaxTokens = 64;  // dense FFN mode up to this block size
 
 struct FfnArgs {
   int mode;  // 0 = SwiGLU (phase A + B), 1 = linear expert (phase B on x)
@@ -223,6 +224,7 @@ struct FfnArgs {
   const void* wc_base;       // packed W_d / W_lin tiles
   int flags;                 // experiments: 1 = no L2 prefetch of the first unit
   int gather_ctas;           // CTAs that gather x rows (and the x_ready target)
+  int dense;                 // every published expert x every token (small blocks)
 };
 
 // Ordered combine arguments (combine_slots_kernel).
@@ -243,6 +245,12 @@ struct CombineArgs {
   int* err;                  // set to 2 on an exchange timeout
   int* zero;                 // FFN counters, zeroed for the next call
   int zero_words;
+  // dense mode (combine_dense_kernel)
+  const int* route_idx;      // [n x k]
+  const double* route_gate;  // [n x k]
+  const uint32_t* pub;       // published list (tagged words)
+  int m, expert_lo, expert_hi;
+  int* stats;                // optional [4]
 };
 
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }
@@ -256,6 +264,7 @@ __global__ void pack_weights_kernel(const uint4* __restrict__ src, const uint4* 
                                     uint4* __restrict__ out, int experts, int rows_per_expert,
                                     int cols, int stacked);
 __global__ void combine_slots_kernel(CombineArgs a);
+__global__ void combine_dense_kernel(CombineArgs a);
 __global__ void ep_wait_kernel(CombineArgs a);
 
 cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,

@@ -94,7 +94,8 @@ def main():
                                 round(float(t[ev == 70 + i].max()), 2)]
     out["kernel_span_us"] = float(t[ev == 5].max())
     out["cta_start_spread_us"] = float(t[ev == 0].max())
-    out["gather_done_us"] = [float(t[ev == 1].min()), float(t[ev == 1].max())]
+    out["gather_done_us"] = ([float(t[ev == 1].min()), float(t[ev == 1].max())]
+                             if (ev == 1).any() else None)
     out["first_dequeue_us"] = float(t[ev == 2].min())
     out["x_ready_seen_us"] = [float(t[ev == 6].min()), float(t[ev == 6].max())] if (ev == 6).any() else None
     done = {int(u): float(tt) for u, tt, e in zip(unit, t, ev) if e == 3}
