@@ -10,13 +10,13 @@ TAG=${2:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
 B="python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --strategies vanilla,vote"
-# launch order per strategy: warmup 3 + timed 3 + phase warmup 1 + phase timed 3
-# = 10 layer calls; vanilla first, so vote's first timed call is call 14.
+# launch order per strategy: warmup 3 + timed 3 + phase warmup 3 + phase timed 3
+# = 12 layer calls; vanilla first, so vote's first timed call is call 16.
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-  --clock-control none -k regex:desmoe\|front_kernel\|ffn_persistent\|combine_slots\|route\|coreset\|permute\|tile_gemm \
+  --clock-control none -k regex:desmoe\|front_kernel\|ffn_persistent\|combine\|route\|coreset\|permute\|tile_gemm \
   --csv --log-file $OUT/launches_${CFG}_${TAG}.csv $B > $OUT/ncu_launches_${CFG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_persistent_kernel \
-  -s 13 -c 1 -f -o $OUT/ffn_${CFG}_${TAG} $B > $OUT/ncu_ffn_${CFG}.log 2>&1
+  -s 15 -c 1 -f -o $OUT/ffn_${CFG}_${TAG} $B > $OUT/ncu_ffn_${CFG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:front_kernel \
-  -s 13 -c 1 -f -o $OUT/front_${CFG}_${TAG} $B > $OUT/ncu_front_${CFG}.log 2>&1
+  -s 15 -c 1 -f -o $OUT/front_${CFG}_${TAG} $B > $OUT/ncu_front_${CFG}.log 2>&1
 ls -la $OUT

@@ -41,7 +41,8 @@ RAW_METRICS = [
 
 
 def short(name):
-    for k in ("ffn_persistent_kernel", "front_kernel", "combine_slots_kernel", "tile_gemm_kernel",
+    for k in ("ffn_persistent_kernel", "front_kernel", "combine_slots_kernel", "combine_dense_kernel",
+              "ep_wait_kernel", "tile_gemm_kernel",
               "fused_route_kernel", "gate_topk_kernel", "coreset_kernel",
               "constrained_route_kernel", "permute_kernel"):
         if k in name:
