@@ -1049,6 +1049,9 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   FrontArgs a{};
   size_t smem = 0;
   if (!front_plan(n, m, k, d, &a, &smem)) return DESMOE_OK;
+  if (std::getenv("DESMOE_DEBUG_PLAN"))
+    std::fprintf(stderr, "front plan n=%d m=%d: chunk=%d stages=%d b_rows=%d vote_rows=%d smem=%zu\n",
+                 n, m, a.chunk, a.stages, a.b_rows, a.vote_rows, smem);
   if (x != c->x_map_ptr || n != c->x_map_n || d != c->x_map_d) {
     int rc = make_box_maps(&c->x_maps, x, n, d);
     if (rc) return rc;
@@ -1083,7 +1086,6 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.err = c->err;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
-  if (const char* pw = std::getenv("DESMOE_PREWARM")) a.prewarm = std::atoi(pw);
   cudaError_t e = launch_front(c->wr_map, c->x_maps, a, smem, st);
   if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("front kernel: ") + cudaGetErrorString(e));
   c->launches += 1;

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
-  __shared__ uint64_t s_ts[24];  // timeline marks (trace buffer only)
+  __shared__ uint64_t s_ts[40];  // timeline marks (trace buffer only)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool tracing = a.trace != nullptr;
   if (tracing && tid == 0) s_ts[24] = clock64();
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
   }
   if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
-  if (!(a.prewarm & 16)) pdl_launch_dependents();
+  pdl_launch_dependents();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
   const uint32_t tag = a.seq ? hand_tag(*a.seq) : 0u;  // this call's hand-off tag
   tc_fence_before();
@@ -591,6 +591,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
     if (tid < hi - lo) own_tok[ob + tid] = c0 + lo + tid;
     own = ob + (hi - lo);
+    if (tracing && tid == 0 && c < 8) s_ts[26 + c] = gtime();
     if (c + 1 < nch) {
       // re-arm for the next chunk, then a (relaxed) cluster barrier: every
       // owner consumed this chunk before anyone pushes the next one
@@ -670,19 +671,25 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   } else {
     const int want = k < m ? k : m;
     const int rounds = want < m ? want + 1 : want;
+    if (tracing && warp == 0 && lane == 0) s_ts[34] = gtime();
 #pragma unroll 1
     for (int j = warp; j < own; j += NW - 1) {
       int* sj = sel + j * 33;
       const float* xr = xrow + j * m;
       const double* er = erow + j * ew;
       long long c0 = clock64();
+      if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[35] = gtime();
       warp_rank_select(xr, m, rounds, nullptr, sj);
-      if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[23] = clock64() - c0;
+      if (tracing && warp == 0 && lane == 0 && j == 0) {
+        s_ts[23] = clock64() - c0;
+        s_ts[36] = gtime();
+      }
       if (lane == 0) {
         bool r = want < m && risky_boundary(xr, er, act, sj, want);
         if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
         risky[j] = r;
       }
+      if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[37] = gtime();
     }
     if (tracing && warp == 0 && lane == 0) s_ts[22] = gtime();
   }
@@ -749,7 +756,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     cluster_wait();
     FRONT_MARK(9);
     front_tail(a.logits_out, xrow, own_tok, own, m, tid);
-    front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 26);
+    front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 38);
     return;
   }
   mbar_wait_cluster(bar_selx, 0);       // every token's selection has arrived
@@ -875,7 +882,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   cluster_wait();  // #3: no CTA exits while others may still read its shared memory
   FRONT_MARK(14);
   front_tail(a.logits_out, xrow, own_tok, own, m, tid);
-  front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 26);
+  front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 38);
 #undef FRONT_MARK
 }
 

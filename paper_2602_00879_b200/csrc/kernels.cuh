@@ -63,7 +63,6 @@ struct FrontArgs {
   int b_rows, box_index, kb_per_cta, stages, tmem_cols;
   int chunk, own_max;  // token chunk of the split-K GEMM; own tokens per CTA bound
   int vote_rows;       // token rows of the shared-memory vote matrix chunk
-  int prewarm;         // experiment bits (16: trigger the FFN launch at the end)
   int* route_idx;      // [n x k]
   double* route_gate;  // [n x k]
   int* route_cnt;      // [n]

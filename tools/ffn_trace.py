@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--strategy", default="vote")
     ap.add_argument("--json", default="")
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm before the traced call")
+    ap.add_argument("--block", type=int, default=0, help="override the block size N")
     args = ap.parse_args()
     import torch
     from bench import CONFIGS
@@ -29,7 +30,9 @@ def main():
     from paper_2602_00879_b200.dessim import _ptr
     from paper_2602_00879_b200.layer import DesMoeLayer, LayerConfig
 
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.block:
+        cfg["block"] = args.block
     n, m, k, d, f = cfg["block"], cfg["experts"], cfg["top_k"], cfg["hidden"], cfg["ffn"]
     wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000)
     wr = synth.router_weights(m, d, seed=2000)
@@ -75,6 +78,13 @@ def main():
     fnames = ["start", "setup", "drained", "partials_synced", "logits", "rowmax", "activated",
               "sums_topk", "selected", "sync2", "v_zeroed", "v_gathered", "coreset", "rerouted",
               "exit", "votes", "ranked", "arrived", "mma_done", "drain_done", "copies_issued", "sums_done", "topk_done"]
+    for i, nm in enumerate(["l4_enter", "l4_call", "l4_selected", "l4_risky"]):
+        if (ev == 74 + i).any():
+            out["front_" + nm] = round(float(t[ev == 74 + i].max()), 2)
+    chunks = [round(float(t[ev == 66 + c].max()), 2) for c in range(4) if (ev == 66 + c).any()
+              and float(t[ev == 66 + c].max()) < 1e6 and float(t[ev == 66 + c].max()) > 0]
+    if chunks:
+        out["front_chunk_ends"] = chunks
     if (ev == 63).any():
         out["select_cycles"] = int(rec[ev == 63][:, 1].max())
     if (ev == 64).any() and (ev == 65).any() and (ev == 40).any() and (ev == 53).any():
