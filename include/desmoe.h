@@ -244,6 +244,18 @@ int desmoe_layer_forward(desmoe_ctx* ctx, const desmoe_experts* ex, const void* 
                          const void* x_dev, int n, const desmoe_route_cfg* cfg, float* y_dev,
                          int* stats_dev, void* stream);
 
+/* A stack of `layers` DES MoE layers applied in sequence to one block (the
+ * MoE layers of one diffusion denoising step): x_dev [n x hidden] bf16 ->
+ * y_dev [n x hidden] fp32; layer l's output feeds layer l+1 as bf16 through
+ * context-owned buffers. The whole stack is captured into ONE CUDA graph
+ * (re-captured when any argument changes). stats_dev: optional int[4*layers].
+ * residual != 0: each layer outputs h + MoE(h) (the residual stream a model's
+ * MoE blocks sit on), so token diversity survives the stack. */
+int desmoe_stack_forward(desmoe_ctx* ctx, desmoe_experts* const* experts,
+                         const void* const* w_router_dev, int layers, const void* x_dev, int n,
+                         const desmoe_route_cfg* cfg, float* y_dev, int* stats_dev, int residual,
+                         void* stream);
+
 /* The fp32 router logits [n x experts] the last desmoe_layer_forward on this
  * context routed with (for checking its routing against the reference). */
 int desmoe_layer_logits(desmoe_ctx* ctx, float* logits_dev, int n, int experts, void* stream);

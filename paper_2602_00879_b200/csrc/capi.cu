@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/desmoe.h"
 #include "common.cuh"
@@ -156,6 +157,10 @@ struct desmoe_ctx {
     bool prof;
   } gkey{};
   int g_n_ev = 0, g_launches = 0;
+  // layer stacks (desmoe_stack_forward): bf16 ping-pong activations and graph
+  __nv_bfloat16* stack_buf[2] = {};
+  cudaGraphExec_t sgexec = nullptr;
+  std::vector<const void*> skey;
   // live phase timing
   bool profiling = false;
   cudaEvent_t ev[8] = {};
@@ -288,6 +293,9 @@ void desmoe_destroy(desmoe_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->sgexec) cudaGraphExecDestroy(c->sgexec);
+  for (auto* b : c->stack_buf)
+    if (b) cudaFree(b);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
@@ -792,7 +800,8 @@ int launch_router_tiles(const CUtensorMap& wa, const BoxMaps& acts, TileArgs a, 
 int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
              const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false,
-             bool after_front = false) {
+             bool after_front = false, __nv_bfloat16* y_bf16 = nullptr,
+             const void* resid = nullptr) {
   const int m = ex->m, d = ex->d, f = ex->f;
   if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
   const int words = ffn_counter_words(m, f);
@@ -899,6 +908,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.k = k;
   ca.d = d;
   ca.y = y;
+  ca.y_bf16 = y_bf16;
+  ca.resid = static_cast<const __nv_bfloat16*>(resid);
   ca.world = ex->world;
   ca.epoch = ex->ep_state;
   ca.done_ctas = ex->ep_state + 1;
@@ -1095,10 +1106,13 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
 
 int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
                        int n, const desmoe_route_cfg* cfg, float* y, int* stats,
-                       cudaStream_t st) {
+                       cudaStream_t st, __nv_bfloat16* y_bf16 = nullptr, bool reset = true,
+                       bool residual = false) {
   int rc;
-  c->n_ev = 0;
-  c->launches = 0;
+  if (reset) {
+    c->n_ev = 0;
+    c->launches = 0;
+  }
   mark(c, st);
   bool zeroed = false;
   rc = front_impl(c, ex, x, w_r, n, cfg, st, &zeroed);
@@ -1119,7 +1133,7 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   mark(c, st);
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
-                front_used);
+                front_used, y_bf16, residual ? x : nullptr);
   if (rc) return rc;
   return DESMOE_OK;
 }
@@ -1406,6 +1420,84 @@ int desmoe_ep_import(desmoe_experts* ex, int world, int rank, const void* handle
     }
   }
   return desmoe_ep_connect(ex, world, rank, slots, flags);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// layer stacks: one block through `layers` DES MoE layers in one CUDA graph
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int desmoe_stack_forward(desmoe_ctx* c, desmoe_experts* const* experts, const void* const* w_router,
+                         int layers, const void* x, int n, const desmoe_route_cfg* cfg, float* y,
+                         int* stats, int residual, void* stream) {
+  if (!c || !experts || !w_router || !x || !y || !cfg) return fail(DESMOE_EINVAL, "null argument");
+  if (layers < 1) return fail(DESMOE_EINVAL, "layers < 1");
+  const int d = experts[0]->d;
+  for (int l = 0; l < layers; ++l) {
+    if (!experts[l] || !w_router[l]) return fail(DESMOE_EINVAL, "null layer");
+    if (experts[l]->d != d || experts[l]->m != cfg->experts)
+      return fail(DESMOE_EINVAL, "layers differ in hidden size or expert count");
+  }
+  int rc = check_block(c, n, cfg->experts);
+  if (rc) return rc;
+  if (d > c->max_d) return fail(DESMOE_EINVAL, "hidden exceeds context capacity");
+  for (auto*& b : c->stack_buf)
+    if (!b) DESMOE_CUDA(cudaMalloc(&b, static_cast<size_t>(c->max_n) * c->max_d * 2));
+  cudaStream_t st = S(stream);
+  auto run = [&](cudaStream_t s) -> int {
+    c->n_ev = 0;
+    c->launches = 0;
+    const void* xin = x;
+    for (int l = 0; l < layers; ++l) {
+      const bool last = l == layers - 1;
+      __nv_bfloat16* out = last ? nullptr : c->stack_buf[l & 1];
+      int r = layer_forward_impl(c, experts[l], w_router[l], xin, n, cfg, y,
+                                 stats ? stats + 4 * l : nullptr, s, out, false, residual != 0);
+      if (r) return r;
+      xin = out;
+    }
+    return DESMOE_OK;
+  };
+  if (!c->use_graphs) return run(st);
+  std::vector<const void*> key;
+  key.reserve(2 * layers + 8);
+  for (int l = 0; l < layers; ++l) {
+    key.push_back(experts[l]);
+    key.push_back(w_router[l]);
+  }
+  key.push_back(x);
+  key.push_back(y);
+  key.push_back(stats);
+  key.push_back(reinterpret_cast<const void*>(static_cast<intptr_t>(n)));
+  const int cfgw[6] = {cfg->experts, cfg->top_k, cfg->activation, cfg->strategy, cfg->seq_k,
+                       cfg->vote_source};
+  for (int v : cfgw) key.push_back(reinterpret_cast<const void*>(static_cast<intptr_t>(v)));
+  long long beta_bits;
+  std::memcpy(&beta_bits, &cfg->vote_beta, 8);
+  key.push_back(reinterpret_cast<const void*>(static_cast<intptr_t>(beta_bits)));
+  key.push_back(reinterpret_cast<const void*>(static_cast<intptr_t>(c->profiling)));
+  key.push_back(reinterpret_cast<const void*>(static_cast<intptr_t>(residual)));
+  if (!c->sgexec || key != c->skey) {
+    cudaGraph_t g = nullptr;
+    DESMOE_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = run(c->cap_stream);
+    cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(DESMOE_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    if (c->sgexec) cudaGraphExecDestroy(c->sgexec);
+    c->sgexec = nullptr;
+    cudaError_t ie = cudaGraphInstantiate(&c->sgexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return fail(DESMOE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    c->skey = key;
+  }
+  DESMOE_CUDA(cudaGraphLaunch(c->sgexec, st));
+  return DESMOE_OK;
 }
 
 }  // extern "C"

@@ -795,6 +795,27 @@ __global__ void __launch_bounds__(32) ep_wait_kernel(CombineArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+__device__ inline void store_row4(const CombineArgs& a, size_t off, float4 v) {
+  if (a.resid) {  // h + MoE(h): the residual stream of a layer stack
+    const uint2 r = *reinterpret_cast<const uint2*>(a.resid + off);
+    const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+    const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+    v.x += r0.x;
+    v.y += r0.y;
+    v.z += r1.x;
+    v.w += r1.y;
+  }
+  if (a.y_bf16) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(a.y_bf16 + off) = u;
+  } else {
+    *reinterpret_cast<float4*>(a.y + off) = v;
+  }
+}
+
 // Dense-mode combine: the FFN computed every published expert for every
 // token (rows [list index][token]); y[t] = sum over the token's routed
 // experts in ascending order of gate * row (gating.cpp:141-155) — the same
@@ -835,7 +856,7 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
       acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, g));
       acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, g));
     }
-    *reinterpret_cast<float4*>(a.y + static_cast<size_t>(tok) * a.d + c) = acc;
+    store_row4(a, static_cast<size_t>(tok) * a.d + c, acc);
   }
   if (blockIdx.x == 0 && a.stats) {
     // unique experts of the route (moe_latency's count route, analysis.cpp:16-30)
@@ -910,7 +931,7 @@ __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
           acc.w += v[j].w;
         }
     }
-    *reinterpret_cast<float4*>(a.y + static_cast<size_t>(tok) * a.d + c) = acc;
+    store_row4(a, static_cast<size_t>(tok) * a.d + c, acc);
   }
   // the FFN is complete: zero its counters for the next call
   for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;

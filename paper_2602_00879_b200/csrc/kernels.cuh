@@ -250,6 +250,8 @@ struct CombineArgs {
   const uint32_t* pub;       // published list (tagged words)
   int m, expert_lo, expert_hi;
   int* stats;                // optional [4]
+  __nv_bfloat16* y_bf16;     // optional: write bf16 here instead of fp32 y (layer stacks)
+  const __nv_bfloat16* resid;  // optional residual stream added before the store (stacks)
 };
 
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }

@@ -84,3 +84,42 @@ class DesMoeLayer:
 
     def check(self):
         check(lib().desmoe_check(self.ctx.h, _stream()))
+
+
+class DesMoeStack:
+    """A stack of DES MoE layers (the MoE layers of one diffusion denoising
+    step) run by desmoe_stack_forward as ONE CUDA graph: layer l's output
+    feeds layer l+1 as bf16. `layers` = list of (w_router, w_gate, w_up,
+    w_down) tuples; all layers share one C-ABI context."""
+
+    def __init__(self, cfg: LayerConfig, layers, max_tokens=256, expert_range=None):
+        import torch
+        self.cfg = cfg
+        self.ctx = _Ctx(torch.cuda.current_device(), max_tokens, max(cfg.experts, 256), 32,
+                        max(cfg.hidden, 4096))
+        self.routers, self.experts = [], []
+        for wr, wg, wu, wd in layers:
+            self.routers.append(wr.contiguous())
+            self.experts.append(ExpertWeights.swiglu(wg, wu, wd, experts=cfg.experts,
+                                                     expert_range=expert_range, ctx=self.ctx))
+        n = len(self.experts)
+        self._ex = (C.c_void_p * n)(*[e.h.value for e in self.experts])
+        self._wr = (C.c_void_p * n)(*[w.data_ptr() for w in self.routers])
+        self.stats = torch.zeros((n, 4), dtype=torch.int32, device="cuda")
+
+    def __len__(self):
+        return len(self.experts)
+
+    def forward(self, x, y=None, strategy=None, stream=None, residual=False):
+        """x [n x d] bf16 -> y [n x d] fp32 after all layers (stream-ordered);
+        residual=True: every layer outputs h + MoE(h)."""
+        import torch
+        n = x.shape[0]
+        if y is None:
+            y = torch.empty((n, self.cfg.hidden), dtype=torch.float32, device=x.device)
+        rc = self.cfg.route_cfg(strategy)
+        st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream()
+        check(lib().desmoe_stack_forward(self.ctx.h, self._ex, self._wr, len(self.experts),
+                                         _ptr(x), n, C.byref(rc), _ptr(y), _ptr(self.stats),
+                                         1 if residual else 0, st))
+        return y

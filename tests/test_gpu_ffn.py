@@ -149,3 +149,36 @@ def test_layer_host_entry_matches_device_entry():
     layer.forward_host(xh, yh, sh)
     assert torch.equal(yh, y_dev.cpu())  # deterministic: bit-identical
     assert sh[0].item() <= 25
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["vote", "vanilla"])
+def test_stack_equals_chained_layers(strategy):
+    """desmoe_stack_forward (one graph, bf16 hand-over between layers) equals
+    running the layers one by one with the output cast to bf16 in between."""
+    import torch
+    from paper_2602_00879_b200.layer import DesMoeLayer, DesMoeStack, LayerConfig
+    m, d, f, n, k, L = 64, 512, 512, 32, 8, 3
+    cfg = LayerConfig(m, k, d, f, strategy=strategy, vote_beta=0.4)
+    params = [(synth.router_weights(m, d, seed=40 + l), *synth.swiglu_weights(m, d, f, seed=50 + l))
+              for l in range(L)]
+    stack = DesMoeStack(cfg, params)
+    x = synth.hidden_states(n, d, seed=3, rho=0.3)
+    y_stack = stack.forward(x).clone()
+    stats = stack.stats.cpu().numpy()
+    y_res = stack.forward(x, residual=True).clone()
+    xin = x
+    for l, (wr, wg, wu, wd) in enumerate(params):
+        layer = DesMoeLayer(cfg, wr, wg, wu, wd, own_context=True)
+        y = layer.forward(xin)
+        torch.cuda.synchronize()
+        assert stats[l].tolist() == layer.stats.cpu().tolist()
+        xin = y.to(torch.bfloat16)
+    assert torch.equal(y_stack, y)
+    # residual stream: h + MoE(h) carried in bf16 between layers
+    xin = x
+    for l, (wr, wg, wu, wd) in enumerate(params):
+        layer = DesMoeLayer(cfg, wr, wg, wu, wd, own_context=True)
+        y = layer.forward(xin) + xin.float()
+        xin = y.to(torch.bfloat16)
+    assert torch.equal(y_res, y)
