@@ -260,6 +260,13 @@ int desmoe_stack_forward(desmoe_ctx* ctx, desmoe_experts* const* experts,
  * context routed with (for checking its routing against the reference). */
 int desmoe_layer_logits(desmoe_ctx* ctx, float* logits_dev, int n, int experts, void* stream);
 
+/* The route of the last desmoe_layer_forward on this context (layout of
+ * desmoe_route_out; any pointer may be NULL): route_idx/gate [n x top_k],
+ * route_cnt [n], coreset members [experts] + count (DES strategies). */
+int desmoe_layer_route(desmoe_ctx* ctx, int* route_idx_dev, double* route_gate_dev,
+                       int* route_cnt_dev, int* members_dev, int* n_members_dev, int n, int top_k,
+                       int experts, void* stream);
+
 /* Same with HOST buffers: copies x (bf16) in, runs the layer, copies y
  * (fp32) and stats back; synchronises. The end-to-end entry a C/C++ caller
  * without device memory uses. */

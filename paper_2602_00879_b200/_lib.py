@@ -69,6 +69,7 @@ _SIGS = {
     "desmoe_layer_forward": (_I, [_P, _P, _P, _P, _I, C.POINTER(RouteCfg), _P, _P, _P]),
     "desmoe_layer_forward_host": (_I, [_P, _P, _P, _P, _I, C.POINTER(RouteCfg), _P, _P, _P]),
     "desmoe_layer_logits": (_I, [_P, _P, _I, _I, _P]),
+    "desmoe_layer_route": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
     "desmoe_stack_forward": (_I, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _I, _P, _I,
                                   C.POINTER(RouteCfg), _P, _P, _I, _P]),
     "desmoe_set_profiling": (_I, [_P, _I]),

@@ -1208,6 +1208,28 @@ int desmoe_layer_logits(desmoe_ctx* c, float* logits_dev, int n, int experts, vo
   return DESMOE_OK;
 }
 
+int desmoe_layer_route(desmoe_ctx* c, int* route_idx_dev, double* route_gate_dev,
+                       int* route_cnt_dev, int* members_dev, int* n_members_dev, int n, int top_k,
+                       int experts, void* stream) {
+  int rc = check_block(c, n, experts);
+  if (rc) return rc;
+  if (top_k < 1 || top_k > c->max_k) return fail(DESMOE_EINVAL, "top_k out of range");
+  cudaStream_t st = S(stream);
+  const size_t nk = static_cast<size_t>(n) * top_k;
+  if (route_idx_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(route_idx_dev, c->route_idx, nk * 4, cudaMemcpyDeviceToDevice, st));
+  if (route_gate_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(route_gate_dev, c->route_gate, nk * 8, cudaMemcpyDeviceToDevice, st));
+  if (route_cnt_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(route_cnt_dev, c->route_cnt, n * 4, cudaMemcpyDeviceToDevice, st));
+  if (members_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(members_dev, c->members, static_cast<size_t>(experts) * 4,
+                                cudaMemcpyDeviceToDevice, st));
+  if (n_members_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(n_members_dev, c->n_members, 4, cudaMemcpyDeviceToDevice, st));
+  return DESMOE_OK;
+}
+
 int desmoe_set_graphs(desmoe_ctx* c, int enable) {
   if (!c) return fail(DESMOE_EINVAL, "null context");
   c->use_graphs = enable != 0;

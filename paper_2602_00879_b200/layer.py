@@ -82,6 +82,22 @@ class DesMoeLayer:
         check(lib().desmoe_layer_logits(self.ctx.h, _ptr(out), n, self.cfg.experts, _stream()))
         return out
 
+    def last_route(self, n):
+        """(idx [n x K] int32, gate [n x K] f64, cnt [n] int32, coreset members
+        list) of the last forward() (numpy)."""
+        import torch
+        k, m = self.cfg.top_k, self.cfg.experts
+        idx = torch.empty((n, k), dtype=torch.int32, device="cuda")
+        gate = torch.empty((n, k), dtype=torch.float64, device="cuda")
+        cnt = torch.empty(n, dtype=torch.int32, device="cuda")
+        mem = torch.empty(m, dtype=torch.int32, device="cuda")
+        nm = torch.empty(1, dtype=torch.int32, device="cuda")
+        check(lib().desmoe_layer_route(self.ctx.h, _ptr(idx), _ptr(gate), _ptr(cnt), _ptr(mem),
+                                       _ptr(nm), n, k, m, _stream()))
+        torch.cuda.synchronize()
+        return (idx.cpu().numpy(), gate.cpu().numpy(), cnt.cpu().numpy(),
+                mem[: int(nm.item())].cpu().numpy().tolist())
+
     def check(self):
         check(lib().desmoe_check(self.ctx.h, _stream()))
 
