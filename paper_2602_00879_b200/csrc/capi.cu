@@ -922,6 +922,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.expert_lo = ex->lo;
   ca.expert_hi = ex->hi;
   ca.stats = stats;
+  ca.trace = c->trace;
+  ca.trace_cap = c->trace_cap;
   if (ex->world > 1) {
     ca.flag = ex->ep_flag;
     ca.arrivals = static_cast<unsigned long long>(ex->world) * grid;

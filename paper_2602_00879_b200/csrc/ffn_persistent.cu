@@ -65,8 +65,8 @@ struct UnitInfo {
   int expert, tile, brow, count;
 };
 
-// dense: every unit covers all n_tok tokens; row block = the expert's index
-// in the published list (t.offset holds it) x n_tok
+// dense: every unit covers all n_tok tokens; row block = expert id x n_tok
+// (t.offset holds the expert id)
 __device__ inline UnitInfo decode(int u, int nA, int tilesA, int tilesB, const Tables& t,
                                   bool dense, int n_tok) {
   UnitInfo r;
@@ -310,7 +310,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     U = s_upub;
     for (int i = tid; i < U; i += kThreads) {
       t.active[i] = pubm[i];
-      t.offset[i] = pubidx[i];
+      t.offset[i] = pubm[i];  // rows [expert][token]: the combine needs no list
+    }
+    if (blockIdx.x == 0 && tid == 0 && a.stats) {
+      a.stats[1] = s_pcnt;  // published list (coreset / union) length
+      a.stats[3] = U;       // experts this rank streams
     }
     __syncthreads();
   } else {
@@ -824,16 +828,10 @@ __device__ inline void store_row4(const CombineArgs& a, size_t off, float4 v) {
 // experts this rank streamed).
 __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  extern __shared__ int inv[];  // [m] expert -> published list index
-  __shared__ int s_epoch, s_cnt;
+  if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 80, -1);
+  __shared__ int s_epoch;
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    s_epoch = *a.epoch;
-    s_cnt = static_cast<int>(a.pub[0] & 1023u);
-  }
-  __syncthreads();
-  const int cnt = s_cnt;
-  for (int i = tid; i < cnt; i += blockDim.x) inv[a.pub[1 + i] & 1023u] = i;
+  if (tid == 0) s_epoch = *a.epoch;
   __syncthreads();
   const float* y_slot = a.y_slot;
   if (a.world > 1) y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
@@ -841,58 +839,68 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
   const int i = blockIdx.x * blockDim.x + tid;
   if (i < a.n * vec) {
     const int tok = i / vec, c = (i - tok * vec) * 4;
-    const int rc = a.route_cnt[tok];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j = 0; j < rc; ++j) {
-      const size_t o = static_cast<size_t>(tok) * a.k + j;
-      const int e = a.route_idx[o];
-      const float g = static_cast<float>(a.route_gate[o]);
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(
-          y_slot + (static_cast<size_t>(inv[e]) * a.n + tok) * a.d + c));
-      // product then add (no contraction): the routed path's epilogue product
-      // followed by the combine's add
-      acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, g));
-      acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, g));
-      acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, g));
-      acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, g));
+    // 8 route entries (ascending experts, -1 padded) and their 8 rows in
+    // flight at once: two memory round trips instead of 2 per expert
+    for (int j0 = 0; j0 < a.k; j0 += 8) {
+      int e[8];
+      float g[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const size_t o = static_cast<size_t>(tok) * a.k + j0 + j;
+        e[j] = j0 + j < a.k ? a.route_idx[o] : -1;
+        g[j] = j0 + j < a.k ? static_cast<float>(a.route_gate[o]) : 0.f;
+      }
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (e[j] >= 0)
+          v[j] = __ldcg(reinterpret_cast<const float4*>(
+              y_slot + (static_cast<size_t>(e[j]) * a.n + tok) * a.d + c));
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (e[j] >= 0) {
+          // product then add (no contraction): the routed path's epilogue
+          // product followed by the combine's add
+          acc.x = __fadd_rn(acc.x, __fmul_rn(v[j].x, g[j]));
+          acc.y = __fadd_rn(acc.y, __fmul_rn(v[j].y, g[j]));
+          acc.z = __fadd_rn(acc.z, __fmul_rn(v[j].z, g[j]));
+          acc.w = __fadd_rn(acc.w, __fmul_rn(v[j].w, g[j]));
+        }
     }
     store_row4(a, static_cast<size_t>(tok) * a.d + c, acc);
   }
   if (blockIdx.x == 0 && a.stats) {
-    // unique experts of the route (moe_latency's count route, analysis.cpp:16-30)
+    // unique experts of the route (moe_latency's count route,
+    // analysis.cpp:16-30) and the selections; the FFN wrote stats[1], [3]
+    extern __shared__ int seen[];  // [m]
     __syncthreads();
-    for (int e = tid; e < a.m; e += blockDim.x) inv[e] = 0;
+    for (int e = tid; e < a.m; e += blockDim.x) seen[e] = 0;
     __syncthreads();
     int sel = 0;
     for (int o = tid; o < a.n * a.k; o += blockDim.x) {
-      const int tok = o / a.k, j = o - tok * a.k;
-      if (j < a.route_cnt[tok]) {
-        inv[a.route_idx[o]] = 1;
+      const int e = a.route_idx[o];
+      if (e >= 0) {
+        seen[e] = 1;
         ++sel;
       }
     }
-    __shared__ int s_sel, s_u, s_own;
-    if (tid == 0) s_sel = s_u = s_own = 0;
-    __syncthreads();
+    __shared__ int s_sel, s_u;
+    if (tid == 0) s_sel = s_u = 0;
+    __syncthreads();  // seen[] complete, counters zeroed
     atomicAdd(&s_sel, sel);
-    int u = 0, own = 0;
-    for (int e = tid; e < a.m; e += blockDim.x) u += inv[e];
-    for (int q = tid; q < cnt; q += blockDim.x) {
-      const int e = static_cast<int>(a.pub[1 + q] & 1023u);
-      own += e >= a.expert_lo && e < a.expert_hi;
-    }
+    int u = 0;
+    for (int e = tid; e < a.m; e += blockDim.x) u += seen[e];
     atomicAdd(&s_u, u);
-    atomicAdd(&s_own, own);
     __syncthreads();
     if (tid == 0) {
       a.stats[0] = s_u;
-      a.stats[1] = cnt;
       a.stats[2] = s_sel;
-      a.stats[3] = s_own;
     }
   }
   for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 81, -1);
   if (tid == 0 && atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
     *a.done_ctas = 0;
     atomicAdd(a.epoch, 1);
@@ -901,6 +909,7 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
 
 __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 80, -1);
   __shared__ int s_epoch;
   if (threadIdx.x == 0) s_epoch = *a.epoch;
   __syncthreads();
@@ -939,6 +948,7 @@ __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
   __syncthreads();
   // (relaxed atomics suffice: each CTA's epoch read completed before its
   // increment; the bump is published by the kernel's completion)
+  if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 81, -1);
   if (threadIdx.x == 0 && atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
     *a.done_ctas = 0;
     atomicAdd(a.epoch, 1);

@@ -388,7 +388,18 @@ __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int ch
 
 __global__ void __launch_bounds__(kFrontThreads, 1)
     front_kernel(const __grid_constant__ CUtensorMap wr_map, const __grid_constant__ BoxMaps x_maps,
-                 FrontArgs a) {
+                 const __grid_constant__ FrontArgs a_param) {
+  // The arguments are copied to shared memory once, all words in flight
+  // together: first touches of kernel-parameter (constant-bank) lines later
+  // in the kernel each stalled the critical path for ~1 us.
+  __shared__ FrontArgs a;
+  {
+    constexpr int kWords = static_cast<int>(sizeof(FrontArgs) / 4);
+    static_assert(sizeof(FrontArgs) % 4 == 0, "FrontArgs size");
+    if (threadIdx.x < kWords)
+      reinterpret_cast<int*>(&a)[threadIdx.x] = reinterpret_cast<const int*>(&a_param)[threadIdx.x];
+    __syncthreads();
+  }
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align to 1024 B by offsetting the shared array itself, so the compiler
   // keeps the shared address space (LDS/STS instead of generic LD/ST)

@@ -252,6 +252,8 @@ struct CombineArgs {
   int* stats;                // optional [4]
   __nv_bfloat16* y_bf16;     // optional: write bf16 here instead of fp32 y (layer stacks)
   const __nv_bfloat16* resid;  // optional residual stream added before the store (stacks)
+  uint64_t* trace;           // optional timeline (events 80 start, 81 end; CTA 0)
+  int trace_cap;
 };
 
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }

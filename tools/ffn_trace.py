@@ -102,6 +102,10 @@ def main():
         if (ev == 70 + i).any():
             out["ffn_" + nm] = [round(float(t[ev == 70 + i].min()), 2),
                                 round(float(t[ev == 70 + i].max()), 2)]
+    if (ev == 80).any():
+        out["combine_start_us"] = round(float(t[ev == 80].max()), 2)
+    if (ev == 81).any():
+        out["combine_end_us"] = round(float(t[ev == 81].max()), 2)
     out["kernel_span_us"] = float(t[ev == 5].max())
     out["cta_start_spread_us"] = float(t[ev == 0].max())
     out["gather_done_us"] = ([float(t[ev == 1].min()), float(t[ev == 1].max())]
