@@ -840,6 +840,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
                      !std::getenv("DESMOE_NO_DENSE");
   a.dense = dense ? 1 : 0;
   if (std::getenv("DESMOE_NO_L2PF")) a.flags |= 1;
+  if (const char* fl = std::getenv("DESMOE_FFN_FLAGS")) a.flags |= std::atoi(fl);  // experiments
   a.pub = ex->pub;
   a.route_words = ex->route_words;
   a.wa_base = ex->packed_a;

@@ -357,13 +357,49 @@ __device__ inline uint64_t gtime() {
 // Optional timeline trace: records {unit<<32 | cta<<8 | event, globaltimer ns}.
 __device__ inline void trace(uint64_t* buf, int cap, int event, int unit) {
   if (!buf) return;
+  // timestamp first: the cursor atomic can take microseconds when many CTAs
+  // trace at once (same-address atomics serialise in L2)
+  const uint64_t ts = gtime();
   unsigned long long* cur = reinterpret_cast<unsigned long long*>(buf);
   const unsigned long long i = atomicAdd(cur, 1ull);
   if (i < static_cast<unsigned long long>(cap)) {
     buf[2 + 2 * i] = (static_cast<uint64_t>(static_cast<uint32_t>(unit)) << 32) |
                      (static_cast<uint64_t>(blockIdx.x) << 8) | static_cast<uint64_t>(event);
-    buf[3 + 2 * i] = gtime();
+    buf[3 + 2 * i] = ts;
   }
+}
+
+// Atomic-free per-thread trace cursor: one emitting thread claims `slots`
+// records at its start (when the memory system is idle) and then only stores
+// into them, so tracing does not stall the traced code on a contended atomic.
+// Unused records are written as event 255 (ignored by the decoders).
+struct TraceCursor {
+  uint64_t* p;
+  int n, cap;
+};
+
+__device__ inline TraceCursor trace_open(uint64_t* buf, int cap, int slots) {
+  TraceCursor c{nullptr, 0, 0};
+  if (!buf) return c;
+  const unsigned long long i0 =
+      atomicAdd(reinterpret_cast<unsigned long long*>(buf), static_cast<unsigned long long>(slots));
+  const long long room = static_cast<long long>(cap) - static_cast<long long>(i0);
+  c.p = buf + 2 + 2 * i0;
+  c.cap = room <= 0 ? 0 : (room < slots ? static_cast<int>(room) : slots);
+  return c;
+}
+
+__device__ inline void trace_put(TraceCursor& c, int event, int unit) {
+  if (c.n >= c.cap) return;
+  const uint64_t ts = gtime();
+  c.p[2 * c.n] = (static_cast<uint64_t>(static_cast<uint32_t>(unit)) << 32) |
+                 (static_cast<uint64_t>(blockIdx.x) << 8) | static_cast<uint64_t>(event);
+  c.p[2 * c.n + 1] = ts;
+  ++c.n;
+}
+
+__device__ inline void trace_close(TraceCursor& c) {
+  for (; c.n < c.cap; ++c.n) c.p[2 * c.n] = 255;
 }
 
 // Programmatic dependent launch: let the next kernel in the stream start its
@@ -404,6 +440,16 @@ __device__ inline uint64_t ld_relaxed_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ inline uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ inline void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ inline int ld_acquire(const int* p) {

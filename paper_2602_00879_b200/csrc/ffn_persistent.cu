@@ -156,7 +156,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_tok = a.n_tok, k = a.top_k, m = a.m, d = a.d, f = a.f;
-  if (tid == 0) trace(a.trace, a.trace_cap, 0, -1);
+  // timeline (desmoe_set_trace): tid 0 = prologue + scheduler, 96 = activation
+  // producer, 128 = epilogue; atomic-free after the claim here
+  TraceCursor tc{nullptr, 0, 0};
+  if (a.trace && (tid == 0 || tid == 96 || tid == 128)) tc = trace_open(a.trace, a.trace_cap, 96);
+  if (tid == 0) trace_put(tc, 0, -1);
   const bool swiglu = a.mode == 0;
   const bool dense = a.dense != 0;
   const int S = a.stages;
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __threadfence();
     atomic_add_release(x_ready, 1);
     if (a.trace) s_pts[4] = gtime();
-    trace(a.trace, a.trace_cap, 1, -1);
+    trace_put(tc, 1, -1);
   }
   const uint32_t tmem_base = *tmem_slot;
 
@@ -500,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         unit_q[q] = uu;
         mbar_arrive(&qfull[q]);
         if (uu < 0) break;
-        trace(a.trace, a.trace_cap, 2, uu);
+        trace_put(tc, 2, uu);
         const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
         const int ksteps = phaseA ? ksA : ksB;
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           fence_proxy_async_global();
           x_seen = true;
-          trace(a.trace, a.trace_cap, 6, uu);
+          trace_put(tc, 6, uu);
         }
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int s = it % S;
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (ld_acquire(flag) == 0) {
                 while (ld_acquire(flag) == 0) {
                 }
-                trace(a.trace, a.trace_cap, 7, uu);
+                trace_put(tc, 7, uu);
               }
             }
             fence_proxy_async_global();
@@ -709,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           atomic_add_release(&h_ready[ui.expert * tilesA + ui.tile], 1);
         }
       }
-      if (etid == 0) trace(a.trace, a.trace_cap, 3, uu);
+      if (etid == 0) trace_put(tc, 3, uu);
       ++nunit;
     }
   }
@@ -729,7 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __threadfence_system();
     for (int p = 0; p < a.world; ++p) atomic_add_release_sys(a.peer_flag[p], 1ull);
   }
-  if (tid == 0) trace(a.trace, a.trace_cap, 5, -1);
+  if (tid == 0) trace_put(tc, 5, -1);
+  trace_close(tc);
   // early mode never waited for the front kernel: do it before completing, so
   // the FFN's completion (which the combine waits for) implies the front's
   if (a.early && tid == 0) pdl_wait();

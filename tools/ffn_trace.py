@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--json", default="")
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm before the traced call")
     ap.add_argument("--block", type=int, default=0, help="override the block size N")
+    ap.add_argument("--raw", default="", help="also save the raw records (.npz) for offline analysis")
     args = ap.parse_args()
     import torch
     from bench import CONFIGS
@@ -38,7 +39,7 @@ def main():
     wr = synth.router_weights(m, d, seed=2000)
     layer = DesMoeLayer(LayerConfig(m, k, d, f, strategy=args.strategy, vote_beta=cfg["beta"]),
                         wr, wg, wu, wd)
-    cap = 1 << 14
+    cap = 1 << 17
     buf = torch.zeros(2 + 2 * cap, dtype=torch.int64, device="cuda")
     L = _lib.lib()
     x = synth.hidden_states(n, d, seed=7, rho=cfg["rho"])
@@ -57,6 +58,7 @@ def main():
     raw = buf.cpu().numpy().view(np.uint64)
     cnt = min(int(raw[0]), cap)
     rec = raw[2: 2 + 2 * cnt].reshape(cnt, 2)
+    rec = rec[(rec[:, 0] & 0xFF) != 255]  # unused per-thread trace records
     ev = (rec[:, 0] & 0xFF).astype(int)
     cta = ((rec[:, 0] >> 8) & 0xFFFFFF).astype(int)
     unit = (rec[:, 0] >> 32).astype(np.int64)
@@ -64,6 +66,8 @@ def main():
     t = rec[:, 1].astype(np.int64)
     t0 = t[ev == 40].min() if (ev == 40).any() else t[ev == 0].min()
     t = (t - t0) / 1e3  # µs
+    if args.raw:
+        np.savez(args.raw, ev=ev, cta=cta, unit=unit, t=t, raw=rec)
     stats = layer.stats.cpu().numpy()
     U = int(stats[0])
     tilesA = f // 64
@@ -80,7 +84,8 @@ def main():
               "exit", "votes", "ranked", "arrived", "mma_done", "drain_done", "copies_issued", "sums_done", "topk_done"]
     for i, nm in enumerate(["l4_enter", "l4_call", "l4_selected", "l4_risky"]):
         if (ev == 74 + i).any():
-            out["front_" + nm] = round(float(t[ev == 74 + i].max()), 2)
+            out["front_" + nm] = [round(float(t[ev == 74 + i].min()), 2),
+                                  round(float(t[ev == 74 + i].max()), 2)]
     chunks = [round(float(t[ev == 66 + c].max()), 2) for c in range(4) if (ev == 66 + c).any()
               and float(t[ev == 66 + c].max()) < 1e6 and float(t[ev == 66 + c].max()) > 0]
     if chunks:
