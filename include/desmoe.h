@@ -126,6 +126,37 @@ int desmoe_route(desmoe_ctx* ctx, const double* logits_dev, int n, const desmoe_
 int desmoe_route_f32(desmoe_ctx* ctx, const float* logits_dev, int n,
                      const desmoe_route_cfg* cfg, const desmoe_route_out* out, void* stream);
 
+/* ---- comparison policies (baselines.hpp / baselines.cpp) -------------------
+ * BaselineParams (baselines.hpp:17-24). */
+#define DESMOE_BASE_TOPK_REDUCE 0
+#define DESMOE_BASE_NAEE 1
+#define DESMOE_BASE_MCMOE 2
+#define DESMOE_SCORE_MAX_GATE 0
+#define DESMOE_SCORE_NEG_ENTROPY 1
+typedef struct {
+  int method;                      /* DESMOE_BASE_*                          */
+  int k_reduced;                   /* TOPK_REDUCE: k in [1, top_k]           */
+  double naee_beta;                /* NAEE: (0, 1)                           */
+  double mcmoe_beta;               /* MCMOE: (0, 1)                          */
+  double mcmoe_important_fraction; /* MCMOE: [0, 1]                          */
+  int mcmoe_score;                 /* DESMOE_SCORE_*                         */
+} desmoe_baseline_cfg;
+
+/* baseline_route (baselines.cpp:125-137): topk_reduce_route (:10-16),
+ * naee_route (:64-76) or mcmoe_route (:78-123) of logits_dev [n x experts]
+ * (fp64; _f32 for router / trace logits). Writes route_idx/gate/cnt of `out`
+ * (row stride top_k; NAEE / MC-MoE rows keep fewer than top_k, -1 / 0
+ * padded) and, if given, probs_dev. Parameter errors carry the reference's
+ * messages ("k_reduced outside [1, top_k]", "naee beta outside (0, 1)",
+ * "mcmoe beta outside (0, 1)", "important_fraction outside [0, 1]");
+ * non-finite logits are reported by desmoe_check. */
+int desmoe_baseline_route(desmoe_ctx* ctx, const double* logits_dev, int n,
+                          const desmoe_route_cfg* cfg, const desmoe_baseline_cfg* params,
+                          const desmoe_route_out* out, void* stream);
+int desmoe_baseline_route_f32(desmoe_ctx* ctx, const float* logits_dev, int n,
+                              const desmoe_route_cfg* cfg, const desmoe_baseline_cfg* params,
+                              const desmoe_route_out* out, void* stream);
+
 /* Stage 1 only: des_seq_coreset (des.cpp:33-45) / des_vote_coreset
  * (des.cpp:65-95, also the contract of fused_vote_pipeline des.cpp:166-224).
  * cfg->strategy selects which; out->coreset_dev / coreset_size_dev required. */

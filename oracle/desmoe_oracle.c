@@ -136,6 +136,122 @@ int or_topk_route(const double* x, int n, int m, int k, int act, int* idx, doubl
   return 0;
 }
 
+/* ---- comparison policies (baselines.cpp) ---------------------------------- */
+
+/* Rank order (value desc, index asc) of the token's top-k: writes rank[0..k). */
+static void rank_top(const double* p, int m, int k, int* rank) {
+  unsigned char* taken = (unsigned char*)calloc((size_t)m, 1);
+  for (int r = 0; r < k; ++r) {
+    int best = -1;
+    for (int i = 0; i < m; ++i) {
+      if (taken[i]) continue;
+      if (best < 0 || precedes(p[i], i, p[best], best)) best = i;
+    }
+    taken[best] = 1;
+    rank[r] = best;
+  }
+  free(taken);
+}
+
+/* baselines.cpp:23-53 (naee_kept): returns the kept count; kept ids ascending
+ * in out[0..keep). total sums the selection in ascending index order; the
+ * tails accumulate from rank K down; rank 1 always stays. */
+static int naee_kept(const double* p, int m, int k, double beta, int* out) {
+  int rank[64], asc[64];
+  rank_top(p, m, k, rank);
+  for (int j = 0; j < k; ++j) asc[j] = rank[j];
+  qsort(asc, (size_t)k, sizeof(int), cmp_int);
+  double total = 0.0;
+  for (int j = 0; j < k; ++j) total += p[asc[j]];
+  double tails[65];
+  double tail = 0.0;
+  for (int u = k; u >= 2; --u) {
+    tail += p[rank[u - 1]];
+    tails[u] = tail;
+  }
+  int keep = k;
+  for (int i = 2; i <= k; ++i)
+    if (tails[i] < beta * total) {
+      keep = i - 1;
+      break;
+    }
+  for (int j = 0; j < keep; ++j) out[j] = rank[j];
+  qsort(out, (size_t)keep, sizeof(int), cmp_int);
+  return keep;
+}
+
+/* baseline_route (baselines.cpp:125-137): method 0 = topk_reduce (:10-16),
+ * 1 = naee (:64-76), 2 = mcmoe (:78-123; score 0 = max gate, 1 = -entropy).
+ * idx/gate [n x k] padded with -1 / 0, cnt[n]. k <= 64. */
+int or_baseline_route(const double* x, int n, int m, int k, int act, int method, int k_reduced,
+                      double naee_beta, double mcmoe_beta, double fraction, int score,
+                      int* idx, double* gate, int* cnt) {
+  if (method == 0 && (k_reduced < 1 || k_reduced > k))
+    return fail("k_reduced outside [1, top_k]");
+  if (method == 1 && (!(naee_beta > 0.0) || !(naee_beta < 1.0)))
+    return fail("naee beta outside (0, 1)");
+  if (method == 2) {
+    if (!(mcmoe_beta > 0.0) || !(mcmoe_beta < 1.0)) return fail("mcmoe beta outside (0, 1)");
+    if (fraction < 0.0 || fraction > 1.0) return fail("important_fraction outside [0, 1]");
+  }
+  if (method < 0 || method > 2) return fail("unknown baseline method");
+  if (check_pool(m, k)) return 1;
+  if (k > 64) return fail("top_k > 64 (restatement limit)");
+  double* p = (double*)malloc(sizeof(double) * (size_t)n * m);
+  if (or_activate(x, n, m, act, p)) { free(p); return 1; }
+  /* MC-MoE: the ceil(fraction * N) tokens first in a stable descending sort
+   * of the score keep their full top-K (:104-113) */
+  unsigned char* full = (unsigned char*)calloc((size_t)n, 1);
+  if (method == 2) {
+    double* sc = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int t = 0; t < n; ++t) {
+      const double* row = p + (size_t)t * m;
+      if (score == 0) {
+        double v = row[0];
+        for (int i = 1; i < m; ++i) v = row[i] > v ? row[i] : v;
+        sc[t] = v;
+      } else {
+        double h = 0.0;
+        for (int i = 0; i < m; ++i)
+          if (row[i] > 0.0) h -= row[i] * log(row[i]);
+        sc[t] = -h;
+      }
+    }
+    int important = (int)ceil(fraction * n);
+    if (important > n) important = n;
+    for (int t = 0; t < n; ++t) {
+      int r = 0;
+      for (int q = 0; q < n; ++q) r += sc[q] > sc[t] || (sc[q] == sc[t] && q < t);
+      full[t] = r < important;
+    }
+    free(sc);
+  }
+  for (int t = 0; t < n; ++t) {
+    const double* row = p + (size_t)t * m;
+    int sel[64];
+    int c;
+    if (method == 0) {
+      c = k_reduced;
+      or_select_top(row, m, NULL, 0, c, sel);
+    } else if (method == 2 && full[t]) {
+      c = k;
+      or_select_top(row, m, NULL, 0, c, sel);
+    } else {
+      c = naee_kept(row, m, k, method == 1 ? naee_beta : mcmoe_beta, sel);
+    }
+    double g[64];
+    renorm(row, sel, c, g);
+    for (int j = 0; j < k; ++j) {
+      idx[(size_t)t * k + j] = j < c ? sel[j] : -1;
+      gate[(size_t)t * k + j] = j < c ? g[j] : 0.0;
+    }
+    cnt[t] = c;
+  }
+  free(full);
+  free(p);
+  return 0;
+}
+
 int or_vote_budget(double beta, int m) { return (int)floor(beta * m); }
 
 /* des.cpp:49-61 */

@@ -100,6 +100,21 @@ class Ref(_Base):
                                             _f64p, _i32p])(x, n, m, k, act, idx, gate, cnt))
         return Route(idx, gate, cnt)
 
+    def baseline_route(self, logits, k, method, act=0, k_reduced=1, naee_beta=0.5,
+                       mcmoe_beta=0.5, fraction=0.5, score=0):
+        """baseline_route (baselines.cpp:125-137); method 0/1/2 = topk_reduce /
+        naee / mcmoe, score 0/1 = max gate / -entropy."""
+        x = _f64(logits)
+        n, m = x.shape
+        idx, gate, cnt = (np.empty((n, k), np.int32), np.empty((n, k), np.float64),
+                          np.empty(n, np.int32))
+        self._check(self._fn("baseline_route",
+                             [_f64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                              C.c_double, C.c_double, C.c_double, C.c_int, _i32p, _f64p,
+                              _i32p])(x, n, m, k, act, method, k_reduced, naee_beta,
+                                      mcmoe_beta, fraction, score, idx, gate, cnt))
+        return Route(idx, gate, cnt)
+
     def seq_coreset(self, logits, k, local_k, act=0):
         x = _f64(logits)
         n, m = x.shape
@@ -274,6 +289,21 @@ class Port(_Base):
                           np.empty(n, np.int32))
         self._check(self._fn("topk_route", [_f64p, C.c_int, C.c_int, C.c_int, C.c_int, _i32p,
                                             _f64p, _i32p])(x, n, m, k, act, idx, gate, cnt))
+        return Route(idx, gate, cnt)
+
+    def baseline_route(self, logits, k, method, act=0, k_reduced=1, naee_beta=0.5,
+                       mcmoe_beta=0.5, fraction=0.5, score=0):
+        """baseline_route (baselines.cpp:125-137); method 0/1/2 = topk_reduce /
+        naee / mcmoe, score 0/1 = max gate / -entropy."""
+        x = _f64(logits)
+        n, m = x.shape
+        idx, gate, cnt = (np.empty((n, k), np.int32), np.empty((n, k), np.float64),
+                          np.empty(n, np.int32))
+        self._check(self._fn("baseline_route",
+                             [_f64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                              C.c_double, C.c_double, C.c_double, C.c_int, _i32p, _f64p,
+                              _i32p])(x, n, m, k, act, method, k_reduced, naee_beta,
+                                      mcmoe_beta, fraction, score, idx, gate, cnt))
         return Route(idx, gate, cnt)
 
     def seq_coreset(self, logits, k, local_k, act=0):

@@ -27,6 +27,7 @@
 #include <thread>
 #include <vector>
 
+#include "dessim/baselines.hpp"
 #include "dessim/analysis.hpp"
 #include "dessim/core.hpp"
 #include "dessim/des.hpp"
@@ -186,6 +187,24 @@ int dsref_des_run(const double* logits, int n, int m, int k, int act, int strate
     DesResult r = des_run(block_of(logits, n, m), pool(m, k, act), p);
     copy_members(r.coreset, members, n_members);
     flatten(r.assignment, k, idx, gates, counts);
+  });
+}
+
+// method: 0 = topk_reduce, 1 = naee, 2 = mcmoe (BaselineMethod order,
+// baselines.hpp:8); score: 0 = max_gate, 1 = neg_entropy
+int dsref_baseline_route(const double* logits, int n, int m, int k, int act, int method,
+                         int k_reduced, double naee_beta, double mcmoe_beta, double fraction,
+                         int score, int* idx, double* gates, int* counts) {
+  return guarded([&] {
+    BaselineParams bp;
+    bp.method = method == 0 ? BaselineMethod::topk_reduce
+                            : (method == 1 ? BaselineMethod::naee : BaselineMethod::mcmoe);
+    bp.k_reduced = k_reduced;
+    bp.naee_beta = naee_beta;
+    bp.mcmoe_beta = mcmoe_beta;
+    bp.mcmoe_important_fraction = fraction;
+    bp.mcmoe_score = score == 1 ? ImportanceScore::neg_entropy : ImportanceScore::max_gate;
+    flatten(baseline_route(block_of(logits, n, m), pool(m, k, act), bp), k, idx, gates, counts);
   });
 }
 

@@ -34,6 +34,15 @@ class RouteOut(C.Structure):
                 ("probs_dev", C.c_void_p)]
 
 
+class BaselineCfg(C.Structure):  # desmoe_baseline_cfg = BaselineParams (baselines.hpp:17-24)
+    _fields_ = [("method", C.c_int), ("k_reduced", C.c_int), ("naee_beta", C.c_double),
+                ("mcmoe_beta", C.c_double), ("mcmoe_important_fraction", C.c_double),
+                ("mcmoe_score", C.c_int)]
+
+
+BASE_TOPK_REDUCE, BASE_NAEE, BASE_MCMOE = 0, 1, 2
+SCORE_MAX_GATE, SCORE_NEG_ENTROPY = 0, 1
+
 # name -> (restype, argtypes)
 _P, _I, _D = C.c_void_p, C.c_int, C.c_double
 _SIGS = {
@@ -51,6 +60,10 @@ _SIGS = {
     "desmoe_activate": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "desmoe_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
     "desmoe_route_f32": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
+    "desmoe_baseline_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(BaselineCfg),
+                                   C.POINTER(RouteOut), _P]),
+    "desmoe_baseline_route_f32": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(BaselineCfg),
+                                       C.POINTER(RouteOut), _P]),
     "desmoe_coreset": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
     "desmoe_constrained_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(C.c_int), _I,
                                       C.POINTER(RouteOut), _P]),

@@ -621,6 +621,77 @@ int desmoe_constrained_route(desmoe_ctx* c, const double* logits, int n,
   return launch_reroute(c, n, m, k, false, ridx, rgate, rcnt, st);
 }
 
+}  // extern "C"
+
+template <typename T>
+int baseline_impl(desmoe_ctx* c, const T* logits, int n, const desmoe_route_cfg* cfg,
+                  const desmoe_baseline_cfg* b, const desmoe_route_out* out, cudaStream_t st) {
+  if (!cfg || !b) return fail(DESMOE_EINVAL, "null config");
+  const int m = cfg->experts, k = cfg->top_k;
+  int rc = check_block(c, n, m);
+  if (rc) return rc;
+  if (k < 1 || k > m || k > c->max_k || k > 32) return fail(DESMOE_EINVAL, "top_k out of range");
+  if (cfg->activation < 0 || cfg->activation > 2)
+    return fail(DESMOE_EINVAL, "unknown gate activation");
+  BaselineArgs<T> a{};
+  // parameter checks in the reference's order (before activate)
+  switch (b->method) {
+    case DESMOE_BASE_TOPK_REDUCE:  // baselines.cpp:12-14
+      if (b->k_reduced < 1 || b->k_reduced > k)
+        return fail(DESMOE_EINVAL, "k_reduced outside [1, top_k]");
+      break;
+    case DESMOE_BASE_NAEE:  // :65-67
+      if (!(b->naee_beta > 0.0) || !(b->naee_beta < 1.0))
+        return fail(DESMOE_EINVAL, "naee beta outside (0, 1)");
+      a.beta = b->naee_beta;
+      break;
+    case DESMOE_BASE_MCMOE: {  // :80-85, important = ceil(fraction * N) (:104-105)
+      if (!(b->mcmoe_beta > 0.0) || !(b->mcmoe_beta < 1.0))
+        return fail(DESMOE_EINVAL, "mcmoe beta outside (0, 1)");
+      if (b->mcmoe_important_fraction < 0.0 || b->mcmoe_important_fraction > 1.0)
+        return fail(DESMOE_EINVAL, "important_fraction outside [0, 1]");
+      if (b->mcmoe_score != DESMOE_SCORE_MAX_GATE && b->mcmoe_score != DESMOE_SCORE_NEG_ENTROPY)
+        return fail(DESMOE_EINVAL, "unknown importance score");
+      a.beta = b->mcmoe_beta;
+      a.score = b->mcmoe_score;
+      a.important = std::min(static_cast<int>(std::ceil(b->mcmoe_important_fraction * n)), n);
+      break;
+    }
+    default:
+      return fail(DESMOE_EINVAL, "unknown baseline method");
+  }
+  a.logits = logits;
+  a.n = n;
+  a.m = m;
+  a.k = k;
+  a.act = cfg->activation;
+  a.method = b->method;
+  a.k_reduced = b->k_reduced;
+  a.probs = out && out->probs_dev ? out->probs_dev : c->probs;
+  a.route_idx = out && out->route_idx_dev ? out->route_idx_dev : c->route_idx;
+  a.route_gate = out && out->route_gate_dev ? out->route_gate_dev : c->route_gate;
+  a.route_cnt = out && out->route_cnt_dev ? out->route_cnt_dev : c->route_cnt;
+  a.err = c->err;
+  const size_t smem = static_cast<size_t>(n) * sizeof(double) + 32 * 32 * sizeof(int);
+  baseline_route_kernel<T><<<1, 1024, smem, st>>>(a);
+  DESMOE_LAUNCHED();
+  return DESMOE_OK;
+}
+
+extern "C" {
+
+int desmoe_baseline_route(desmoe_ctx* c, const double* logits, int n, const desmoe_route_cfg* cfg,
+                          const desmoe_baseline_cfg* b, const desmoe_route_out* out,
+                          void* stream) {
+  return baseline_impl<double>(c, logits, n, cfg, b, out, S(stream));
+}
+
+int desmoe_baseline_route_f32(desmoe_ctx* c, const float* logits, int n,
+                              const desmoe_route_cfg* cfg, const desmoe_baseline_cfg* b,
+                              const desmoe_route_out* out, void* stream) {
+  return baseline_impl<float>(c, logits, n, cfg, b, out, S(stream));
+}
+
 int desmoe_permute(desmoe_ctx* c, const int* route_idx, const int* route_cnt, int n, int k,
                    int m, int* expert_count, int* expert_offset, int* slot_of, int* slot_token,
                    int* active, int* n_active, void* stream) {

@@ -256,6 +256,23 @@ struct CombineArgs {
   int trace_cap;
 };
 
+// Comparison policies (baselines.cu): method 0 = top-k reduce, 1 = NAEE,
+// 2 = MC-MoE (score 0 = max gate, 1 = -entropy).
+template <typename T>
+struct BaselineArgs {
+  const T* logits;     // [n x m]
+  int n, m, k, act;
+  int method, k_reduced, score, important;
+  double beta;
+  double* probs;       // [n x m] workspace (activated rows)
+  int* route_idx;      // [n x k]
+  double* route_gate;  // [n x k]
+  int* route_cnt;      // [n]
+  int* err;            // bit 0: non-finite logit
+};
+template <typename T>
+__global__ void baseline_route_kernel(BaselineArgs<T> a);
+
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }
 
 __global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,

@@ -446,6 +446,82 @@ def des_run(block: RouterBlock, cfg: PoolConfig, params: DesParams) -> DesResult
 
 
 # ---------------------------------------------------------------------------
+# baselines.hpp: comparison expert-skipping policies (csrc/baselines.cu)
+# ---------------------------------------------------------------------------
+
+class BaselineMethod(enum.IntEnum):  # baselines.hpp:8
+    topk_reduce = 0
+    naee = 1
+    mcmoe = 2
+
+
+class ImportanceScore(enum.IntEnum):  # baselines.hpp:13
+    max_gate = 0
+    neg_entropy = 1
+
+
+@dataclass
+class BaselineParams:  # baselines.hpp:17-24
+    method: BaselineMethod = BaselineMethod.topk_reduce
+    k_reduced: int = 1
+    naee_beta: float = 0.5
+    mcmoe_beta: float = 0.5
+    mcmoe_important_fraction: float = 0.5
+    mcmoe_score: ImportanceScore = ImportanceScore.max_gate
+
+
+def _baseline(block: RouterBlock, cfg: PoolConfig, b) -> RoutingAssignment:
+    _check_block(block, cfg)
+    n, m, k = block.block_size, block.experts, cfg.top_k
+    ctx = _Ctx.get(n, m, k)
+    bufs = _RouteBufs(n, m, k)
+    x = _dev_f64(block.logits)
+    rc = _cfg(cfg, _lib.VANILLA)
+    check(lib().desmoe_baseline_route(ctx.h, _ptr(x), n, C.byref(rc), C.byref(b),
+                                      C.byref(bufs.out()), _stream()))
+    _finish(ctx)
+    return bufs.assignment()
+
+
+def topk_reduce_route(block: RouterBlock, cfg: PoolConfig, k_reduced: int) -> RoutingAssignment:
+    """baselines.cpp:10-16: vanilla routing with K -> k_reduced."""
+    if k_reduced < 1 or k_reduced > cfg.top_k:
+        raise ValueError("k_reduced outside [1, top_k]")
+    return _baseline(block, cfg, _lib.BaselineCfg(_lib.BASE_TOPK_REDUCE, k_reduced, 0.5, 0.5,
+                                                  0.5, 0))
+
+
+def naee_route(block: RouterBlock, cfg: PoolConfig, beta: float) -> RoutingAssignment:
+    """baselines.cpp:64-76: drop the selected gates' cumulative tail below beta."""
+    if not (beta > 0.0) or not (beta < 1.0):
+        raise ValueError("naee beta outside (0, 1)")
+    return _baseline(block, cfg, _lib.BaselineCfg(_lib.BASE_NAEE, 1, beta, 0.5, 0.5, 0))
+
+
+def mcmoe_route(block: RouterBlock, cfg: PoolConfig, beta: float, important_fraction: float,
+                score: ImportanceScore = ImportanceScore.max_gate) -> RoutingAssignment:
+    """baselines.cpp:78-123: important tokens keep top-K, the rest get NAEE."""
+    if not (beta > 0.0) or not (beta < 1.0):
+        raise ValueError("mcmoe beta outside (0, 1)")
+    if important_fraction < 0.0 or important_fraction > 1.0:
+        raise ValueError("important_fraction outside [0, 1]")
+    return _baseline(block, cfg, _lib.BaselineCfg(_lib.BASE_MCMOE, 1, 0.5, beta,
+                                                  important_fraction, int(score)))
+
+
+def baseline_route(block: RouterBlock, cfg: PoolConfig,
+                   params: BaselineParams) -> RoutingAssignment:  # baselines.cpp:125-137
+    if params.method == BaselineMethod.topk_reduce:
+        return topk_reduce_route(block, cfg, params.k_reduced)
+    if params.method == BaselineMethod.naee:
+        return naee_route(block, cfg, params.naee_beta)
+    if params.method == BaselineMethod.mcmoe:
+        return mcmoe_route(block, cfg, params.mcmoe_beta, params.mcmoe_important_fraction,
+                           params.mcmoe_score)
+    raise ValueError("unknown baseline method")
+
+
+# ---------------------------------------------------------------------------
 # ExpertBank / moe_forward (gating.hpp:48-72) on the tcgen05 expert kernels
 # ---------------------------------------------------------------------------
 

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "dessim/baselines.hpp"
 #include "../../include/desmoe.h"
 #include "dessim/core.hpp"
 #include "dessim/des.hpp"
@@ -622,4 +623,82 @@ VoteResult fused_vote_pipeline(const RouterBlock& block, const PoolConfig& cfg, 
   return des_vote_coreset(block, cfg, beta, VoteSource::activated);
 }
 
+// ===========================================================================
+// baselines.hpp
+// ===========================================================================
+
+namespace {
+
+RoutingAssignment run_baseline(const RouterBlock& block, const PoolConfig& cfg,
+                               const desmoe_baseline_cfg& b) {
+  const int n = block.block_size, m = block.experts, k = cfg.top_k;
+  Gpu& g = gpu(n, m, k);
+  const double* x = g.upload(0, block.logits.data(), block.logits.size());
+  int* idx = g.s[1].get<int>(static_cast<size_t>(n) * k);
+  double* gate = g.s[2].get<double>(static_cast<size_t>(n) * k);
+  int* cnt = g.s[3].get<int>(n);
+  desmoe_route_cfg c = route_cfg(cfg, DESMOE_VANILLA);
+  desmoe_route_out o{};
+  o.route_idx_dev = idx;
+  o.route_gate_dev = gate;
+  o.route_cnt_dev = cnt;
+  ok(desmoe_baseline_route(g.ctx, x, n, &c, &b, &o, g.st()));
+  g.finish();
+  return read_assignment(g, idx, gate, cnt, n, k);
+}
+
+}  // namespace
+
+RoutingAssignment topk_reduce_route(const RouterBlock& block, const PoolConfig& cfg,
+                                    int k_reduced) {
+  if (k_reduced < 1 || k_reduced > cfg.top_k)  // baselines.cpp:12-14
+    throw std::invalid_argument("k_reduced outside [1, top_k]");
+  validate_block(block, cfg);
+  desmoe_baseline_cfg b{};
+  b.method = DESMOE_BASE_TOPK_REDUCE;
+  b.k_reduced = k_reduced;
+  return run_baseline(block, cfg, b);
+}
+
+RoutingAssignment naee_route(const RouterBlock& block, const PoolConfig& cfg, double beta) {
+  if (!(beta > 0.0) || !(beta < 1.0))  // baselines.cpp:65-67
+    throw std::invalid_argument("naee beta outside (0, 1)");
+  validate_block(block, cfg);
+  desmoe_baseline_cfg b{};
+  b.method = DESMOE_BASE_NAEE;
+  b.naee_beta = beta;
+  return run_baseline(block, cfg, b);
+}
+
+RoutingAssignment mcmoe_route(const RouterBlock& block, const PoolConfig& cfg, double beta,
+                              double important_fraction, ImportanceScore score) {
+  if (!(beta > 0.0) || !(beta < 1.0))  // baselines.cpp:80-85
+    throw std::invalid_argument("mcmoe beta outside (0, 1)");
+  if (important_fraction < 0.0 || important_fraction > 1.0)
+    throw std::invalid_argument("important_fraction outside [0, 1]");
+  validate_block(block, cfg);
+  desmoe_baseline_cfg b{};
+  b.method = DESMOE_BASE_MCMOE;
+  b.mcmoe_beta = beta;
+  b.mcmoe_important_fraction = important_fraction;
+  b.mcmoe_score =
+      score == ImportanceScore::neg_entropy ? DESMOE_SCORE_NEG_ENTROPY : DESMOE_SCORE_MAX_GATE;
+  return run_baseline(block, cfg, b);
+}
+
+RoutingAssignment baseline_route(const RouterBlock& block, const PoolConfig& cfg,
+                                 const BaselineParams& params) {
+  switch (params.method) {  // baselines.cpp:125-137
+    case BaselineMethod::topk_reduce:
+      return topk_reduce_route(block, cfg, params.k_reduced);
+    case BaselineMethod::naee:
+      return naee_route(block, cfg, params.naee_beta);
+    case BaselineMethod::mcmoe:
+      return mcmoe_route(block, cfg, params.mcmoe_beta, params.mcmoe_important_fraction,
+                         params.mcmoe_score);
+  }
+  throw std::invalid_argument("unknown baseline method");
+}
+
 }  // namespace dessim
+

@@ -1,9 +1,10 @@
-"""The reference's OWN unit tests (/root/reference/proj/tests/test_gating.cpp
-and test_des.cpp, compiled unchanged by tests/cpp/Makefile) run against the
-C++ facade include/dessim/*.hpp -> libdessim_gpu.so -> libdesmoe.so.
+"""The reference's OWN unit tests (/root/reference/proj/tests/test_gating.cpp,
+test_des.cpp and test_baselines.cpp, compiled unchanged by tests/cpp/Makefile)
+run against the C++ facade include/dessim/*.hpp -> libdessim_gpu.so ->
+libdesmoe.so.
 
 * CPU: the doctest stand-in runs the same suites against the reference library
-  itself (oracle/_ref) with 47/47 passing, the facade exports the reference's
+  itself (oracle/_ref) with 60/60 passing, the facade exports the reference's
   dessim:: symbols, and without a GPU the facade fails loudly (no CPU path).
 * GPU: every reference test case passes on the B200 path.
 """
@@ -28,7 +29,7 @@ def _run(path):
 def test_doctest_standin_runs_reference_suites_on_reference():
     r = _run(ON_REF)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "| 47 passed | 0 failed" in r.stdout, r.stdout
+    assert "| 60 passed | 0 failed" in r.stdout, r.stdout
 
 
 def test_facade_exports_reference_api():
@@ -40,7 +41,8 @@ def test_facade_exports_reference_api():
                 "dessim::vote_budget(", "dessim::des_seq_coreset(", "dessim::des_vote_coreset(",
                 "dessim::constrained_route(", "dessim::des_run(", "dessim::fused_vote_pipeline(",
                 "dessim::validate_config(", "dessim::make_router_block(", "dessim::Rng::next_normal(",
-                "dessim::Coreset::of("]:
+                "dessim::Coreset::of(", "dessim::topk_reduce_route(", "dessim::naee_route(",
+                "dessim::mcmoe_route(", "dessim::baseline_route("]:
         assert sym in out, sym
 
 

@@ -304,3 +304,77 @@ def test_golden_fixtures(port):
         r = port.topk_route(x, k, act)
         assert np.array_equal(r.idx, g[f"van_idx{i}"])
         assert np.array_equal(r.gate, g[f"van_gate{i}"])
+
+
+# ---- comparison policies (baselines.cpp; proj/tests/test_baselines.cpp) --------
+
+def _probs_block(rows):
+    """block_with_probs (test_baselines.cpp:18-27): logits = log(p)."""
+    return np.log(np.asarray(rows, np.float64))
+
+
+def test_baselines_hand(impl):
+    x = _probs_block([[0.5, 0.3, 0.15, 0.05]])
+    # tail(4) = 0.05 < 0.2, tail(3) = 0.20 is not: ranks 1..3 stay (:61-69)
+    r = impl.baseline_route(x, 4, 1, naee_beta=0.2)
+    assert r.experts(0) == [0, 1, 2]
+    for g, w in zip(r.gates(0), [0.5 / 0.95, 0.3 / 0.95, 0.15 / 0.95]):
+        assert abs(g - w) <= 1e-9
+    r = impl.baseline_route(x, 4, 1, naee_beta=0.6)  # tail(2) = 0.5 < 0.6 (:71-74)
+    assert r.experts(0) == [0] and r.gates(0) == [1.0]
+    # MC-MoE: the confident token keeps its top-K, the diffuse one is skipped (:133-146)
+    x = _probs_block([[0.9, 0.05, 0.03, 0.02], [0.3, 0.28, 0.22, 0.2]])
+    r = impl.baseline_route(x, 4, 2, mcmoe_beta=0.6, fraction=0.5)
+    assert r.experts(0) == [0, 1, 2, 3] and r.experts(1) == [0, 1]
+    assert abs(r.gates(1)[0] - 0.3 / 0.58) <= 1e-9 and abs(r.gates(1)[1] - 0.28 / 0.58) <= 1e-9
+    # top-k reduce with k = 1 is the per-token argmax with gate 1 (:46-58)
+    x = random_block_np(5, 16, 22)
+    r = impl.baseline_route(x, 4, 0, k_reduced=1)
+    for t in range(5):
+        assert r.experts(t) == [int(np.argmax(x[t]))] and r.gates(t) == [1.0]
+
+
+def random_block_np(n, m, seed):
+    return np.random.default_rng(seed).normal(size=(n, m))
+
+
+@pytest.mark.parametrize("method,kw,msg", [
+    (0, dict(k_reduced=5), "k_reduced outside [1, top_k]"),
+    (0, dict(k_reduced=0), "k_reduced outside [1, top_k]"),
+    (1, dict(naee_beta=0.0), "naee beta outside (0, 1)"),
+    (1, dict(naee_beta=1.0), "naee beta outside (0, 1)"),
+    (2, dict(mcmoe_beta=1.0), "mcmoe beta outside (0, 1)"),
+    (2, dict(fraction=-0.1), "important_fraction outside [0, 1]"),
+    (2, dict(fraction=1.1), "important_fraction outside [0, 1]"),
+])
+def test_baselines_validate(impl, method, kw, msg):
+    with pytest.raises(ValueError, match=msg.replace("(", r"\(").replace(")", r"\)")
+                       .replace("[", r"\[").replace("]", r"\]")):
+        impl.baseline_route(random_block_np(2, 8, 23), 4, method, **kw)
+
+
+def test_port_baselines_bit_identical_to_reference(ref, port):
+    rng = np.random.default_rng(90210)
+    for _ in range(200):
+        n, m = int(rng.integers(1, 48)), int(rng.integers(2, 160))
+        k = int(rng.integers(1, min(m, 16) + 1))
+        x = rng.normal(size=(n, m)) * rng.uniform(0.3, 4.0)
+        act, method = int(rng.integers(0, 2)), int(rng.integers(0, 3))
+        kw = dict(k_reduced=int(rng.integers(1, k + 1)), naee_beta=float(rng.uniform(0.02, 0.98)),
+                  mcmoe_beta=float(rng.uniform(0.02, 0.98)), fraction=float(rng.uniform(0, 1)),
+                  score=int(rng.integers(0, 2)))
+        a = ref.baseline_route(x, k, method, act, **kw)
+        b = port.baseline_route(x, k, method, act, **kw)
+        assert np.array_equal(a.idx, b.idx) and np.array_equal(a.cnt, b.cnt)
+        assert np.array_equal(a.gate, b.gate)
+
+
+def test_baselines_golden_fixtures(port):
+    g = np.load(os.path.join(GOLDEN, "baselines_golden.npz"))
+    for i in range(int(g["count"])):
+        x, k, act = g[f"x{i}"], int(g[f"k{i}"]), int(g[f"act{i}"])
+        for j, (meth, kr, nb, mb, fr, sc) in enumerate(g["params"]):
+            r = port.baseline_route(x, k, int(meth), act, k_reduced=min(int(kr), k),
+                                    naee_beta=nb, mcmoe_beta=mb, fraction=fr, score=int(sc))
+            assert np.array_equal(r.idx, g[f"idx{i}_{j}"]) and np.array_equal(r.cnt, g[f"cnt{i}_{j}"])
+            assert np.array_equal(r.gate, g[f"gate{i}_{j}"])
