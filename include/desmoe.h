@@ -157,6 +157,42 @@ int desmoe_baseline_route_f32(desmoe_ctx* ctx, const float* logits_dev, int n,
                               const desmoe_route_cfg* cfg, const desmoe_baseline_cfg* params,
                               const desmoe_route_out* out, void* stream);
 
+/* ---- MOET router traces (trace.hpp:30-85, trace.cpp:122-442) ----------------
+ * The reference's trace file format, so captured router traces feed the
+ * routing entry points in logits-in mode. Binary v1: "MOET", u16 version,
+ * u8 model, u8 reserved, u32 experts/top_k/layers/block_size/steps, u64 seed,
+ * f32 rho/temperature, then per (step, layer) record u32 step, u32 layer and
+ * block_size x experts f32 logits, little-endian. JSONL: a header object line
+ * and one {"layer","logits","step"} line per record. Host-only (no GPU). */
+#define DESMOE_MOET_BINARY 0
+#define DESMOE_MOET_JSONL 1
+/* TraceError::Code (trace.hpp:58-66) */
+#define DESMOE_MOET_IO 0
+#define DESMOE_MOET_BAD_MAGIC 1
+#define DESMOE_MOET_BAD_VERSION 2
+#define DESMOE_MOET_BAD_HEADER 3
+#define DESMOE_MOET_TRUNCATED 4
+#define DESMOE_MOET_SHAPE_MISMATCH 5
+#define DESMOE_MOET_BAD_VALUE 6
+
+typedef struct { /* TraceHeader (trace.hpp:30-40) */
+  int experts, top_k, layers, block_size, steps;
+  int model; /* SynthModel: 0 iid_gaussian, 1 dirichlet, 2 shared_bias */
+  double rho, temperature;
+  uint64_t seed;
+} desmoe_moet_header;
+
+/* decode_trace (trace.cpp:432-441; format sniffed from the first byte).
+ * `logits` (may be NULL: validate and read the header only) receives
+ * steps*layers*block_size*experts doubles in (step, layer) record order.
+ * Errors: DESMOE_EINVAL, the reference's message in desmoe_last_error() and
+ * the TraceError code in *trace_code. */
+int desmoe_moet_decode(const void* bytes, size_t len, desmoe_moet_header* header,
+                       double* logits, int* trace_code);
+/* encode_trace (trace.cpp:422-430): out == NULL -> *len = bytes needed. */
+int desmoe_moet_encode(const desmoe_moet_header* header, const double* logits, int format,
+                       void* out, size_t* len, int* trace_code);
+
 /* Stage 1 only: des_seq_coreset (des.cpp:33-45) / des_vote_coreset
  * (des.cpp:65-95, also the contract of fused_vote_pipeline des.cpp:166-224).
  * cfg->strategy selects which; out->coreset_dev / coreset_size_dev required. */

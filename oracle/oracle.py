@@ -52,6 +52,15 @@ def _i32(a):
     return np.ascontiguousarray(a, dtype=np.int32)
 
 
+class TraceDecodeError(Exception):
+    """A MOET decode failure: TraceError::Code (trace.hpp:58-66) + message."""
+
+    def __init__(self, code, message):
+        super().__init__(message)
+        self.code = code
+        self.message = message
+
+
 class _Base:
     prefix = ""
 
@@ -220,6 +229,38 @@ class Ref(_Base):
                                            C.c_int, C.c_int, C.c_int, C.c_ulonglong, _f64p])(
             m, k, mid, rho, tau, layers, steps, n, seed, out))
         return out
+
+    def trace_bytes(self, m, k, n, seed, rho=0.0, tau=1.0, model="shared_bias", layers=1,
+                    steps=1, fmt="binary"):
+        """gen_trace + encode_trace: the reference's own MOET bytes."""
+        mid = {"iid_gaussian": 0, "dirichlet": 1, "shared_bias": 2}[model]
+        f = self._fn("trace_bytes", [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                     C.c_int, C.c_int, C.c_ulonglong, C.c_int, C.c_char_p,
+                                     C.POINTER(C.c_size_t)])
+        n_ = C.c_size_t(0)
+        args = (m, k, mid, rho, tau, layers, steps, n, seed, 0 if fmt == "binary" else 1)
+        self._check(f(*args, None, C.byref(n_)))
+        buf = C.create_string_buffer(n_.value)
+        self._check(f(*args, buf, C.byref(n_)))
+        return buf.raw[: n_.value]
+
+    def trace_decode(self, data: bytes):
+        """decode_trace -> (header dict, logits [blocks, n, m]) or raises
+        TraceDecodeError(code, message)."""
+        hdr = (C.c_int * 6)()
+        hd = (C.c_double * 2)()
+        seed = C.c_ulonglong()
+        code = C.c_int()
+        f = self._fn("trace_decode", [C.c_char_p, C.c_size_t, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_ulonglong), C.c_void_p])
+        if f(data, len(data), C.byref(code), hdr, hd, C.byref(seed), None):
+            raise TraceDecodeError(code.value, self._err().decode())
+        m, k, layers, n, steps, model = list(hdr)
+        x = np.empty((steps * layers, n, m), np.float64)
+        f(data, len(data), C.byref(code), hdr, hd, C.byref(seed), x.ctypes.data)
+        return dict(experts=m, top_k=k, layers=layers, block_size=n, steps=steps, model=model,
+                    rho=hd[0], temperature=hd[1], seed=seed.value), x
 
     def rng_u64(self, seed, count):
         out = np.empty(count, np.uint64)

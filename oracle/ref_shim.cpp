@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <string_view>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -206,6 +207,57 @@ int dsref_baseline_route(const double* logits, int n, int m, int k, int act, int
     bp.mcmoe_score = score == 1 ? ImportanceScore::neg_entropy : ImportanceScore::max_gate;
     flatten(baseline_route(block_of(logits, n, m), pool(m, k, act), bp), k, idx, gates, counts);
   });
+}
+
+// gen_trace + encode_trace (format 0 binary, 1 jsonl): the reference's own
+// bytes; out == NULL -> *len = size
+int dsref_trace_bytes(int m, int k, int model, double rho, double tau, int layers, int steps,
+                      int n, unsigned long long seed, int format, char* out, size_t* len) {
+  return guarded([&] {
+    SynthParams p;
+    p.model = model == 0 ? SynthModel::iid_gaussian
+                         : (model == 1 ? SynthModel::dirichlet : SynthModel::shared_bias);
+    p.rho = rho;
+    p.temperature = tau;
+    TraceFile f = gen_trace(pool(m, k, 0), p, layers, steps, n, seed);
+    std::string b = encode_trace(f, format == 0 ? TraceFormat::binary : TraceFormat::jsonl);
+    if (out) std::memcpy(out, b.data(), std::min(*len, b.size()));
+    *len = b.size();
+  });
+}
+
+// decode_trace: 0 ok (header ints {experts, top_k, layers, block_size, steps,
+// model}, doubles {rho, temperature}, seed, logits if non-NULL), else 1 with
+// *code = TraceError::Code (or -1 for another exception) and the message
+int dsref_trace_decode(const char* bytes, size_t len, int* code, int* hdr, double* hdr_d,
+                       unsigned long long* seed, double* logits) {
+  *code = -1;
+  try {
+    TraceFile f = decode_trace(std::string_view(bytes, len));
+    const TraceHeader& h = f.header;
+    const int v[6] = {h.experts, h.top_k, h.layers, h.block_size, h.steps,
+                      static_cast<int>(h.model)};
+    std::memcpy(hdr, v, sizeof v);
+    hdr_d[0] = h.rho;
+    hdr_d[1] = h.temperature;
+    *seed = h.seed;
+    if (logits) {
+      std::size_t o = 0;
+      for (const RouterBlock& b : f.blocks) {
+        std::memcpy(logits + o, b.logits.data(), sizeof(double) * b.logits.size());
+        o += b.logits.size();
+      }
+    }
+    g_err.clear();
+    return 0;
+  } catch (const TraceError& e) {
+    *code = static_cast<int>(e.code);
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 int dsref_make_expert_bank(int m, int k, int dim, int n, unsigned long long seed,

@@ -43,6 +43,14 @@ class BaselineCfg(C.Structure):  # desmoe_baseline_cfg = BaselineParams (baselin
 BASE_TOPK_REDUCE, BASE_NAEE, BASE_MCMOE = 0, 1, 2
 SCORE_MAX_GATE, SCORE_NEG_ENTROPY = 0, 1
 
+class MoetHeader(C.Structure):  # desmoe_moet_header = TraceHeader (trace.hpp:29-39)
+    _fields_ = [("experts", C.c_int), ("top_k", C.c_int), ("layers", C.c_int),
+                ("block_size", C.c_int), ("steps", C.c_int), ("model", C.c_int),
+                ("rho", C.c_double), ("temperature", C.c_double), ("seed", C.c_uint64)]
+
+
+MOET_BINARY, MOET_JSONL = 0, 1
+
 # name -> (restype, argtypes)
 _P, _I, _D = C.c_void_p, C.c_int, C.c_double
 _SIGS = {
@@ -60,6 +68,10 @@ _SIGS = {
     "desmoe_activate": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "desmoe_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
     "desmoe_route_f32": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(RouteOut), _P]),
+    "desmoe_moet_decode": (_I, [_P, C.c_size_t, C.POINTER(MoetHeader), _P,
+                                C.POINTER(C.c_int)]),
+    "desmoe_moet_encode": (_I, [C.POINTER(MoetHeader), _P, _I, _P, C.POINTER(C.c_size_t),
+                                C.POINTER(C.c_int)]),
     "desmoe_baseline_route": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(BaselineCfg),
                                    C.POINTER(RouteOut), _P]),
     "desmoe_baseline_route_f32": (_I, [_P, _P, _I, C.POINTER(RouteCfg), C.POINTER(BaselineCfg),

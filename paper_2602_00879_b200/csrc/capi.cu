@@ -199,6 +199,10 @@ struct desmoe_experts {
   void* packed_b = nullptr;         // W_d / W_lin tiles
 };
 
+namespace desmoe {
+int set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace desmoe
+
 extern "C" {
 
 const char* desmoe_last_error(void) { return g_err.c_str(); }

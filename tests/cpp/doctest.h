@@ -1,9 +1,11 @@
 // TEST INFRASTRUCTURE ONLY — a minimal stand-in for the doctest single header
 // (absent from this image) covering exactly the macros the
 // reference's unit tests use: TEST_SUITE, TEST_CASE, CHECK, CHECK_FALSE,
-// REQUIRE, CHECK_THROWS_AS, CHECK_THROWS_WITH_AS, CHECK_NOTHROW, MESSAGE,
-// doctest::Approx. It lets /root/reference/proj/tests/test_{gating,des}.cpp
-// compile UNCHANGED against this repo's C++ facade (include/dessim/*.hpp).
+// REQUIRE, CHECK_THROWS_AS, CHECK_THROWS_WITH_AS, CHECK_NOTHROW, MESSAGE, FAIL,
+// SUBCASE (flat, one leaf per pass of the test case, as doctest runs them) and
+// doctest::Approx. It lets /root/reference/proj/tests/test_{gating,des,
+// baselines,trace}.cpp compile UNCHANGED against this repo's C++ facade
+// (include/dessim/*.hpp).
 // Define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN in exactly one translation unit.
 #pragma once
 
@@ -38,6 +40,7 @@ struct Registrar {
 struct State {
   long asserts = 0, failed_asserts = 0;
   bool current_failed = false;
+  int sub_target = 0, sub_seen = 0;  // SUBCASE: the leaf this pass runs / leaves met
 };
 
 inline State& state() {
@@ -46,6 +49,12 @@ inline State& state() {
 }
 
 struct RequireFailed {};
+
+// true for exactly one SUBCASE per pass of the enclosing test case
+inline bool enter_subcase() {
+  State& s = state();
+  return s.sub_seen++ == s.sub_target;
+}
 
 inline void report(bool ok, const char* kind, const char* expr, const char* file, int line,
                    const std::string& extra = std::string()) {
@@ -87,15 +96,19 @@ inline int run_all() {
   int failed = 0, passed = 0;
   for (const TestCase& tc : registry()) {
     state().current_failed = false;
-    try {
-      tc.fn();
-    } catch (const RequireFailed&) {
-    } catch (const std::exception& e) {
-      report(false, "TEST_CASE", tc.name, tc.file, tc.line,
-             std::string("threw exception: ") + e.what());
-    } catch (...) {
-      report(false, "TEST_CASE", tc.name, tc.file, tc.line, "threw unknown exception");
-    }
+    state().sub_target = 0;
+    do {  // one pass per SUBCASE leaf (a single pass without subcases)
+      state().sub_seen = 0;
+      try {
+        tc.fn();
+      } catch (const RequireFailed&) {
+      } catch (const std::exception& e) {
+        report(false, "TEST_CASE", tc.name, tc.file, tc.line,
+               std::string("threw exception: ") + e.what());
+      } catch (...) {
+        report(false, "TEST_CASE", tc.name, tc.file, tc.line, "threw unknown exception");
+      }
+    } while (++state().sub_target < state().sub_seen);
     if (state().current_failed) {
       ++failed;
       std::fprintf(stderr, "[doctest] FAILED: %s (%s:%d)\n", tc.name, tc.file, tc.line);
@@ -123,6 +136,12 @@ inline int run_all() {
   DOCTEST_TEST_CASE_IMPL(DOCTEST_CAT(doctest_case_, __LINE__),                    \
                          DOCTEST_CAT(doctest_reg_, __LINE__), name)
 #define TEST_SUITE(name) namespace DOCTEST_CAT(doctest_suite_, __LINE__)
+#define SUBCASE(name) if (::doctest::enter_subcase())
+#define FAIL(msg)                                                            \
+  do {                                                                       \
+    ::doctest::report(false, "FAIL", msg, __FILE__, __LINE__);               \
+    throw ::doctest::RequireFailed();                                        \
+  } while (0)
 
 #define CHECK(...) ::doctest::report(static_cast<bool>(__VA_ARGS__), "CHECK", #__VA_ARGS__, __FILE__, __LINE__)
 #define CHECK_FALSE(...) ::doctest::report(!static_cast<bool>(__VA_ARGS__), "CHECK_FALSE", #__VA_ARGS__, __FILE__, __LINE__)

@@ -1,10 +1,11 @@
 """The reference's OWN unit tests (/root/reference/proj/tests/test_gating.cpp,
-test_des.cpp and test_baselines.cpp, compiled unchanged by tests/cpp/Makefile)
+test_des.cpp, test_baselines.cpp and test_trace.cpp, compiled unchanged by
+tests/cpp/Makefile)
 run against the C++ facade include/dessim/*.hpp -> libdessim_gpu.so ->
 libdesmoe.so.
 
 * CPU: the doctest stand-in runs the same suites against the reference library
-  itself (oracle/_ref) with 60/60 passing, the facade exports the reference's
+  itself (oracle/_ref) with 72/72 passing, the facade exports the reference's
   dessim:: symbols, and without a GPU the facade fails loudly (no CPU path).
 * GPU: every reference test case passes on the B200 path.
 """
@@ -29,7 +30,7 @@ def _run(path):
 def test_doctest_standin_runs_reference_suites_on_reference():
     r = _run(ON_REF)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "| 60 passed | 0 failed" in r.stdout, r.stdout
+    assert "| 72 passed | 0 failed" in r.stdout, r.stdout
 
 
 def test_facade_exports_reference_api():
@@ -42,7 +43,9 @@ def test_facade_exports_reference_api():
                 "dessim::constrained_route(", "dessim::des_run(", "dessim::fused_vote_pipeline(",
                 "dessim::validate_config(", "dessim::make_router_block(", "dessim::Rng::next_normal(",
                 "dessim::Coreset::of(", "dessim::topk_reduce_route(", "dessim::naee_route(",
-                "dessim::mcmoe_route(", "dessim::baseline_route("]:
+                "dessim::mcmoe_route(", "dessim::baseline_route(", "dessim::gen_trace(",
+                "dessim::encode_trace(", "dessim::decode_trace(", "dessim::read_trace(",
+                "dessim::write_trace("]:
         assert sym in out, sym
 
 
