@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "dessim/analysis.hpp"
 #include "dessim/baselines.hpp"
 #include "../../include/desmoe.h"
 #include "dessim/core.hpp"
@@ -700,5 +701,77 @@ RoutingAssignment baseline_route(const RouterBlock& block, const PoolConfig& cfg
   throw std::invalid_argument("unknown baseline method");
 }
 
+// ===========================================================================
+// analysis.hpp
+// ===========================================================================
+
+TrafficReport moe_latency(const RoutingAssignment& assign, const PoolConfig& cfg,
+                          const LatencyParams& params) {
+  const int m = cfg.experts_total;
+  const int n = assign.block_size();
+  int kmax = 0, total_b = 0;
+  for (const TokenRoute& tok : assign.tokens) {
+    for (int e : tok.experts)  // analysis.cpp:18-22
+      if (e < 0 || e >= m) throw std::invalid_argument("expert index out of range");
+    kmax = std::max(kmax, static_cast<int>(tok.experts.size()));
+    total_b += static_cast<int>(tok.experts.size());
+  }
+  TrafficReport r;
+  r.per_expert_counts.assign(m, 0);
+  if (n >= 1 && kmax >= 1) {
+    // route A: per-expert counts from the permutation kernel (the FFN's count route)
+    Gpu& g = gpu(n, m, kmax);
+    std::vector<int> idx(static_cast<size_t>(n) * kmax, -1), cnt(n, 0);
+    for (int t = 0; t < n; ++t) {
+      const auto& ex = assign.tokens[t].experts;
+      cnt[t] = static_cast<int>(ex.size());
+      std::copy(ex.begin(), ex.end(), idx.begin() + static_cast<size_t>(t) * kmax);
+    }
+    const int* di = g.upload(0, idx.data(), idx.size());
+    const int* dc = g.upload(1, cnt.data(), cnt.size());
+    int* count = g.s[2].get<int>(m);
+    int* offset = g.s[3].get<int>(m);
+    int* active = g.s[4].get<int>(m);
+    int* n_active = g.s[5].get<int>(1);
+    ok(desmoe_permute(g.ctx, di, dc, n, kmax, m, count, offset, nullptr, nullptr, active,
+                      n_active, g.st()));
+    r.per_expert_counts = g.download(count, m);
+  }
+  int unique_a = 0, total_a = 0;
+  for (int c : r.per_expert_counts) {
+    unique_a += c > 0;
+    total_a += c;
+  }
+  // route B: union of the selections (analysis.cpp:32-41)
+  const Coreset uni = unique_experts(assign);
+  if (unique_a != uni.size() || total_a != total_b)
+    throw std::logic_error("latency model forms disagree");
+  r.unique_experts = unique_a;
+  r.total_selections = total_a;
+  r.latency = params.fetch_per_expert * unique_a + params.compute_per_token * total_a;
+  r.memory_bytes = memory_footprint(unique_a, cfg.bytes_per_expert);
+  return r;
+}
+
+double coreset_latency_bound(const Coreset& coreset, int block_size, int top_k,
+                             const LatencyParams& params) {
+  return params.fetch_per_expert * coreset.size() +
+         params.compute_per_token * (static_cast<double>(block_size) * top_k);
+}
+
+double expected_unique_experts(int experts_total, int top_k, int block_size) {
+  if (top_k < 1 || top_k > experts_total)
+    throw std::invalid_argument("top_k outside [1, experts_total]");
+  if (block_size < 1) throw std::invalid_argument("block_size < 1");
+  const double m = static_cast<double>(experts_total);
+  return m * (1.0 - std::pow(1.0 - static_cast<double>(top_k) / m,
+                             static_cast<double>(block_size)));
+}
+
+std::uint64_t memory_footprint(int unique_experts, std::uint64_t bytes_per_expert) {
+  return static_cast<std::uint64_t>(unique_experts) * bytes_per_expert;
+}
+
 }  // namespace dessim
+
 

@@ -1,11 +1,12 @@
 """The reference's OWN unit tests (/root/reference/proj/tests/test_gating.cpp,
-test_des.cpp, test_baselines.cpp and test_trace.cpp, compiled unchanged by
-tests/cpp/Makefile)
+test_des.cpp, test_baselines.cpp, test_trace.cpp and test_analysis.cpp,
+compiled unchanged by tests/cpp/Makefile; test_analysis.cpp's one Monte-Carlo
+oracle comes from the test-only stub tests/cpp/stub/dessim/oracle.hpp)
 run against the C++ facade include/dessim/*.hpp -> libdessim_gpu.so ->
 libdesmoe.so.
 
 * CPU: the doctest stand-in runs the same suites against the reference library
-  itself (oracle/_ref) with 72/72 passing, the facade exports the reference's
+  itself (oracle/_ref) with 85/85 passing, the facade exports the reference's
   dessim:: symbols, and without a GPU the facade fails loudly (no CPU path).
 * GPU: every reference test case passes on the B200 path.
 """
@@ -30,7 +31,7 @@ def _run(path):
 def test_doctest_standin_runs_reference_suites_on_reference():
     r = _run(ON_REF)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "| 72 passed | 0 failed" in r.stdout, r.stdout
+    assert "| 85 passed | 0 failed" in r.stdout, r.stdout
 
 
 def test_facade_exports_reference_api():
@@ -45,7 +46,8 @@ def test_facade_exports_reference_api():
                 "dessim::Coreset::of(", "dessim::topk_reduce_route(", "dessim::naee_route(",
                 "dessim::mcmoe_route(", "dessim::baseline_route(", "dessim::gen_trace(",
                 "dessim::encode_trace(", "dessim::decode_trace(", "dessim::read_trace(",
-                "dessim::write_trace("]:
+                "dessim::write_trace(", "dessim::moe_latency(", "dessim::coreset_latency_bound(",
+                "dessim::expected_unique_experts(", "dessim::memory_footprint("]:
         assert sym in out, sym
 
 
