@@ -993,6 +993,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.zero_words = words;
   ca.route_idx = route_idx;
   ca.route_gate = route_gate;
+  ca.route_words = ex->route_words;
   ca.pub = ex->pub;
   ca.m = m;
   ca.expert_lo = ex->lo;
@@ -1021,7 +1022,6 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
     c->launches += 1;
   }
   if (dense) {
-    cc.dynamicSmemBytes = static_cast<size_t>(m) * sizeof(int);
     DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_dense_kernel, ca));
   } else {
     DESMOE_CUDA(cudaLaunchKernelEx(&cc, combine_slots_kernel, ca));

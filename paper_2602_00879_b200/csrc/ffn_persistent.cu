@@ -626,6 +626,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++nunit;
     }
+  } else if (warp == 2) {
+    // ============ (idle after the TMEM allocation) ============
+    if (dense && blockIdx.x == 0 && a.stats) {
+      // the route stats (unique experts of the route, analysis.cpp:16-30, and
+      // the selections) off the combine's critical path; t.count is unused in
+      // dense mode and marks the experts seen
+      int* seen = t.count;
+      for (int i = lane; i < m; i += 32) seen[i] = 0;
+      __syncwarp();
+      int sel = 0;
+      for (int o = lane; o < n_tok * k; o += 32) {
+        uint64_t w;
+        do {
+          w = ld_relaxed_u64(a.route_words + o);
+        } while (((static_cast<uint32_t>(w) >> 10) & kTagMask) != tag);
+        const int x = static_cast<int>(w & 1023u);
+        if (x != kPadExpert) {
+          ++sel;
+          seen[x] = 1;
+        }
+      }
+      __syncwarp();
+      int u = 0;
+      for (int i = lane; i < m; i += 32) u += seen[i];
+      u = __reduce_add_sync(0xffffffffu, u);
+      sel = __reduce_add_sync(0xffffffffu, sel);
+      if (lane == 0) {
+        a.stats[0] = u;
+        a.stats[2] = sel;
+      }
+    }
   } else if (warp >= 4) {
     // ============ epilogue ============
     const int q4 = warp & 3;
@@ -831,77 +862,87 @@ __device__ inline void store_row4(const CombineArgs& a, size_t off, float4 v) {
 // fp32 products and sums as the routed path. CTA 0 also writes the block's
 // stats (unique experts of the route, published list length, selections,
 // experts this rank streamed).
+// Ordered combine of 4 columns [c, c+4) of token tok over 8 route entries
+// (moe_forward's order, gating.cpp:141-155): ascending slot order (=
+// ascending expert), dense rows [expert][token], y += gate * row as a product
+// then an add (no contraction) — the routed path's epilogue product followed
+// by its combine add. All 8 rows are in flight at once.
+__device__ __forceinline__ float4 combine4_rows(const float* ys, const int* e, const float* g,
+                                                int n, int d, int tok, int c, float4 acc) {
+  float4 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (e[j] >= 0)
+      v[j] = __ldcg(
+          reinterpret_cast<const float4*>(ys + (static_cast<size_t>(e[j]) * n + tok) * d + c));
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (e[j] >= 0) {
+      acc.x = __fadd_rn(acc.x, __fmul_rn(v[j].x, g[j]));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(v[j].y, g[j]));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(v[j].z, g[j]));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(v[j].w, g[j]));
+    }
+  return acc;
+}
+
 __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 80, -1);
+  // before the FFN grid completes: the call's tag and this thread's route
+  // (the front's tagged words; the previous call's sequence bump completed
+  // before this call's front started), so after the wait only the rows'
+  // round trip remains. The FFN computed the route stats.
   __shared__ int s_epoch;
   const int tid = threadIdx.x;
   if (tid == 0) s_epoch = *a.epoch;
   __syncthreads();
-  const float* y_slot = a.y_slot;
-  if (a.world > 1) y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
+  const uint32_t tag = hand_tag(s_epoch);
   const int vec = a.d / 4;
   const int i = blockIdx.x * blockDim.x + tid;
-  if (i < a.n * vec) {
-    const int tok = i / vec, c = (i - tok * vec) * 4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    // 8 route entries (ascending experts, -1 padded) and their 8 rows in
-    // flight at once: two memory round trips instead of 2 per expert
-    for (int j0 = 0; j0 < a.k; j0 += 8) {
-      int e[8];
-      float g[8];
+  const bool mine = i < a.n * vec;
+  const int tok = mine ? i / vec : 0, c = mine ? (i - tok * vec) * 4 : 0;
+  constexpr int kMaxK = 32;
+  int e[kMaxK];
+  float g[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) {
+    e[j] = -1;
+    g[j] = 0.f;
+  }
+  if (mine) {
+#pragma unroll
+    for (int j0 = 0; j0 < kMaxK; j0 += 8) {
+      if (j0 >= a.k) break;
+      uint64_t w[8];
+      bool ok;
+      do {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          w[j] = j0 + j < a.k ? ld_relaxed_u64(a.route_words + static_cast<size_t>(tok) * a.k + j0 + j)
+                              : route_word(tag, kPadExpert, 0.f);
+        ok = true;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ok &= ((static_cast<uint32_t>(w[j]) >> 10) & kTagMask) == tag;
+      } while (!ok);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const size_t o = static_cast<size_t>(tok) * a.k + j0 + j;
-        e[j] = j0 + j < a.k ? a.route_idx[o] : -1;
-        g[j] = j0 + j < a.k ? static_cast<float>(a.route_gate[o]) : 0.f;
+        const int x = static_cast<int>(w[j] & 1023u);
+        e[j0 + j] = x == kPadExpert ? -1 : x;
+        g[j0 + j] = __uint_as_float(static_cast<uint32_t>(w[j] >> 32));
       }
-      float4 v[8];
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (blockIdx.x == 0 && tid == 0) trace(a.trace, a.trace_cap, 80, -1);
+  const float* y_slot = a.y_slot;
+  if (a.world > 1) y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
+  if (mine) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (e[j] >= 0)
-          v[j] = __ldcg(reinterpret_cast<const float4*>(
-              y_slot + (static_cast<size_t>(e[j]) * a.n + tok) * a.d + c));
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (e[j] >= 0) {
-          // product then add (no contraction): the routed path's epilogue
-          // product followed by the combine's add
-          acc.x = __fadd_rn(acc.x, __fmul_rn(v[j].x, g[j]));
-          acc.y = __fadd_rn(acc.y, __fmul_rn(v[j].y, g[j]));
-          acc.z = __fadd_rn(acc.z, __fmul_rn(v[j].z, g[j]));
-          acc.w = __fadd_rn(acc.w, __fmul_rn(v[j].w, g[j]));
-        }
+    for (int j0 = 0; j0 < kMaxK; j0 += 8) {
+      if (j0 >= a.k) break;
+      acc = combine4_rows(y_slot, e + j0, g + j0, a.n, a.d, tok, c, acc);
     }
     store_row4(a, static_cast<size_t>(tok) * a.d + c, acc);
-  }
-  if (blockIdx.x == 0 && a.stats) {
-    // unique experts of the route (moe_latency's count route,
-    // analysis.cpp:16-30) and the selections; the FFN wrote stats[1], [3]
-    extern __shared__ int seen[];  // [m]
-    __syncthreads();
-    for (int e = tid; e < a.m; e += blockDim.x) seen[e] = 0;
-    __syncthreads();
-    int sel = 0;
-    for (int o = tid; o < a.n * a.k; o += blockDim.x) {
-      const int e = a.route_idx[o];
-      if (e >= 0) {
-        seen[e] = 1;
-        ++sel;
-      }
-    }
-    __shared__ int s_sel, s_u;
-    if (tid == 0) s_sel = s_u = 0;
-    __syncthreads();  // seen[] complete, counters zeroed
-    atomicAdd(&s_sel, sel);
-    int u = 0;
-    for (int e = tid; e < a.m; e += blockDim.x) u += seen[e];
-    atomicAdd(&s_u, u);
-    __syncthreads();
-    if (tid == 0) {
-      a.stats[0] = s_u;
-      a.stats[2] = s_sel;
-    }
   }
   for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;
   __syncthreads();

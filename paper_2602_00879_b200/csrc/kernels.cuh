@@ -245,6 +245,7 @@ struct CombineArgs {
   int* zero;                 // FFN counters, zeroed for the next call
   int zero_words;
   // dense mode (combine_dense_kernel)
+  const uint64_t* route_words;  // [n x k] the front's tagged route (read before the FFN ends)
   const int* route_idx;      // [n x k]
   const double* route_gate;  // [n x k]
   const uint32_t* pub;       // published list (tagged words)
