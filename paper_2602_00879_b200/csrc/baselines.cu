@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(1024, 1) baseline_route_kernel(BaselineArgs<T>
   }
   __syncthreads();
   if (s_bad) {
-    if (tid == 0) atomicOr(a.err, 1);
+    if (tid == 0) raise_flag(a.err, 1);
     return;
   }
 

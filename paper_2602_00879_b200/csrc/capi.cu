@@ -140,6 +140,11 @@ struct desmoe_ctx {
   void* x_dev = nullptr;
   float* y_dev = nullptr;
   int* stats_dev = nullptr;
+  // pinned, device-mapped [8]: [0..3] the host entry's stats (written by the
+  // kernels straight into host memory), [4] the data-check word (c->err is
+  // its device address), read by the host after a synchronisation
+  int* host_tail = nullptr;
+  int* host_tail_dev = nullptr;
   // cached router descriptors
   const void* x_map_ptr = nullptr;
   int x_map_n = -1, x_map_d = -1;
@@ -260,7 +265,6 @@ int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
   A(alloc(&c->route_gate, nk));
   A(alloc(&c->route_gate32, nk));
   A(alloc(&c->route_cnt, max_tokens));
-  A(alloc(&c->err, 1));
   A(alloc(&c->expert_count, max_experts));
   A(alloc(&c->expert_offset, max_experts));
   A(alloc(&c->slot_of, nk));
@@ -274,7 +278,14 @@ int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
   A(alloc(reinterpret_cast<__nv_bfloat16**>(&c->x_dev), static_cast<size_t>(max_tokens) * max_hidden));
   A(alloc(&c->y_dev, static_cast<size_t>(max_tokens) * max_hidden));
   A(alloc(&c->stats_dev, 4));
-  if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->host_tail), 8 * sizeof(int), cudaHostAllocMapped);
+  if (e == cudaSuccess)
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->host_tail_dev), c->host_tail, 0);
+  if (e == cudaSuccess) {
+    std::memset(c->host_tail, 0, 8 * sizeof(int));
+    c->err = c->host_tail_dev + 4;
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = desmoe::set_kernel_smem_limits();
   if (e != cudaSuccess) {
@@ -288,12 +299,13 @@ int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
 void desmoe_destroy(desmoe_ctx* c) {
   if (!c) return;
   void* ptrs[] = {c->probs, c->topk_idx, c->members, c->n_members, c->member_flag, c->votes,
-                  c->route_idx, c->route_gate, c->route_gate32, c->route_cnt, c->err,
+                  c->route_idx, c->route_gate, c->route_gate32, c->route_cnt,
                   c->expert_count, c->expert_offset, c->slot_of, c->slot_token, c->slot_gate,
                   c->active, c->n_active, c->total, c->logits32, c->partials, c->x_dev,
                   c->y_dev, c->stats_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (c->host_tail) cudaFreeHost(c->host_tail);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -307,10 +319,11 @@ void desmoe_destroy(desmoe_ctx* c) {
 int desmoe_check(desmoe_ctx* c, void* stream) {
   if (!c) return fail(DESMOE_EINVAL, "null context");
   DESMOE_CUDA(cudaStreamSynchronize(S(stream)));
-  int flag = 0;
-  DESMOE_CUDA(cudaMemcpy(&flag, c->err, sizeof(int), cudaMemcpyDeviceToHost));
+  // the flag word is host memory the kernels write through the mapping
+  volatile int* fw = c->host_tail + 4;
+  const int flag = *fw;
   if (flag) {
-    DESMOE_CUDA(cudaMemset(c->err, 0, sizeof(int)));
+    *fw = 0;
     if (flag == 2)
       return fail(DESMOE_ECUDA, "expert-parallel exchange timed out (a peer rank stopped)");
     return fail(DESMOE_EINVAL, "non-finite logit");
@@ -1175,6 +1188,7 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.err = c->err;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
+  if (const char* ff = std::getenv("DESMOE_FRONT_FLAGS")) a.flags = std::atoi(ff);
   cudaError_t e = launch_front(c->wr_map, c->x_maps, a, smem, st);
   if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("front kernel: ") + cudaGetErrorString(e));
   c->launches += 1;
@@ -1355,14 +1369,22 @@ int desmoe_layer_forward_host(desmoe_ctx* c, const desmoe_experts* ex, const voi
   cudaStream_t st = S(stream);
   const size_t xb = static_cast<size_t>(n) * ex->d * 2, yb = static_cast<size_t>(n) * ex->d * 4;
   DESMOE_CUDA(cudaMemcpyAsync(c->x_dev, x_host, xb, cudaMemcpyHostToDevice, st));
-  rc = desmoe_layer_forward(c, ex, w_r, c->x_dev, n, cfg, c->y_dev, c->stats_dev, stream);
+  // pinned (device-mapped) y: the combine writes it straight into host memory
+  // over the bus; pageable y: a device copy then one D2H transfer
+  cudaPointerAttributes pa{};
+  float* y_dev = c->y_dev;
+  if (cudaPointerGetAttributes(&pa, y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+      pa.devicePointer)
+    y_dev = static_cast<float*>(pa.devicePointer);
+  else
+    cudaGetLastError();
+  rc = desmoe_layer_forward(c, ex, w_r, c->x_dev, n, cfg, y_dev, c->host_tail_dev, stream);
   if (rc) return rc;
-  DESMOE_CUDA(cudaMemcpyAsync(y_host, c->y_dev, yb, cudaMemcpyDeviceToHost, st));
-  if (stats_host)
-    DESMOE_CUDA(cudaMemcpyAsync(stats_host, c->stats_dev, 4 * sizeof(int),
-                                cudaMemcpyDeviceToHost, st));
-  DESMOE_CUDA(cudaStreamSynchronize(st));
-  return desmoe_check(c, stream);
+  if (y_dev == c->y_dev)
+    DESMOE_CUDA(cudaMemcpyAsync(y_host, c->y_dev, yb, cudaMemcpyDeviceToHost, st));
+  rc = desmoe_check(c, stream);  // one synchronisation; stats and flag are host memory
+  if (stats_host) std::memcpy(stats_host, const_cast<const int*>(c->host_tail), 4 * sizeof(int));
+  return rc;
 }
 
 }  // extern "C"

@@ -442,6 +442,10 @@ __device__ inline uint64_t ld_relaxed_u64(const uint64_t* p) {
   return v;
 }
 
+// Data-check flags (c->err) live in host-mapped pinned memory: a plain
+// (volatile) store, no atomics (PCIe may lack native host atomics).
+__device__ inline void raise_flag(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
 __device__ inline uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

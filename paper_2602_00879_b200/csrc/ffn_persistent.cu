@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned long long i0 = atomicAdd(cur, 5ull);
     for (int i = 0; i < 5; ++i)
       if (i0 + i < static_cast<unsigned long long>(a.trace_cap)) {
-        a.trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (70 + i);
+        a.trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (90 + i);
         a.trace[3 + 2 * (i0 + i)] = s_pts[i];
       }
   }
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(32) ep_wait_kernel(CombineArgs a) {
     const uint64_t t0 = gtime();
     while (ld_acquire_sys(a.flag) < want) {
       if (gtime() - t0 > 4000000000ull) {  // 4 s: a peer is gone; fail, never hang
-        atomicExch(a.err, 2);
+        raise_flag(a.err, 2);
         break;
       }
       __nanosleep(100);

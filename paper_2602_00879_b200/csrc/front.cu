@@ -501,6 +501,20 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   cluster_arrive_relaxed();
   cluster_wait();
   FRONT_MARK(1);
+  if (!(a.flags & 1) && warp >= 8) {
+    // instruction-cache prewarm: the layer's FFN streams hundreds of MB
+    // between two calls, so this kernel's code comes back from far memory and
+    // every new code region costs a miss chain (~2 µs measured at the top-K
+    // entry). Idle warps run the selection / exp / division code once on
+    // scratch while the router GEMM runs (DESMOE_FRONT_FLAGS=1 disables)
+    const float* dx = reinterpret_cast<const float*>(erow);
+    int* ds = wsel_all + warp * 33;
+    warp_rank_select(dx, m, k < m ? k + 1 : k, nullptr, ds);
+    if (lane == 0) {
+      volatile double sink = f_exp(dx[0] * 0.0) + f_div(1.0, 2.0);
+      (void)sink;
+    }
+  }
 
   // ---- R + L1: per token chunk, split-K GEMM, then the owners' logit sums ----------
   int own = 0;
@@ -706,7 +720,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   }
   __syncthreads();
   FRONT_MARK(7);
-  if (s_bad && tid == 0) atomicOr(a.err, 1);
+  if (s_bad && tid == 0) raise_flag(a.err, 1);
   // ---- L5: exact fallback for near-ties; vote weights / vanilla routes ---------------
   {
     const int want = k < m ? k : m;

@@ -78,6 +78,7 @@ struct FrontArgs {
   const int* seq;          // [1] bumped by the combine kernel after every call
   uint32_t* pub;           // [1 + m] {tag | count}, {tag | expert} ...
   uint64_t* route_words;   // [n x k] {gate f32 | tag | expert}, expert kPadExpert = none
+  int flags;               // experiments (DESMOE_FRONT_FLAGS)
 };
 
 // Tagged hand-off words (front -> FFN). A word is valid for the current call

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(1024, 1) fused_route_kernel(FusedRouteArgs<T> 
   }
   __syncthreads();
   if (s_bad) {
-    if (tid == 0) atomicOr(a.err, 1);
+    if (tid == 0) raise_flag(a.err, 1);
     return;
   }
   if (vanilla) return;

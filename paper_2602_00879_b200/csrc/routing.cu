@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(GateTopkArgs<T> a) {
     mx = fmax(mx, x);
   }
   if (__any_sync(0xffffffffu, bad)) {
-    if (lane == 0) atomicOr(a.err, 1);
+    if (lane == 0) raise_flag(a.err, 1);
     return;
   }
 #pragma unroll

@@ -104,9 +104,9 @@ def main():
         if (ev == e_).any():
             out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
     for i, nm in enumerate(["pdl_released", "counted", "slotted", "gathered", "x_ready_added"]):
-        if (ev == 70 + i).any():
-            out["ffn_" + nm] = [round(float(t[ev == 70 + i].min()), 2),
-                                round(float(t[ev == 70 + i].max()), 2)]
+        if (ev == 90 + i).any():
+            out["ffn_" + nm] = [round(float(t[ev == 90 + i].min()), 2),
+                                round(float(t[ev == 90 + i].max()), 2)]
     if (ev == 80).any():
         out["combine_start_us"] = round(float(t[ev == 80].max()), 2)
     if (ev == 81).any():
