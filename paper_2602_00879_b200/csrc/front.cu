@@ -282,6 +282,21 @@ __device__ __noinline__ void front_dump_marks(uint64_t* trace, int cap, const ui
     }
 }
 
+// Part `idx / m` of expert (idx mod m)'s rank in (vote desc, index asc): the
+// number of experts before it among indices [j0, j1) of that part.
+__device__ __noinline__ void rank_part(const uint64_t* vkey, int m, int parts, int idx, int* rankp) {
+  const int i = idx % m, part = idx / m;
+  const uint64_t ki = vkey[i];
+  int r = 0;
+  const int j0 = (m * part) / parts, j1 = (m * (part + 1)) / parts;
+#pragma unroll 4
+  for (int j = j0; j < j1; ++j) {
+    const uint64_t kj = vkey[j];
+    r += (kj > ki) | ((kj == ki) & (j < i));
+  }
+  rankp[part * m + i] = r;
+}
+
 // Publishes the ascending list of flagged experts (coreset / union): the
 // tagged words the expert-FFN kernel polls to start streaming weights, plus
 // the C-ABI outputs members / n_members. One warp.
@@ -409,6 +424,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
   __shared__ uint64_t s_ts[40];  // timeline marks (trace buffer only)
+  __shared__ uint64_t s_pw[96];  // instruction-cache prewarm scratch
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool tracing = a.trace != nullptr;
   if (tracing && tid == 0) s_ts[24] = clock64();
@@ -501,18 +517,34 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   cluster_arrive_relaxed();
   cluster_wait();
   FRONT_MARK(1);
-  if (!(a.flags & 1) && warp >= 8) {
+  if (!(a.flags & 1) && warp >= 8 && warp < 12) {
     // instruction-cache prewarm: the layer's FFN streams hundreds of MB
     // between two calls, so this kernel's code comes back from far memory and
     // every new code region costs a miss chain (~2 µs measured at the top-K
-    // entry). Idle warps run the selection / exp / division code once on
-    // scratch while the router GEMM runs (DESMOE_FRONT_FLAGS=1 disables)
-    const float* dx = reinterpret_cast<const float*>(erow);
+    // entry). While the router GEMM runs, four idle warps each run one later
+    // phase's code once on scratch (s_pw; 32 dummy experts), in parallel so
+    // the misses overlap (DESMOE_FRONT_FLAGS=1 disables)
+    uint64_t* dk = s_pw;                                      // [32] keys
+    int* dr = reinterpret_cast<int*>(s_pw + 32);              // [32] ranks / pub words
+    uint8_t* df = reinterpret_cast<uint8_t*>(s_pw + 48);      // [32] flags; pub words at +52
     int* ds = wsel_all + warp * 33;
-    warp_rank_select(dx, m, k < m ? k + 1 : k, nullptr, ds);
-    if (lane == 0) {
-      volatile double sink = f_exp(dx[0] * 0.0) + f_div(1.0, 2.0);
-      (void)sink;
+    if (warp == 8) {
+      warp_rank_select(reinterpret_cast<const float*>(erow), m, k < m ? k + 1 : k, nullptr, ds);
+    } else if (warp == 9) {
+      if (lane == 0) {
+        volatile double sink = f_exp(0.0) + f_div(1.0, 2.0);
+        (void)sink;
+      }
+      dk[lane] = static_cast<uint64_t>(lane);
+      __syncwarp();
+      rank_part(dk, 32, 1, lane, dr);
+    } else if (warp == 10) {
+      df[lane] = static_cast<uint8_t>(lane & 1);
+      __syncwarp();
+      publish_list(df, 32, 0u, reinterpret_cast<uint32_t*>(s_pw + 52), nullptr, nullptr);
+    } else {
+      write_route(erow, 1.0, 2, ds, 0, 0, 0, reinterpret_cast<double*>(s_pw + 64), nullptr,
+                  nullptr, ds, nullptr, 0u);
     }
   }
 
@@ -848,18 +880,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     // rank of expert i = #experts before it in (vote desc, index asc), the
     // pool split into `parts` ranges counted by different threads
     const int parts = kFrontThreads / m < 16 ? kFrontThreads / m : 16;
-    if (tid < parts * m) {
-      const int i = tid % m, part = tid / m;
-      const uint64_t ki = vkey[i];
-      int r = 0;
-      const int j0 = (m * part) / parts, j1 = (m * (part + 1)) / parts;
-#pragma unroll 4
-      for (int j = j0; j < j1; ++j) {
-        const uint64_t kj = vkey[j];
-        r += (kj > ki) | ((kj == ki) & (j < i));
-      }
-      rankp[part * m + i] = r;
-    }
+    if (tid < parts * m) rank_part(vkey, m, parts, tid, rankp);
     __syncthreads();
     FRONT_MARK(16);
     if (tid < m) {
