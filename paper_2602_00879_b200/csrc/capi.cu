@@ -1150,7 +1150,14 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
     return fail(DESMOE_EINVAL, "unknown gate activation");
   FrontArgs a{};
   size_t smem = 0;
-  if (!front_plan(n, m, k, d, &a, &smem)) return DESMOE_OK;
+  // router GEMM shape: split-K over the cluster with a partial-logit exchange
+  // (small blocks: each CTA streams 1/8 of W_r), or token split (large
+  // blocks: no exchange, no token chunking; each CTA streams all of W_r).
+  // Measured crossover (tools/sweep.py): token split wins from N*M = 32768.
+  int tsplit = static_cast<long>(n) * m >= 32768 ? 2 : 0;
+  if (const char* ts = std::getenv("DESMOE_FRONT_TSPLIT")) tsplit = std::atoi(ts);
+  if (!front_plan(n, m, k, d, &a, &smem, tsplit) && !front_plan(n, m, k, d, &a, &smem, 0))
+    return DESMOE_OK;
   if (std::getenv("DESMOE_DEBUG_PLAN"))
     std::fprintf(stderr, "front plan n=%d m=%d: chunk=%d stages=%d b_rows=%d vote_rows=%d smem=%zu\n",
                  n, m, a.chunk, a.stages, a.b_rows, a.vote_rows, smem);

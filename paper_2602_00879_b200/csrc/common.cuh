@@ -231,6 +231,19 @@ __device__ inline void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint6
       : "memory");
 }
 
+// 2-D tile load multicast to the CTAs of `mask` in the cluster: the tile lands
+// at the same shared-memory offset in each and completes the transaction
+// bytes on the mbarrier at `bar`'s offset in each
+__device__ inline void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                      int c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask),
+      "l"(policy)
+      : "memory");
+}
+
 // 3-D tile load (packed weight tiles): coords (c0, c1, c2)
 __device__ inline void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                    int c1, int c2, uint64_t policy) {
@@ -328,6 +341,15 @@ __device__ inline void tc_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+
+// arrive (once) on the mbarrier at `bar`'s offset in every CTA of `mask` when
+// this thread's prior tcgen05 operations complete
+__device__ inline void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
 

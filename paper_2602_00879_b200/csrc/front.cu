@@ -347,7 +347,8 @@ struct FrontSmem {
 __host__ __device__ inline size_t fr_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int chunk, int own_max,
-                                                      int stages, int b_rows, int vote_rows) {
+                                                      int stages, int b_rows, int vote_rows,
+                                                      int tsplit) {
   FrontSmem p{};
   const int mt = (m + kBM - 1) / kBM;
   const size_t ring = static_cast<size_t>(stages) * (mt * kATile + b_rows * 128);
@@ -368,11 +369,12 @@ __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int ch
   // region B: the partial logits pushed to this CTA for its own tokens of the
   // current chunk: [sender][own][m]
   p.partial = fr_align(a_end, 1024);
-  const int ocm = (chunk + kFrontCta - 1) / kFrontCta;
+  // (token split: no partials are exchanged)
+  const int ocm = tsplit ? 0 : (chunk + kFrontCta - 1) / kFrontCta;
   const int m4 = (m + 3) & ~3;
   size_t o = p.partial + fr_align(static_cast<size_t>(kFrontCta) * ocm * m4 * 4, 16);
   p.stage = o;  // this CTA's own partial [chunk][m4], copied out in owner blocks
-  o += fr_align(static_cast<size_t>(chunk) * m4 * 4, 16);
+  o += tsplit ? 0 : fr_align(static_cast<size_t>(chunk) * m4 * 4, 16);
   // every token's selection pushed by its owner: [n][k] ids + weights
   p.allsel = o;
   o += fr_align(static_cast<size_t>(n) * k * 4, 16);
@@ -419,7 +421,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // align to 1024 B by offsetting the shared array itself, so the compiler
   // keeps the shared address space (LDS/STS instead of generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t bars[2 * 4 + 3];  // full[4], empty[4], tdone, recv, selx
+  constexpr int kMaxStages = 12;  // ring stages (the token-split GEMM runs deep rings)
+  __shared__ uint64_t bars[2 * kMaxStages + 3];  // full[], empty[], tdone, recv, selx
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
@@ -439,7 +442,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   const int mt = (m + kBM - 1) / kBM;
   const int Tc = a.chunk, nch = (n + Tc - 1) / Tc;
   const int opc = (Tc * (rk + 1)) / C - (Tc * rk) / C;  // own tokens per full chunk
-  const FrontSmem P = front_smem_plan(n, m, k, Tc, a.own_max, a.stages, a.b_rows, a.vote_rows);
+  const FrontSmem P =
+      front_smem_plan(n, m, k, Tc, a.own_max, a.stages, a.b_rows, a.vote_rows, a.tsplit);
   unsigned char* ring = smem + P.ring;
   double* erow = reinterpret_cast<double*>(smem + P.erow);  // [own][m + 1]
   float* recv = reinterpret_cast<float*>(smem + P.partial);  // [C][ocm][m4]
@@ -456,10 +460,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   uint8_t* risky = flag + m;                                 // [own]
   const int ew = m + 1;                                      // erow row stride
   uint64_t* full = bars;
-  uint64_t* empty = bars + 4;
-  uint64_t* tdone = bars + 8;
-  uint64_t* bar_recv = bars + 9;  // partials pushed to this CTA (one phase per chunk)
-  uint64_t* bar_selx = bars + 10; // every token's selection pushed to this CTA
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* tdone = bars + 2 * kMaxStages;
+  uint64_t* bar_recv = bars + 2 * kMaxStages + 1;  // partials pushed to this CTA (one phase per chunk)
+  uint64_t* bar_selx = bars + 2 * kMaxStages + 2;  // every token's selection pushed to this CTA
   int* allsel = reinterpret_cast<int*>(smem + P.allsel);       // [n][k]
   double* allp = reinterpret_cast<double*>(smem + P.allp);     // [n][k]
   const int ocm = (Tc + C - 1) / C;                            // recv rows per sender
@@ -478,7 +482,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 #pragma unroll 1
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      // token split with multicast W_r: every CTA's MMA frees a slot
+      mbar_init(&empty[s], a.tsplit == 1 ? C : 1);
     }
     mbar_init(tdone, 1);
     mbar_init(bar_recv, 1);
@@ -489,15 +494,27 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     // and (DES) every token's top-`depth` selection
     const int nc0 = n < Tc ? n : Tc;
     const int own0 = (nc0 * (rk + 1)) / C - (nc0 * rk) / C;
-    mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
+    if (!a.tsplit) mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
     if (a.strategy >= 0)
       mbar_arrive_expect_tx(bar_selx,
                             static_cast<uint32_t>(n * depth * (a.strategy == 1 ? 12 : 4)));
     else if (rk == 0 && a.pub)
       mbar_arrive_expect_tx(bar_selx, static_cast<uint32_t>(n * k * 4));  // union of top-K
     const uint64_t pol = l2_policy_evict_last();  // W_r: small, read every call
+    if (a.tsplit == 2) {
+      // token split, local W_r: the first S K-blocks stream before the
+      // previous kernel is waited for (the X rows follow after pdl_wait)
 #pragma unroll 1
-    for (int i = 0; i < kb_cta && i < S; ++i) {
+      for (int i = 0; i < kb_cta * C && i < S; ++i) {
+        unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
+        mbar_arrive_expect_tx(&full[i], mt * kATile + xbytes);
+#pragma unroll 1
+        for (int tl = 0; tl < mt; ++tl)
+          tma_load_2d(st + tl * kATile, &wr_map, &full[i], i * kBK, tl * kBM, pol);
+      }
+    }
+#pragma unroll 1
+    for (int i = 0; i < kb_cta && i < S && !a.tsplit; ++i) {
       unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
       mbar_arrive_expect_tx(&full[i], mt * kATile + xbytes);
 #pragma unroll 1
@@ -550,8 +567,92 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 
   // ---- R + L1: per token chunk, split-K GEMM, then the owners' logit sums ----------
   int own = 0;
+  if (a.tsplit) {
+    // token split: this CTA owns tokens [tlo, thi) and computes their logits
+    // over the whole hidden dimension. K-block `it` of W_r is loaded once per
+    // cluster by CTA (it mod C) and multicast into every CTA's ring slot;
+    // each CTA adds its own X rows. A slot is refilled once all C CTAs'
+    // MMAs have released it (each commits to every CTA's empty barrier).
+    const int tlo = (n * rk) / C, thi = (n * (rk + 1)) / C;
+    own = thi - tlo;
+    const int KB = kb_cta * C;
+    const int n_mma = a.b_rows;
+    if (warp == 0 && lane == 0) {
+      const uint64_t pol_w = l2_policy_evict_last();
+      const uint64_t pol_x = l2_policy_evict_last();
 #pragma unroll 1
-  for (int c = 0; c < nch; ++c) {
+      for (int it = 0; it < KB; ++it) {
+        const int s = it % S;
+        unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
+        if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        const bool pre = a.tsplit == 2 && it < S;  // W_r already issued in the setup
+        if (!pre) mbar_arrive_expect_tx(&full[s], mt * kATile + xbytes);
+        if (pre) {
+        } else if (a.tsplit == 2) {  // every CTA streams all of W_r itself (no cluster lockstep)
+#pragma unroll 1
+          for (int tl = 0; tl < mt; ++tl)
+            tma_load_2d(st + tl * kATile, &wr_map, &full[s], it * kBK, tl * kBM, pol_w);
+        } else if (it % C == rk) {
+#pragma unroll 1
+          for (int tl = 0; tl < mt; ++tl)
+            tma_load_2d_mc(st + tl * kATile, &wr_map, &full[s], it * kBK, tl * kBM,
+                           static_cast<uint16_t>((1u << C) - 1u), pol_w);
+        }
+        tma_load_2d(st + mt * kATile, &x_maps.map[a.box_index], &full[s], it * kBK, tlo, pol_x);
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
+#pragma unroll 1
+      for (int it = 0; it < KB; ++it) {
+        const int s = it % S;
+        mbar_wait(&full[s], (it / S) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
+          const uint32_t b0 = a0 + mt * kATile;
+#pragma unroll 1
+          for (int tl = 0; tl < mt; ++tl)
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              tc_mma_bf16(tmem_base + tl * 256, sw128_kmajor_desc(a0 + tl * kATile + kk * 32),
+                          sw128_kmajor_desc(b0 + kk * 32), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          if (a.tsplit == 1)
+            tc_commit_mc(&empty[s], static_cast<uint16_t>((1u << C) - 1u));
+          else
+            tc_commit(&empty[s]);
+          if (it == KB - 1) tc_commit(tdone);
+        }
+        __syncwarp();
+      }
+    } else if (warp >= 4 && warp < 8) {
+      // drain TMEM: the own tokens' logits straight into xrow
+      mbar_wait(tdone, 0);
+      tc_fence_after();
+      const int q = warp & 3;
+      const int r = q * 32 + lane;
+#pragma unroll 1
+      for (int tl = 0; tl < mt; ++tl) {
+        const int e = tl * kBM + r;
+        const uint32_t lb = tmem_base + tl * 256 + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+        for (int cc = 0; cc < n_mma; cc += 16) {
+          float v[16];
+          tmem_ld16(lb + cc, v);
+          if (e < m) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (cc + j < own) xrow[(cc + j) * m + e] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+    }
+    if (tid < own) own_tok[tid] = tlo + tid;
+    FRONT_MARK(2);
+    FRONT_MARK(3);
+  }
+#pragma unroll 1
+  for (int c = 0; c < nch && !a.tsplit; ++c) {
     const int c0 = c * Tc;
     const int nc = n - c0 < Tc ? n - c0 : Tc;
     const int n_mma = (nc + 15) & ~15;
@@ -934,11 +1035,39 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 
 // Host plan: token chunk, pipeline depth, shared memory. Returns false when
 // the shape is outside the kernel's envelope.
-bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem) {
+bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem, int tsplit) {
   if (n < 1 || n > 256 || m < 1 || m > 256 || k < 1 || k > 32 || k > m) return false;
   if (d % (kBK * kFrontCta)) return false;
   const int mt = (m + kBM - 1) / kBM;
   const int kb_cta = (d / kBK) / kFrontCta;
+  if (tsplit) {
+    // token split: one "chunk", own = ceil(n / C) rows per CTA, X boxes of
+    // b_rows >= own rows, up to 4 ring stages over all d / 64 K-blocks
+    const int own_max = (n + kFrontCta - 1) / kFrontCta;
+    int b_rows = 16;
+    while (b_rows < own_max) b_rows <<= 1;
+    for (int vr = n;; vr = vr > 16 ? (vr + 1) / 2 : 0) {
+      if (vr == 0) return false;
+      const int kb_total = kb_cta * kFrontCta;
+      for (int stages = kb_total < 12 ? kb_total : 12; stages >= 2; --stages) {
+        const FrontSmem p = front_smem_plan(n, m, k, n, own_max, stages, b_rows, vr, 1);
+        if (p.total > static_cast<size_t>(kFrontSmemLimit)) continue;
+        int bi = 0;
+        while ((16 << bi) < b_rows) ++bi;
+        a->tsplit = tsplit;
+        a->chunk = n;
+        a->own_max = own_max;
+        a->stages = stages;
+        a->b_rows = b_rows;
+        a->box_index = bi;
+        a->kb_per_cta = kb_cta;
+        a->tmem_cols = mt * 256;
+        a->vote_rows = vr;
+        *smem = p.total;
+        return true;
+      }
+    }
+  }
   const int max_stages = kb_cta < 4 ? kb_cta : 4;
   // prefer: whole block in one GEMM chunk, >= 2 pipeline stages, the whole
   // vote matrix on chip; shrink the vote chunk first, then the token chunk
@@ -951,7 +1080,7 @@ bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem) {
       if (vr == 0) break;
       for (int stages = max_stages; stages >= 1; --stages) {
         if (stages < 2 && kb_cta > 1) break;
-        const FrontSmem p = front_smem_plan(n, m, k, chunk, own_max, stages, b_rows, vr);
+        const FrontSmem p = front_smem_plan(n, m, k, chunk, own_max, stages, b_rows, vr, 0);
         if (p.total > static_cast<size_t>(kFrontSmemLimit)) continue;
         int bi = 0;
         while ((16 << bi) < b_rows) ++bi;

@@ -62,6 +62,7 @@ struct FrontArgs {
   int n, m, k, act, strategy, seq_k, m_core, raw;
   int b_rows, box_index, kb_per_cta, stages, tmem_cols;
   int chunk, own_max;  // token chunk of the split-K GEMM; own tokens per CTA bound
+  int tsplit;          // 1: token-split router GEMM (multicast W_r, no partial exchange)
   int vote_rows;       // token rows of the shared-memory vote matrix chunk
   int* route_idx;      // [n x k]
   double* route_gate;  // [n x k]
@@ -107,7 +108,7 @@ __host__ __device__ inline uint64_t route_word(uint32_t tag, int expert, float g
 
 // Fills the plan fields of `a` (chunk, stages, boxes, TMEM) and the dynamic
 // shared memory; false if the shape is outside the cluster kernel's envelope.
-bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem);
+bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem, int tsplit = 0);
 
 struct CoresetArgs {
   int n, m, k, strategy, seq_k, m_core, raw;
