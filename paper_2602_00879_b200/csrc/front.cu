@@ -606,6 +606,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       for (int it = 0; it < KB; ++it) {
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
+        if (tracing && lane == 0 && (it & 7) == 0 && it < 40) s_ts[26 + it / 8] = gtime();
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);

@@ -86,7 +86,7 @@ def main():
         if (ev == 74 + i).any():
             out["front_" + nm] = [round(float(t[ev == 74 + i].min()), 2),
                                   round(float(t[ev == 74 + i].max()), 2)]
-    chunks = [round(float(t[ev == 66 + c].max()), 2) for c in range(4) if (ev == 66 + c).any()
+    chunks = [round(float(t[ev == 66 + c].max()), 2) for c in range(5) if (ev == 66 + c).any()
               and float(t[ev == 66 + c].max()) < 1e6 and float(t[ev == 66 + c].max()) > 0]
     if chunks:
         out["front_chunk_ends"] = chunks
