@@ -1,12 +1,13 @@
 """The reference's OWN unit tests (/root/reference/proj/tests/test_gating.cpp,
-test_des.cpp, test_baselines.cpp, test_trace.cpp and test_analysis.cpp,
-compiled unchanged by tests/cpp/Makefile; test_analysis.cpp's one Monte-Carlo
-oracle comes from the test-only stub tests/cpp/stub/dessim/oracle.hpp)
+test_des.cpp, test_baselines.cpp, test_trace.cpp, test_analysis.cpp and
+test_metrics.cpp, compiled unchanged by tests/cpp/Makefile; test_analysis.cpp's
+one Monte-Carlo oracle comes from the test-only stub
+tests/cpp/stub/dessim/oracle.hpp)
 run against the C++ facade include/dessim/*.hpp -> libdessim_gpu.so ->
 libdesmoe.so.
 
 * CPU: the doctest stand-in runs the same suites against the reference library
-  itself (oracle/_ref) with 85/85 passing, the facade exports the reference's
+  itself (oracle/_ref) with 99/99 passing, the facade exports the reference's
   dessim:: symbols, and without a GPU the facade fails loudly (no CPU path).
 * GPU: every reference test case passes on the B200 path.
 """
@@ -31,7 +32,7 @@ def _run(path):
 def test_doctest_standin_runs_reference_suites_on_reference():
     r = _run(ON_REF)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "| 85 passed | 0 failed" in r.stdout, r.stdout
+    assert "| 99 passed | 0 failed" in r.stdout, r.stdout
 
 
 def test_facade_exports_reference_api():
@@ -47,7 +48,9 @@ def test_facade_exports_reference_api():
                 "dessim::mcmoe_route(", "dessim::baseline_route(", "dessim::gen_trace(",
                 "dessim::encode_trace(", "dessim::decode_trace(", "dessim::read_trace(",
                 "dessim::write_trace(", "dessim::moe_latency(", "dessim::coreset_latency_bound(",
-                "dessim::expected_unique_experts(", "dessim::memory_footprint("]:
+                "dessim::expected_unique_experts(", "dessim::memory_footprint(",
+                "dessim::topk_recall(", "dessim::reconstruction_loss(",
+                "dessim::expert_importance_map(", "dessim::hit_rates(", "dessim::hit_rate_cosine("]:
         assert sym in out, sym
 
 
