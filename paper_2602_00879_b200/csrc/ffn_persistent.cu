@@ -739,10 +739,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[buf]);
       if (phaseA) {
         named_bar_sync(1, 128);
-        if (etid == 0) {
-          __threadfence();  // all epilogue stores (ordered by the barrier) -> gpu scope
-          atomic_add_release(&h_ready[ui.expert * tilesA + ui.tile], 1);
-        }
+        if (etid == 0)  // the barrier orders every epilogue thread's H stores before this
+          atomic_add_release(&h_ready[ui.expert * tilesA + ui.tile], 1);  // cumulative release
       }
       if (etid == 0) trace_put(tc, 3, uu);
       ++nunit;
