@@ -149,6 +149,18 @@ def test_layer_host_entry_matches_device_entry():
     layer.forward_host(xh, yh, sh)
     assert torch.equal(yh, y_dev.cpu())  # deterministic: bit-identical
     assert sh[0].item() <= 25
+    # pageable buffers: the entry copies y back instead of writing it in place
+    yp = torch.empty((n, d), dtype=torch.float32)
+    sp = torch.empty(4, dtype=torch.int32)
+    layer.forward_host(x.cpu(), yp, sp)
+    assert torch.equal(yp, y_dev.cpu()) and torch.equal(sp, sh)
+    # a non-finite input is reported through the host-mapped check word
+    xb = x.cpu().clone()
+    xb[3, 5] = float("nan")
+    with pytest.raises(ValueError, match="non-finite logit"):
+        layer.forward_host(xb.pin_memory(), yh, sh)
+    layer.forward_host(xh, yh, sh)  # the flag was cleared
+    assert torch.equal(yh, y_dev.cpu())
 
 
 @pytest.mark.gpu
