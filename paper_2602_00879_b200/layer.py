@@ -52,6 +52,7 @@ class DesMoeLayer:
                                             expert_range=expert_range, ctx=ctx)
         self.ctx = self.experts.ctx
         self.stats = torch.zeros(4, dtype=torch.int32, device="cuda")
+        self._rc = {}  # strategy -> RouteCfg (built once: the per-call path stays thin)
 
     def forward(self, x, y=None, strategy=None, stream=None):
         """x [n x d] bf16 on the device -> y [n x d] fp32 (stream-ordered)."""
@@ -59,20 +60,28 @@ class DesMoeLayer:
         n = x.shape[0]
         if y is None:
             y = torch.empty((n, self.cfg.hidden), dtype=torch.float32, device=x.device)
-        rc = self.cfg.route_cfg(strategy)
-        st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream()
-        check(lib().desmoe_layer_forward(self.ctx.h, self.experts.h, _ptr(self.w_router),
-                                         _ptr(x), n, C.byref(rc), _ptr(y), _ptr(self.stats), st))
+        rc = self._route_cfg(strategy)
+        st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        check(lib().desmoe_layer_forward(self.ctx.h, self.experts.h, self.w_router.data_ptr(),
+                                         x.data_ptr(), n, C.byref(rc), y.data_ptr(),
+                                         self.stats.data_ptr(), st))
         return y
+
+    def _route_cfg(self, strategy):
+        rc = self._rc.get(strategy)
+        if rc is None:
+            rc = self._rc[strategy] = self.cfg.route_cfg(strategy)
+        return rc
 
     def forward_host(self, x_host, y_host, stats_host=None, strategy=None):
         """Host (pinned) bf16 x -> host fp32 y through desmoe_layer_forward_host
         (H2D copy, layer, D2H copy, synchronise)."""
-        rc = self.cfg.route_cfg(strategy)
+        import torch
         check(lib().desmoe_layer_forward_host(
-            self.ctx.h, self.experts.h, _ptr(self.w_router), _ptr(x_host), x_host.shape[0],
-            C.byref(rc), _ptr(y_host), _ptr(stats_host) if stats_host is not None else None,
-            _stream()))
+            self.ctx.h, self.experts.h, self.w_router.data_ptr(), x_host.data_ptr(),
+            x_host.shape[0], C.byref(self._route_cfg(strategy)), y_host.data_ptr(),
+            stats_host.data_ptr() if stats_host is not None else None,
+            torch.cuda.current_stream().cuda_stream))
         return y_host
 
     def last_logits(self, n):
