@@ -108,6 +108,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+SPIN_CYCLES = 50_000  # ~25 µs at 1.9 GHz
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -261,6 +264,10 @@ def main():
                 flush.fill_(i & 0xFF)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            # a ~25 µs spin kernel ahead of the start event keeps the stream
+            # busy while the host enqueues the layer, so the events bracket
+            # device work only (no host launch gap inside the timed interval)
+            torch.cuda._sleep(SPIN_CYCLES)
             e0.record(stream)
             layer.forward(x_in, y, strategy=strat)
             e1.record(stream)

@@ -68,9 +68,11 @@ class DesMoeLayer:
         return y
 
     def _route_cfg(self, strategy):
-        rc = self._rc.get(strategy)
+        c = self.cfg  # LayerConfig is mutable (e.g. seq_k): key on every routed field
+        key = (strategy, c.experts, c.top_k, c.activation, c.strategy, c.seq_k, c.vote_beta)
+        rc = self._rc.get(key)
         if rc is None:
-            rc = self._rc[strategy] = self.cfg.route_cfg(strategy)
+            rc = self._rc[key] = c.route_cfg(strategy)
         return rc
 
     def forward_host(self, x_host, y_host, stats_host=None, strategy=None):

@@ -194,3 +194,23 @@ def test_stack_equals_chained_layers(strategy):
         y = layer.forward(xin) + xin.float()
         xin = y.to(torch.bfloat16)
     assert torch.equal(y_res, y)
+
+
+@pytest.mark.gpu
+def test_layer_config_changes_take_effect():
+    """LayerConfig is mutable (bench.py switches seq_k between DES-Seq k=3 and
+    k=2 on one layer): every call must route with the current fields."""
+    m, d, f, n = 64, 512, 512, 32
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=31)
+    wr = synth.router_weights(m, d, seed=32)
+    x = synth.hidden_states(n, d, seed=33, rho=0.3)
+    cfg = LayerConfig(m, 8, d, f, strategy="seq", seq_k=3)
+    layer = DesMoeLayer(cfg, wr, wg, wu, wd)
+    layer.forward(x)
+    torch.cuda.synchronize()
+    core3 = int(layer.stats[1].item())
+    cfg.seq_k = 1
+    layer.forward(x)
+    torch.cuda.synchronize()
+    core1 = int(layer.stats[1].item())
+    assert core1 < core3, (core1, core3)

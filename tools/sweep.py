@@ -65,6 +65,7 @@ def main():
                         flush.fill_(i & 0xFF)
                         e0 = torch.cuda.Event(enable_timing=True)
                         e1 = torch.cuda.Event(enable_timing=True)
+                        torch.cuda._sleep(50_000)  # keeps the host launch gap outside the events
                         e0.record(stream)
                         layer.forward(x_in, y, strategy=s)
                         e1.record(stream)
