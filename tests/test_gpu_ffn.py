@@ -94,6 +94,7 @@ def test_moe_forward_facade(ref):
     (64, 2048, 1024, 32, "vote"),
     (256, 1024, 512, 64, "seq"),
     (128, 512, 768, 256, "vote"),
+    (256, 2048, 512, 256, "vote"),   # token-split router GEMM at the C3 shape
 ])
 def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
     torch.manual_seed(0)
