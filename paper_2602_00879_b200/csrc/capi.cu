@@ -927,7 +927,9 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
                      static_cast<size_t>(m) * n <= static_cast<size_t>(c->max_n) * c->max_k &&
                      !std::getenv("DESMOE_NO_DENSE");
   a.dense = dense ? 1 : 0;
-  if (std::getenv("DESMOE_NO_L2PF")) a.flags |= 1;
+  // the first unit's L2 bulk prefetch at pick-up measured slightly slower
+  // (the SMs' own TMA streams start at once in dense mode): opt-in only
+  if (!std::getenv("DESMOE_L2PF")) a.flags |= 1;
   if (const char* fl = std::getenv("DESMOE_FFN_FLAGS")) a.flags |= std::atoi(fl);  // experiments
   a.pub = ex->pub;
   a.route_words = ex->route_words;
