@@ -947,7 +947,9 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
                     4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
   int stages = (kSmemLimit - 256 - fixed) / stage_bytes;  // 256 B: the kernel's static smem
-  stages = std::max(2, std::min(stages, 8));
+  // 4 stages (128 KB of weights in flight per SM) measured best: deeper
+  // rings only lengthen the queues every other memory access waits behind
+  stages = std::max(2, std::min(stages, 4));
   if (const char* sv = std::getenv("DESMOE_FFN_STAGES"))  // tuning experiments
     stages = std::max(2, std::min(stages, std::atoi(sv)));
   a.stages = stages;
