@@ -889,7 +889,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
              const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false,
              bool after_front = false, __nv_bfloat16* y_bf16 = nullptr,
-             const void* resid = nullptr) {
+             const void* resid = nullptr, bool prefer_dense = false) {
   const int m = ex->m, d = ex->d, f = ex->f;
   if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
   const int words = ffn_counter_words(m, f);
@@ -923,7 +923,9 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   // dense: small blocks compute every published expert for every token (the
   // tensor pipe is nearly idle in this memory-bound layer), so the FFN needs
   // only the published expert list — no route, permutation or gather
-  const bool dense = a.early && n <= kDenseMaxTokens &&
+  // (dense writes U x N output rows where the routed mode writes N x K: it
+  // pays when U is small, as for the DES coresets — the caller's hint)
+  const bool dense = a.early && n <= kDenseMaxTokens && prefer_dense &&
                      static_cast<size_t>(m) * n <= static_cast<size_t>(c->max_n) * c->max_k &&
                      !std::getenv("DESMOE_NO_DENSE");
   a.dense = dense ? 1 : 0;
@@ -1234,9 +1236,16 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
     c->launches += zeroed ? 1 : (cfg->strategy == DESMOE_VANILLA ? 1 : 3);
   }
   mark(c, st);
+  // dense FFN mode (every streamed expert x every token) for the DES
+  // coresets; vanilla's union (~57 of 64 experts at C2) writes fewer rows in
+  // the routed mode unless the block is tiny. Measured at C2 N=32: vanilla
+  // 131.6 routed vs 133.0 dense; DES-Seq k=2 87.5 dense vs 89.4 routed.
+  const bool prefer_dense = cfg->strategy != DESMOE_VANILLA ||
+                            std::min(cfg->experts, n * cfg->top_k) <= 4 * cfg->top_k ||
+                            std::getenv("DESMOE_ALWAYS_DENSE");
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
-                front_used, y_bf16, residual ? x : nullptr);
+                front_used, y_bf16, residual ? x : nullptr, prefer_dense);
   if (rc) return rc;
   return DESMOE_OK;
 }
