@@ -1238,10 +1238,10 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   mark(c, st);
   // dense FFN mode (every streamed expert x every token) for the DES
   // coresets; vanilla's union (~57 of 64 experts at C2) writes fewer rows in
-  // the routed mode unless the block is tiny. Measured at C2 N=32: vanilla
-  // 131.6 routed vs 133.0 dense; DES-Seq k=2 87.5 dense vs 89.4 routed.
-  const bool prefer_dense = cfg->strategy != DESMOE_VANILLA ||
-                            std::min(cfg->experts, n * cfg->top_k) <= 4 * cfg->top_k ||
+  // the routed mode from N = 32 on. Measured (C2): vanilla N=32 131.6 routed
+  // vs 133.0 dense, N=64 149.5 vs 153.6, but N=8 96.3 dense vs 100.3 routed;
+  // DES-Seq k=2 at N=32 87.5 dense vs 89.4 routed.
+  const bool prefer_dense = cfg->strategy != DESMOE_VANILLA || n <= 16 ||
                             std::getenv("DESMOE_ALWAYS_DENSE");
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
