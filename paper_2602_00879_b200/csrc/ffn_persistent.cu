@@ -143,6 +143,7 @@ __device__ int block_exclusive_scan(int* v, int n, int* warp_sums) {
 
 }  // namespace
 
+template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,   // packed gate/up tiles
                           const __grid_constant__ CUtensorMap w_b,   // (unused)
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool dense = a.dense != 0;
   const int S = a.stages;
   const int b_box_bytes = a.b_rows * 128;
-  const int stage_bytes = 2 * kATile + 2 * b_box_bytes;
+  const int stage_bytes = KB * kATile + KB * b_box_bytes;
 
   // ---- shared-memory carve-up --------------------------------------------
   unsigned char* ring = smem;
@@ -232,8 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tag = hand_tag(seq);
   const int lo = a.expert_lo, hi = a.expert_hi;
   const int tilesA = f / kHalf, tilesB = d / kBM;
-  const int ksA = d / (2 * kBK);                 // k-steps: 2 K blocks each
-  const int ksB = (swiglu ? f : d) / (2 * kBK);
+  const int ksA = d / (KB * kBK);               // k-steps: KB K blocks each
+  const int ksB = (swiglu ? f : d) / (KB * kBK);
   int pre_u = -1, pre_ks = 0;  // early mode: unit claimed and k-steps issued before the prologue
   if (a.early && warp == 0) {
     // the published expert list (coreset / union) -> the unit list; claim
@@ -284,21 +285,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
         for (; pre_ks < ksteps && pre_ks < S - 1; ++pre_ks) {
           unsigned char* st = ring + static_cast<size_t>(pre_ks) * stage_bytes;
-          mbar_arrive_expect_tx(&full[pre_ks], 2 * kATile);
-          const int tile0 = phaseA ? (el * tilesA + tile) * (2 * ksA) + 2 * pre_ks
-                                   : (el * tilesB + tile) * (2 * ksB) + 2 * pre_ks;
-          tma_load_3d(st, wmap, &full[pre_ks], 0, 0, tile0, pol_w);
-          tma_load_3d(st + kATile, wmap, &full[pre_ks], 0, 0, tile0 + 1, pol_w);
+          mbar_arrive_expect_tx(&full[pre_ks], KB * kATile);
+          const int tile0 = phaseA ? (el * tilesA + tile) * (KB * ksA) + KB * pre_ks
+                                   : (el * tilesB + tile) * (KB * ksB) + KB * pre_ks;
+#pragma unroll
+          for (int j = 0; j < KB; ++j)
+            tma_load_3d(st + j * kATile, wmap, &full[pre_ks], 0, 0, tile0 + j, pol_w);
         }
         // the rest of the unit (one contiguous packed region) goes to L2 now,
         // so HBM keeps streaming while the prologue waits for the route
         if (pre_ks < ksteps && !(a.flags & 1)) {
-          const int tile0 = phaseA ? (el * tilesA + tile) * (2 * ksA) + 2 * pre_ks
-                                   : (el * tilesB + tile) * (2 * ksB) + 2 * pre_ks;
+          const int tile0 = phaseA ? (el * tilesA + tile) * (KB * ksA) + KB * pre_ks
+                                   : (el * tilesB + tile) * (KB * ksB) + KB * pre_ks;
           const unsigned char* base =
               static_cast<const unsigned char*>(phaseA ? a.wa_base : a.wc_base);
           bulk_prefetch_l2(base + static_cast<size_t>(tile0) * kATile,
-                           static_cast<uint32_t>((ksteps - pre_ks) * 2 * kATile));
+                           static_cast<uint32_t>((ksteps - pre_ks) * KB * kATile));
         }
       }
     }
@@ -514,15 +516,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
-          mbar_arrive_expect_tx(&full[s], 2 * kATile);
+          mbar_arrive_expect_tx(&full[s], KB * kATile);
           // packed weights: tile-contiguous 16 KB blocks in (expert, row tile,
           // K block) order, so a unit streams one contiguous region
           const int el = ui.expert - lo;  // packed weights hold the owned experts only
-          const int tile0 = phaseA ? (el * tilesA + ui.tile) * (2 * ksA) + 2 * ks
-                                   : (el * tilesB + ui.tile) * (2 * ksB) + 2 * ks;
+          const int tile0 = phaseA ? (el * tilesA + ui.tile) * (KB * ksA) + KB * ks
+                                   : (el * tilesB + ui.tile) * (KB * ksB) + KB * ks;
           const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
-          tma_load_3d(st, wmap, &full[s], 0, 0, tile0, pol_w);
-          tma_load_3d(st + kATile, wmap, &full[s], 0, 0, tile0 + 1, pol_w);
+#pragma unroll
+          for (int j = 0; j < KB; ++j)
+            tma_load_3d(st + j * kATile, wmap, &full[s], 0, 0, tile0 + j, pol_w);
         }
       }
     }
@@ -561,8 +564,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (!from_x) {
             // H columns [128 ks, 128 ks + 128) = phase-A tiles 2ks, 2ks+1
-            for (int h = 0; h < 2; ++h) {
-              const int* flag = &h_ready[ui.expert * tilesA + 2 * ks + h];
+            for (int h = 0; h < KB; ++h) {
+              const int* flag = &h_ready[ui.expert * tilesA + KB * ks + h];
               if (ld_acquire(flag) == 0) {
                 while (ld_acquire(flag) == 0) {
                 }
@@ -571,12 +574,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             fence_proxy_async_global();
           }
-          unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes + 2 * kATile;
-          mbar_arrive_expect_tx(&full[s], 2 * box_bytes);
+          unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes + KB * kATile;
+          mbar_arrive_expect_tx(&full[s], KB * box_bytes);
           const int row = dense && from_x ? 0 : ui.brow;  // dense: X itself (all tokens)
-          tma_load_2d(st, &acts.map[bi], &full[s], 2 * ks * kBK, row, pol_x);
-          tma_load_2d(st + b_box_bytes, &acts.map[bi], &full[s], (2 * ks + 1) * kBK, row,
-                      pol_x);
+#pragma unroll
+          for (int j = 0; j < KB; ++j)
+            tma_load_2d(st + j * b_box_bytes, &acts.map[bi], &full[s], (KB * ks + j) * kBK, row,
+                        pol_x);
         }
       }
     }
@@ -611,9 +615,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
-          const uint32_t b0 = a0 + 2 * kATile;
+          const uint32_t b0 = a0 + KB * kATile;
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < KB; ++h)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
               tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + h * kATile + kk * 32),
@@ -772,6 +776,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_dealloc(tmem_base, 512);
   }
 }
+
+template __global__ void ffn_persistent_kernel<2>(const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ BoxMaps,
+                                                   const __grid_constant__ BoxMaps, FfnArgs);
+template __global__ void ffn_persistent_kernel<4>(const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ BoxMaps,
+                                                   const __grid_constant__ BoxMaps, FfnArgs);
 
 // Packs row-major bf16 weights into tile-contiguous blocks:
 //   out[((e * row_tiles + rt) * kblocks + kb)][r][c] = src(e, rt, r)[kb * 64 + c]

@@ -226,6 +226,7 @@ struct FfnArgs {
   int flags;                 // experiments: 1 = no L2 prefetch of the first unit
   int gather_ctas;           // CTAs that gather x rows (and the x_ready target)
   int dense;                 // every published expert x every token (small blocks)
+  int kb;                    // 64-wide K blocks per ring stage: 4 when d, F allow, else 2
 };
 
 // Ordered combine arguments (combine_slots_kernel).
@@ -278,6 +279,9 @@ __global__ void baseline_route_kernel(BaselineArgs<T> a);
 
 inline int ffn_counter_words(int m, int f) { return 2 + m * (f / 64); }
 
+// KB = 64-wide K blocks per ring stage (2 or 4; compile-time so the stage
+// loops unroll — a runtime count measured 2-3 us slower per block)
+template <int KB>
 __global__ void ffn_persistent_kernel(const __grid_constant__ CUtensorMap w_a,
                                       const __grid_constant__ CUtensorMap w_b,
                                       const __grid_constant__ CUtensorMap w_c,

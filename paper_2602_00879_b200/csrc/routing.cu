@@ -388,7 +388,8 @@ cudaError_t set_kernel_smem_limits() {
   set(reinterpret_cast<const void*>(constrained_route_kernel), routing);
   set(reinterpret_cast<const void*>(permute_kernel), routing);
   set(reinterpret_cast<const void*>(tile_gemm_kernel), 227 * 1024);
-  set(reinterpret_cast<const void*>(ffn_persistent_kernel), 227 * 1024);
+  set(reinterpret_cast<const void*>(ffn_persistent_kernel<2>), 227 * 1024);
+  set(reinterpret_cast<const void*>(ffn_persistent_kernel<4>), 227 * 1024);
   const cudaError_t f = set_fused_route_smem_limit(kFusedRouteSmem);
   const cudaError_t g = set_front_smem_limit();
   return e != cudaSuccess ? e : (f != cudaSuccess ? f : g);
