@@ -241,10 +241,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the first unit and start streaming its weights while the route is
     // still being computed (one warp polls the list in parallel)
     uint32_t w0 = 0;
+    int u0 = 0;
     if (lane == 0) {
       do {
         w0 = ld_relaxed_u32(a.pub);
       } while ((w0 >> 10) != tag);
+      // claim the first unit now (the counter was zeroed before the front
+      // published): its round trip overlaps the list words' below
+      u0 = atomicAdd(sched, 1);
     }
     const int cnt = static_cast<int>(__shfl_sync(0xffffffffu, w0, 0) & 1023u);
     if (lane == 0) s_pcnt = cnt;
@@ -272,7 +276,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       s_upub = u;
       const int n_units0 = (swiglu ? u * tilesA : 0) + u * tilesB;
-      const int u0 = atomicAdd(sched, 1);
       if (u0 < n_units0) {
         pre_u = u0;
         const int nA0 = swiglu ? u * tilesA : 0;
