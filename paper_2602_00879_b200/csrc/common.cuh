@@ -506,4 +506,10 @@ __device__ inline void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Arrive on a named barrier without waiting (producer side of a hand-off:
+// the threads that bar.sync on it see this thread's earlier shared writes).
+__device__ inline void named_bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 }  // namespace desmoe

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   __shared__ uint64_t s_pts[8];  // prologue timeline (trace buffer only)
+  if (a.trace && tid < 8) s_pts[tid] = 0;
   __shared__ int s_upub;         // early mode: owned published experts
   __shared__ int s_pcnt;         // early mode: published list length
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // claim the first unit now (the counter was zeroed before the front
       // published): its round trip overlaps the list words' below
       u0 = atomicAdd(sched, 1);
+      if (a.trace) s_pts[5] = gtime();  // list count seen
     }
     const int cnt = static_cast<int>(__shfl_sync(0xffffffffu, w0, 0) & 1023u);
     if (lane == 0) s_pcnt = cnt;
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     if (lane == 0) {
+      if (a.trace) s_pts[6] = gtime();  // list words loaded
       s_upub = u;
       const int n_units0 = (swiglu ? u * tilesA : 0) + u * tilesB;
       if (u0 < n_units0) {
@@ -756,8 +759,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (a.trace && tid == 0) {
     unsigned long long* cur = reinterpret_cast<unsigned long long*>(a.trace);
-    const unsigned long long i0 = atomicAdd(cur, 5ull);
-    for (int i = 0; i < 5; ++i)
+    const unsigned long long i0 = atomicAdd(cur, 7ull);
+    for (int i = 0; i < 7; ++i)
       if (i0 + i < static_cast<unsigned long long>(a.trace_cap)) {
         a.trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (90 + i);
         a.trace[3 + 2 * (i0 + i)] = s_pts[i];

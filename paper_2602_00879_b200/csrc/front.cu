@@ -772,85 +772,183 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     tmem_dealloc(tmem_base, a.tmem_cols);
   }
 
-  // ---- L2: row max + finiteness (warp per token) ----------------------------------
+  // ---- L2-L4 in two warp groups (small blocks: at most one token per warp) ------
+  // The top-K selection keys on the fp32 logits (every activation is monotone
+  // in the logit), so warps 0-7 select while warps 8-15 compute the row max,
+  // the fp64 activation and the ordered sums; the selectors then wait (named
+  // barrier 2) for the activation to check their boundaries.
+  constexpr int kGW = NW / 2;  // warps per group
+  if (own <= kGW && !(a.flags & 2)) {  // (flag 2: always in sequence, for A/B runs)
+    if (warp < kGW) {
+      const int want = k < m ? k : m;
+      const int rounds = want < m ? want + 1 : want;
+      if (tracing && warp == 0 && lane == 0) s_ts[34] = gtime();
 #pragma unroll 1
-  for (int j = warp; j < own; j += NW) {
-    uint32_t best = 0;
-    bool bad = false;
-#pragma unroll 1
-    for (int i = lane; i < m; i += 32) {
-      const float v = xrow[j * m + i];
-      bad |= !isfinite(v);
-      const uint32_t kk = fkey(v);
-      best = kk > best ? kk : best;
-    }
-    best = __reduce_max_sync(0xffffffffu, best);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
-    if (lane == 0) mxv[j] = __uint_as_float((best & 0x80000000u) ? (best & 0x7fffffffu) : ~best);
-  }
-  __syncthreads();
-  FRONT_MARK(5);
-  // ---- L3: activation in fp64, data-parallel over (own token, expert) ----------
-#pragma unroll 1
-  for (int w = tid; w < own * m; w += kFrontThreads) {
-    const int j = w / m, i = w - j * m;
-    const double x = static_cast<double>(xrow[w]);
-    double e = x;
-    if (act < 2) {
-      const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x);
-      e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
-    }
-    erow[j * ew + i] = e;
-  }
-  __syncthreads();
-  FRONT_MARK(6);
-  // ---- L4: ordered softmax sums (one lane per token, last warp) || top-K (others)
-  if (warp == NW - 1) {
-#pragma unroll 1
-    for (int j = lane; j < own; j += 32) {
-      double s = 1.0;
-      if (act == 0) {
-        s = 0.0;
-        const double* er = erow + j * ew;
-        int i = 0;
-#pragma unroll 1
-        for (; i + 8 <= m; i += 8) {  // ascending index (gating.cpp:31-33)
-          double v[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = er[i + q];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) s += v[q];
+      for (int j = warp; j < own; j += kGW) {
+        long long c0 = clock64();
+        if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[35] = gtime();
+        warp_rank_select(xrow + j * m, m, rounds, nullptr, sel + j * 33);
+        if (tracing && warp == 0 && lane == 0 && j == 0) {
+          s_ts[23] = clock64() - c0;
+          s_ts[36] = gtime();
         }
-#pragma unroll 1
-        for (; i < m; ++i) s += er[i];
       }
-      ssum[j] = s;
-    }
-    if (tracing && lane == 0) s_ts[21] = gtime();
+      named_bar_sync(2, kFrontThreads);  // the activation (erow) is written
+#pragma unroll 1
+      for (int j = warp; j < own; j += kGW) {
+        if (lane == 0) {
+          const int* sj = sel + j * 33;
+          const float* xr = xrow + j * m;
+          const double* er = erow + j * ew;
+          bool r = want < m && risky_boundary(xr, er, act, sj, want);
+          if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
+          risky[j] = r;
+        }
+      }
+      if (tracing && warp == 0 && lane == 0) s_ts[37] = gtime();
+      if (tracing && warp == 0 && lane == 0) s_ts[22] = gtime();
   } else {
-    const int want = k < m ? k : m;
-    const int rounds = want < m ? want + 1 : want;
-    if (tracing && warp == 0 && lane == 0) s_ts[34] = gtime();
+      const int gw = warp - kGW, gt = tid - kGW * 32;
+      // L2: row max + finiteness (warp per token)
 #pragma unroll 1
-    for (int j = warp; j < own; j += NW - 1) {
-      int* sj = sel + j * 33;
-      const float* xr = xrow + j * m;
-      const double* er = erow + j * ew;
-      long long c0 = clock64();
-      if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[35] = gtime();
-      warp_rank_select(xr, m, rounds, nullptr, sj);
-      if (tracing && warp == 0 && lane == 0 && j == 0) {
-        s_ts[23] = clock64() - c0;
-        s_ts[36] = gtime();
+      for (int j = gw; j < own; j += kGW) {
+        uint32_t best = 0;
+        bool bad = false;
+#pragma unroll 1
+        for (int i = lane; i < m; i += 32) {
+          const float v = xrow[j * m + i];
+          bad |= !isfinite(v);
+          const uint32_t kk = fkey(v);
+          best = kk > best ? kk : best;
+        }
+        best = __reduce_max_sync(0xffffffffu, best);
+        if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+        if (lane == 0) mxv[j] = __uint_as_float((best & 0x80000000u) ? (best & 0x7fffffffu) : ~best);
       }
-      if (lane == 0) {
-        bool r = want < m && risky_boundary(xr, er, act, sj, want);
-        if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
-        risky[j] = r;
+      named_bar_sync(3, kFrontThreads / 2);
+      if (tracing && gt == 0) s_ts[5] = gtime();
+      // L3: activation in fp64, data-parallel over (own token, expert)
+#pragma unroll 1
+      for (int w = gt; w < own * m; w += kFrontThreads / 2) {
+        const int j = w / m, i = w - j * m;
+        const double x = static_cast<double>(xrow[w]);
+        double e = x;
+        if (act < 2) {
+          const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x);
+          e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
+        }
+        erow[j * ew + i] = e;
       }
-      if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[37] = gtime();
+      named_bar_sync(3, kFrontThreads / 2);
+      named_bar_arrive(2, kFrontThreads);  // hand the activation to the selectors
+      if (tracing && gt == 0) s_ts[6] = gtime();
+      // L4: ordered softmax sums, one lane per token (ascending index, gating.cpp:31-33)
+      if (warp == NW - 1) {
+#pragma unroll 1
+        for (int j = lane; j < own; j += 32) {
+          double s = 1.0;
+          if (act == 0) {
+            s = 0.0;
+            const double* er = erow + j * ew;
+            int i = 0;
+#pragma unroll 1
+            for (; i + 8 <= m; i += 8) {
+              double v[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) v[q] = er[i + q];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) s += v[q];
+            }
+#pragma unroll 1
+            for (; i < m; ++i) s += er[i];
+          }
+          ssum[j] = s;
+        }
+        if (tracing && lane == 0) s_ts[21] = gtime();
+      }
     }
-    if (tracing && warp == 0 && lane == 0) s_ts[22] = gtime();
+    } else {
+    // large blocks: the phases in sequence over all warps
+    // ---- L2: row max + finiteness (warp per token) ----------------------------------
+#pragma unroll 1
+    for (int j = warp; j < own; j += NW) {
+      uint32_t best = 0;
+      bool bad = false;
+#pragma unroll 1
+      for (int i = lane; i < m; i += 32) {
+        const float v = xrow[j * m + i];
+        bad |= !isfinite(v);
+        const uint32_t kk = fkey(v);
+        best = kk > best ? kk : best;
+      }
+      best = __reduce_max_sync(0xffffffffu, best);
+      if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+      if (lane == 0) mxv[j] = __uint_as_float((best & 0x80000000u) ? (best & 0x7fffffffu) : ~best);
+    }
+    __syncthreads();
+    FRONT_MARK(5);
+    // ---- L3: activation in fp64, data-parallel over (own token, expert) ----------
+#pragma unroll 1
+    for (int w = tid; w < own * m; w += kFrontThreads) {
+      const int j = w / m, i = w - j * m;
+      const double x = static_cast<double>(xrow[w]);
+      double e = x;
+      if (act < 2) {
+        const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x);
+        e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
+      }
+      erow[j * ew + i] = e;
+    }
+    __syncthreads();
+    FRONT_MARK(6);
+    // ---- L4: ordered softmax sums (one lane per token, last warp) || top-K (others)
+    if (warp == NW - 1) {
+#pragma unroll 1
+      for (int j = lane; j < own; j += 32) {
+        double s = 1.0;
+        if (act == 0) {
+          s = 0.0;
+          const double* er = erow + j * ew;
+          int i = 0;
+#pragma unroll 1
+          for (; i + 8 <= m; i += 8) {  // ascending index (gating.cpp:31-33)
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = er[i + q];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += v[q];
+          }
+#pragma unroll 1
+          for (; i < m; ++i) s += er[i];
+        }
+        ssum[j] = s;
+      }
+      if (tracing && lane == 0) s_ts[21] = gtime();
+    } else {
+      const int want = k < m ? k : m;
+      const int rounds = want < m ? want + 1 : want;
+      if (tracing && warp == 0 && lane == 0) s_ts[34] = gtime();
+#pragma unroll 1
+      for (int j = warp; j < own; j += NW - 1) {
+        int* sj = sel + j * 33;
+        const float* xr = xrow + j * m;
+        const double* er = erow + j * ew;
+        long long c0 = clock64();
+        if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[35] = gtime();
+        warp_rank_select(xr, m, rounds, nullptr, sj);
+        if (tracing && warp == 0 && lane == 0 && j == 0) {
+          s_ts[23] = clock64() - c0;
+          s_ts[36] = gtime();
+        }
+        if (lane == 0) {
+          bool r = want < m && risky_boundary(xr, er, act, sj, want);
+          if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
+          risky[j] = r;
+        }
+        if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[37] = gtime();
+      }
+      if (tracing && warp == 0 && lane == 0) s_ts[22] = gtime();
+    }
   }
   __syncthreads();
   FRONT_MARK(7);

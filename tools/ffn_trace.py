@@ -103,16 +103,19 @@ def main():
     for e_, nm in names.items():
         if (ev == e_).any():
             out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
-    for i, nm in enumerate(["pdl_released", "counted", "slotted", "gathered", "x_ready_added"]):
-        if (ev == 90 + i).any():
-            out["ffn_" + nm] = [round(float(t[ev == 90 + i].min()), 2),
-                                round(float(t[ev == 90 + i].max()), 2)]
+    for i, nm in enumerate(["pdl_released", "counted", "slotted", "gathered", "x_ready_added",
+                            "list_count_seen", "list_loaded"]):
+        sel = (ev == 90 + i) & (rec[:, 1] != 0)  # (0 = not reached in this mode)
+        if sel.any():
+            out["ffn_" + nm] = [round(float(t[sel].min()), 2), round(float(np.median(t[sel])), 2),
+                                round(float(t[sel].max()), 2)]
     if (ev == 80).any():
         out["combine_start_us"] = round(float(t[ev == 80].max()), 2)
     if (ev == 81).any():
         out["combine_end_us"] = round(float(t[ev == 81].max()), 2)
     out["kernel_span_us"] = float(t[ev == 5].max())
     out["cta_start_spread_us"] = float(t[ev == 0].max())
+    out["cta_start_pct"] = [round(float(x), 2) for x in np.percentile(t[ev == 0], [0, 50, 90, 95, 100])]
     out["gather_done_us"] = ([float(t[ev == 1].min()), float(t[ev == 1].max())]
                              if (ev == 1).any() else None)
     out["first_dequeue_us"] = float(t[ev == 2].min())
