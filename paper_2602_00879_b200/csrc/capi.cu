@@ -954,6 +954,14 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   if (kb == 4 && 2 * (4 * kATile + 4 * a.b_rows * 128) + 8192 > kSmemLimit - 256) kb = 2;
   if (kb == 4 && (d % (4 * kBK) || kdim_b % (4 * kBK))) kb = 2;
   a.kb = kb;
+  // dense mode: phase-B units of two d tiles that share one H stream (the
+  // activations count against each SM's ~50 GB/s ingress like the weights);
+  // the queue's last pairs run as single tiles (DESMOE_FFN_PAIRB=0 disables,
+  // DESMOE_FFN_SPLIT = how many pairs are split)
+  a.pair_b = dense && (d / kBM) % 2 == 0 && !std::getenv("DESMOE_FFN_PAIRB0") ? 1 : 0;
+  if (const char* pv = std::getenv("DESMOE_FFN_PAIRB")) a.pair_b = a.pair_b && std::atoi(pv) != 0;
+  a.split_b = c->num_sms / 2;
+  if (const char* sv = std::getenv("DESMOE_FFN_SPLIT")) a.split_b = std::max(0, std::atoi(sv));
   const int stage_bytes = kb * kATile + kb * a.b_rows * 128;
   const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
                     4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;

@@ -63,24 +63,49 @@ struct Tables {
 struct UnitInfo {
   int phase;  // 0 = A (gate/up), 1 = B (down / linear)
   int expert, tile, brow, count;
+  int nt;     // row tiles: 2 = a phase-B pair (tiles tile, tile + 1) sharing the activations
 };
+
+// Queue position -> (phase, list index, first tile, tiles). Phase A units
+// first (expert-major), then phase B: pw tiles per unit (pw = 2: pairs that
+// read the expert's H once for both tiles), the last nBs pairs split into
+// single tiles so the queue drains on small units.
+struct UnitPos {
+  int phase, ei, tile, nt;
+};
+__device__ inline UnitPos unit_pos(int u, int nA, int nBp, int tilesA, int tilesB, int pw) {
+  UnitPos r;
+  r.nt = 1;
+  if (u < nA) {
+    r.phase = 0;
+    r.ei = u / tilesA;
+    r.tile = u - r.ei * tilesA;
+    return r;
+  }
+  const int b = u - nA;
+  int tb;  // first tile in the flat phase-B tile order
+  if (b < nBp) {
+    tb = b * pw;
+    r.nt = pw;
+  } else {
+    tb = nBp * pw + (b - nBp);
+  }
+  r.phase = 1;
+  r.ei = tb / tilesB;
+  r.tile = tb - r.ei * tilesB;
+  return r;
+}
 
 // dense: every unit covers all n_tok tokens; row block = expert id x n_tok
 // (t.offset holds the expert id)
-__device__ inline UnitInfo decode(int u, int nA, int tilesA, int tilesB, const Tables& t,
-                                  bool dense, int n_tok) {
+__device__ inline UnitInfo decode(int u, int nA, int nBp, int tilesA, int tilesB, int pw,
+                                  const Tables& t, bool dense, int n_tok) {
   UnitInfo r;
-  int ei;
-  if (u < nA) {
-    r.phase = 0;
-    ei = u / tilesA;
-    r.tile = u - ei * tilesA;
-  } else {
-    u -= nA;
-    r.phase = 1;
-    ei = u / tilesB;
-    r.tile = u - ei * tilesB;
-  }
+  const UnitPos p = unit_pos(u, nA, nBp, tilesA, tilesB, pw);
+  const int ei = p.ei;
+  r.phase = p.phase;
+  r.tile = p.tile;
+  r.nt = p.nt;
   r.expert = t.active[ei];
   if (dense) {
     r.brow = t.offset[ei] * n_tok;
@@ -236,6 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tilesA = f / kHalf, tilesB = d / kBM;
   const int ksA = d / (KB * kBK);               // k-steps: KB K blocks each
   const int ksB = (swiglu ? f : d) / (KB * kBK);
+  constexpr int KH = KB / 2;  // a phase-B pair stage: KH K blocks of each tile (+ KH boxes)
+  const int pw = a.pair_b ? 2 : 1;
   int pre_u = -1, pre_ks = 0;  // early mode: unit claimed and k-steps issued before the prologue
   if (a.early && warp == 0) {
     // the published expert list (coreset / union) -> the unit list; claim
@@ -278,14 +305,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       if (a.trace) s_pts[6] = gtime();  // list words loaded
       s_upub = u;
-      const int n_units0 = (swiglu ? u * tilesA : 0) + u * tilesB;
-      if (u0 < n_units0) {
-        pre_u = u0;
-        const int nA0 = swiglu ? u * tilesA : 0;
-        const bool phaseA = u0 < nA0;
-        const int ei = phaseA ? u0 / tilesA : (u0 - nA0) / tilesB;
-        const int tile = phaseA ? u0 - ei * tilesA : (u0 - nA0) - ei * tilesB;
-        const int el = pubm[ei] - lo;
+      const int nA0 = swiglu ? u * tilesA : 0;
+      const int nBs0 = pw == 2 ? min(a.split_b, u * (tilesB / 2)) : 0;
+      const int nBp0 = u * (tilesB / pw) - nBs0;
+      const int n_units0 = nA0 + nBp0 + pw * nBs0;
+      if (u0 < n_units0) pre_u = u0;
+      const UnitPos p0 = unit_pos(u0, nA0, nBp0, tilesA, tilesB, pw);
+      if (u0 < n_units0 && p0.nt == 1) {  // (a first pair streams from the main loop)
+        const bool phaseA = p0.phase == 0;
+        const int tile = p0.tile;
+        const int el = pubm[p0.ei] - lo;
         const int ksteps = phaseA ? ksA : ksB;
         const uint64_t pol_w = l2_policy_evict_first();
         const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
@@ -496,7 +525,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int nA = swiglu ? U * tilesA : 0;
-  const int n_units = nA + U * tilesB;
+  const int nBs = pw == 2 ? min(a.split_b, U * (tilesB / 2)) : 0;  // pairs run as single tiles
+  const int nBp = U * (tilesB / pw) - nBs;
+  const int n_units = nA + nBp + pw * nBs;
 
   if (warp == 0) {
     // ============ scheduler + weight producer ============
@@ -513,9 +544,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&qfull[q]);
         if (uu < 0) break;
         trace_put(tc, 2, uu);
-        const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
+        const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
-        const int ksteps = phaseA ? ksA : ksB;
+        const bool pair = ui.nt == 2;
+        const int ksteps = phaseA ? ksA : (pair ? 2 * ksB : ksB);
         const int ks0 = pre ? pre_ks : 0;
         it += ks0;
         for (int ks = ks0; ks < ksteps; ++ks, ++it) {
@@ -526,6 +558,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           // packed weights: tile-contiguous 16 KB blocks in (expert, row tile,
           // K block) order, so a unit streams one contiguous region
           const int el = ui.expert - lo;  // packed weights hold the owned experts only
+          if (pair) {  // KH blocks of each of the two tiles
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt) {
+              const int tile0 = (el * tilesB + ui.tile + tt) * (KB * ksB) + KH * ks;
+#pragma unroll
+              for (int j = 0; j < KH; ++j)
+                tma_load_3d(st + (tt * KH + j) * kATile, &w_c, &full[s], 0, 0, tile0 + j, pol_w);
+            }
+            continue;
+          }
           const int tile0 = phaseA ? (el * tilesA + ui.tile) * (KB * ksA) + KB * ks
                                    : (el * tilesB + ui.tile) * (KB * ksB) + KB * ks;
           const CUtensorMap* wmap = phaseA ? &w_a : &w_c;
@@ -547,13 +589,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int uu = unit_q[q];
         mbar_arrive(&qempty[q]);
         if (uu < 0) break;
-        const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
+        const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
         const bool from_x = phaseA || !swiglu;
         const int bi = box_for(ui.count);
         const uint32_t box_bytes = (16u << bi) * 128u;
         const BoxMaps& acts = from_x ? xp_maps : h_maps;
-        const int ksteps = phaseA ? ksA : ksB;
+        const int nb = ui.nt == 2 ? KH : KB;  // activation boxes per k-step
+        const int ksteps = phaseA ? ksA : (ui.nt == 2 ? 2 * ksB : ksB);
         if (from_x && !x_seen && ui.count > 0 && !dense) {
           while (ld_acquire(x_ready) < a.gather_ctas) {
           }
@@ -570,8 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (!from_x) {
             // H columns [128 ks, 128 ks + 128) = phase-A tiles 2ks, 2ks+1
-            for (int h = 0; h < KB; ++h) {
-              const int* flag = &h_ready[ui.expert * tilesA + KB * ks + h];
+            for (int h = 0; h < nb; ++h) {
+              const int* flag = &h_ready[ui.expert * tilesA + nb * ks + h];
               if (ld_acquire(flag) == 0) {
                 while (ld_acquire(flag) == 0) {
                 }
@@ -581,12 +624,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_global();
           }
           unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes + KB * kATile;
-          mbar_arrive_expect_tx(&full[s], KB * box_bytes);
+          mbar_arrive_expect_tx(&full[s], nb * box_bytes);
           const int row = dense && from_x ? 0 : ui.brow;  // dense: X itself (all tokens)
 #pragma unroll
           for (int j = 0; j < KB; ++j)
-            tma_load_2d(st + j * b_box_bytes, &acts.map[bi], &full[s], (KB * ks + j) * kBK, row,
-                        pol_x);
+            if (j < nb)
+              tma_load_2d(st + j * b_box_bytes, &acts.map[bi], &full[s], (nb * ks + j) * kBK, row,
+                          pol_x);
         }
       }
     }
@@ -600,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[q]);
       if (uu < 0) break;
-      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
+      const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
@@ -609,7 +653,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t d_acc = tmem_base + buf * 256u;
-      const int ksteps = phaseA ? ksA : ksB;
+      const bool pair = ui.nt == 2;
+      const int ksteps = phaseA ? ksA : (pair ? 2 * ksB : ksB);
       for (int ks = 0; ks < ksteps; ++ks, ++it) {
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
@@ -622,13 +667,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
           const uint32_t b0 = a0 + KB * kATile;
+          if (pair) {
+            // tile tt: its KH blocks x the KH shared boxes -> columns [128 tt, 128 tt + n_mma)
+            // (pairs only in dense mode: n_mma <= 64)
 #pragma unroll
-          for (int h = 0; h < KB; ++h)
+            for (int tt = 0; tt < 2; ++tt)
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-              tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + h * kATile + kk * 32),
-                          sw128_kmajor_desc(b0 + h * b_box_bytes + kk * 32), idesc,
-                          (ks > 0 || h > 0 || kk > 0) ? 1u : 0u);
+              for (int h = 0; h < KH; ++h)
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                  tc_mma_bf16(d_acc + tt * 128u,
+                              sw128_kmajor_desc(a0 + (tt * KH + h) * kATile + kk * 32),
+                              sw128_kmajor_desc(b0 + h * b_box_bytes + kk * 32), idesc,
+                              (ks > 0 || h > 0 || kk > 0) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int h = 0; h < KB; ++h)
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk)
+                tc_mma_bf16(d_acc, sw128_kmajor_desc(a0 + h * kATile + kk * 32),
+                            sw128_kmajor_desc(b0 + h * b_box_bytes + kk * 32), idesc,
+                            (ks > 0 || h > 0 || kk > 0) ? 1u : 0u);
+          }
           tc_commit(&empty[s]);
           if (ks == ksteps - 1) tc_commit(&tfull[buf]);
         }
@@ -680,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       if (etid == 0) mbar_arrive(&qempty[q]);
       if (uu < 0) break;
-      const UnitInfo ui = decode(uu, nA, tilesA, tilesB, t, dense, n_tok);
+      const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t buf = nunit & 1u;
@@ -714,10 +774,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1, 128);
         }
       } else if (a.world <= 1) {
-        float* yrow = a.y_slot + static_cast<size_t>(ui.brow) * d + ui.tile * kBM + r;
+        for (int tt = 0; tt < ui.nt; ++tt) {
+        float* yrow = a.y_slot + static_cast<size_t>(ui.brow) * d + (ui.tile + tt) * kBM + r;
         for (int c0 = 0; c0 < n_mma; c0 += 16) {
           float v[16];
-          tmem_ld16(lane_base + c0, v);
+          tmem_ld16(lane_base + tt * 128u + c0, v);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int col = c0 + j;
@@ -726,13 +787,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                   dense ? v[j] : v[j] * t.slot_gate[ui.brow + col];
           }
         }
+        }  // tiles of the unit
       } else {
         // expert parallel: push the gate-scaled rows straight into every
         // rank's slot buffer (own + NVLink peers) while later tiles stream
-        const size_t off = ep_half + static_cast<size_t>(ui.brow) * d + ui.tile * kBM + r;
+        for (int tt = 0; tt < ui.nt; ++tt) {
+        const size_t off =
+            ep_half + static_cast<size_t>(ui.brow) * d + (ui.tile + tt) * kBM + r;
         for (int c0 = 0; c0 < n_mma; c0 += 16) {
           float v[16];
-          tmem_ld16(lane_base + c0, v);
+          tmem_ld16(lane_base + tt * 128u + c0, v);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int col = c0 + j;
@@ -743,6 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        }  // tiles of the unit
       }
       tc_fence_before();
       __syncwarp();

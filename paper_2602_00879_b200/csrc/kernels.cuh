@@ -227,6 +227,8 @@ struct FfnArgs {
   int gather_ctas;           // CTAs that gather x rows (and the x_ready target)
   int dense;                 // every published expert x every token (small blocks)
   int kb;                    // 64-wide K blocks per ring stage: 4 when d, F allow, else 2
+  int pair_b;                // dense mode: phase-B units of two d tiles sharing one H stream
+  int split_b;               // the queue's last phase-B pairs run as single-tile units
 };
 
 // Ordered combine arguments (combine_slots_kernel).
