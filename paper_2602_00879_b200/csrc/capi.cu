@@ -962,6 +962,12 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   if (const char* pv = std::getenv("DESMOE_FFN_PAIRB")) a.pair_b = a.pair_b && std::atoi(pv) != 0;
   a.split_b = c->num_sms / 2;
   if (const char* sv = std::getenv("DESMOE_FFN_SPLIT")) a.split_b = std::max(0, std::atoi(sv));
+  // phase A likewise: two F tiles sharing one X stream (X is 128 KB per
+  // 512 KB tile at N = 32, d = 2048), the last pairs split
+  a.pair_a = a.pair_b && ex->kind == DESMOE_FFN_SWIGLU && (f / 64) % 2 == 0 ? 1 : 0;
+  if (const char* pv = std::getenv("DESMOE_FFN_PAIRA")) a.pair_a = a.pair_a && std::atoi(pv) != 0;
+  a.split_a = c->num_sms;
+  if (const char* sv = std::getenv("DESMOE_FFN_SPLITA")) a.split_a = std::max(0, std::atoi(sv));
   const int stage_bytes = kb * kATile + kb * a.b_rows * 128;
   const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
                     4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;

@@ -73,13 +73,26 @@ struct UnitInfo {
 struct UnitPos {
   int phase, ei, tile, nt;
 };
-__device__ inline UnitPos unit_pos(int u, int nA, int nBp, int tilesA, int tilesB, int pw) {
+// Phase A the same way: pa tiles per unit (two F tiles sharing the X stream),
+// the last A pairs split; nA = phase-A units, nAp of them pairs.
+struct UnitMap {
+  int nA, nAp, pa, nBp, pw, total;
+};
+__device__ inline UnitPos unit_pos(int u, const UnitMap& q, int tilesA, int tilesB) {
+  const int nA = q.nA, nBp = q.nBp, pw = q.pw;
   UnitPos r;
   r.nt = 1;
   if (u < nA) {
+    int ta;
+    if (u < q.nAp) {
+      ta = u * q.pa;
+      r.nt = q.pa;
+    } else {
+      ta = q.nAp * q.pa + (u - q.nAp);
+    }
     r.phase = 0;
-    r.ei = u / tilesA;
-    r.tile = u - r.ei * tilesA;
+    r.ei = ta / tilesA;
+    r.tile = ta - r.ei * tilesA;
     return r;
   }
   const int b = u - nA;
@@ -98,10 +111,10 @@ __device__ inline UnitPos unit_pos(int u, int nA, int nBp, int tilesA, int tiles
 
 // dense: every unit covers all n_tok tokens; row block = expert id x n_tok
 // (t.offset holds the expert id)
-__device__ inline UnitInfo decode(int u, int nA, int nBp, int tilesA, int tilesB, int pw,
+__device__ inline UnitInfo decode(int u, const UnitMap& q, int tilesA, int tilesB,
                                   const Tables& t, bool dense, int n_tok) {
   UnitInfo r;
-  const UnitPos p = unit_pos(u, nA, nBp, tilesA, tilesB, pw);
+  const UnitPos p = unit_pos(u, q, tilesA, tilesB);
   const int ei = p.ei;
   r.phase = p.phase;
   r.tile = p.tile;
@@ -263,6 +276,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ksB = (swiglu ? f : d) / (KB * kBK);
   constexpr int KH = KB / 2;  // a phase-B pair stage: KH K blocks of each tile (+ KH boxes)
   const int pw = a.pair_b ? 2 : 1;
+  const int pa = a.pair_a && swiglu ? 2 : 1;
+  // the unit list for U owned experts
+  auto unit_map = [&](int u_) {
+    UnitMap q;
+    const int nAs = pa == 2 ? min(a.split_a, u_ * (tilesA / 2)) : 0;
+    q.pa = pa;
+    q.nAp = swiglu ? u_ * (tilesA / pa) - nAs : 0;
+    q.nA = q.nAp + pa * nAs;
+    const int nBs = pw == 2 ? min(a.split_b, u_ * (tilesB / 2)) : 0;
+    q.pw = pw;
+    q.nBp = u_ * (tilesB / pw) - nBs;
+    q.total = q.nA + q.nBp + pw * nBs;
+    return q;
+  };
   int pre_u = -1, pre_ks = 0;  // early mode: unit claimed and k-steps issued before the prologue
   if (a.early && warp == 0) {
     // the published expert list (coreset / union) -> the unit list; claim
@@ -305,12 +332,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       if (a.trace) s_pts[6] = gtime();  // list words loaded
       s_upub = u;
-      const int nA0 = swiglu ? u * tilesA : 0;
-      const int nBs0 = pw == 2 ? min(a.split_b, u * (tilesB / 2)) : 0;
-      const int nBp0 = u * (tilesB / pw) - nBs0;
-      const int n_units0 = nA0 + nBp0 + pw * nBs0;
+      const UnitMap q0 = unit_map(u);
+      const int n_units0 = q0.total;
       if (u0 < n_units0) pre_u = u0;
-      const UnitPos p0 = unit_pos(u0, nA0, nBp0, tilesA, tilesB, pw);
+      const UnitPos p0 = unit_pos(u0, q0, tilesA, tilesB);
       if (u0 < n_units0 && p0.nt == 1) {  // (a first pair streams from the main loop)
         const bool phaseA = p0.phase == 0;
         const int tile = p0.tile;
@@ -524,10 +549,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   const uint32_t tmem_base = *tmem_slot;
 
-  const int nA = swiglu ? U * tilesA : 0;
-  const int nBs = pw == 2 ? min(a.split_b, U * (tilesB / 2)) : 0;  // pairs run as single tiles
-  const int nBp = U * (tilesB / pw) - nBs;
-  const int n_units = nA + nBp + pw * nBs;
+  const UnitMap qm = unit_map(U);
+  const int n_units = qm.total;
 
   if (warp == 0) {
     // ============ scheduler + weight producer ============
@@ -544,10 +567,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&qfull[q]);
         if (uu < 0) break;
         trace_put(tc, 2, uu);
-        const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
+        const UnitInfo ui = decode(uu, qm, tilesA, tilesB, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
         const bool pair = ui.nt == 2;
-        const int ksteps = phaseA ? ksA : (pair ? 2 * ksB : ksB);
+        const int ksteps = (phaseA ? ksA : ksB) * ui.nt;
         const int ks0 = pre ? pre_ks : 0;
         it += ks0;
         for (int ks = ks0; ks < ksteps; ++ks, ++it) {
@@ -559,12 +582,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           // K block) order, so a unit streams one contiguous region
           const int el = ui.expert - lo;  // packed weights hold the owned experts only
           if (pair) {  // KH blocks of each of the two tiles
+            const CUtensorMap* pmap = phaseA ? &w_a : &w_c;
 #pragma unroll
             for (int tt = 0; tt < 2; ++tt) {
-              const int tile0 = (el * tilesB + ui.tile + tt) * (KB * ksB) + KH * ks;
+              const int tile0 = phaseA ? (el * tilesA + ui.tile + tt) * (KB * ksA) + KH * ks
+                                       : (el * tilesB + ui.tile + tt) * (KB * ksB) + KH * ks;
 #pragma unroll
               for (int j = 0; j < KH; ++j)
-                tma_load_3d(st + (tt * KH + j) * kATile, &w_c, &full[s], 0, 0, tile0 + j, pol_w);
+                tma_load_3d(st + (tt * KH + j) * kATile, pmap, &full[s], 0, 0, tile0 + j, pol_w);
             }
             continue;
           }
@@ -589,14 +614,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int uu = unit_q[q];
         mbar_arrive(&qempty[q]);
         if (uu < 0) break;
-        const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
+        const UnitInfo ui = decode(uu, qm, tilesA, tilesB, t, dense, n_tok);
         const bool phaseA = ui.phase == 0;
         const bool from_x = phaseA || !swiglu;
         const int bi = box_for(ui.count);
         const uint32_t box_bytes = (16u << bi) * 128u;
         const BoxMaps& acts = from_x ? xp_maps : h_maps;
         const int nb = ui.nt == 2 ? KH : KB;  // activation boxes per k-step
-        const int ksteps = phaseA ? ksA : (ui.nt == 2 ? 2 * ksB : ksB);
+        const int ksteps = (phaseA ? ksA : ksB) * ui.nt;
         if (from_x && !x_seen && ui.count > 0 && !dense) {
           while (ld_acquire(x_ready) < a.gather_ctas) {
           }
@@ -644,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[q]);
       if (uu < 0) break;
-      const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
+      const UnitInfo ui = decode(uu, qm, tilesA, tilesB, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
@@ -654,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t d_acc = tmem_base + buf * 256u;
       const bool pair = ui.nt == 2;
-      const int ksteps = phaseA ? ksA : (pair ? 2 * ksB : ksB);
+      const int ksteps = (phaseA ? ksA : ksB) * ui.nt;
       for (int ks = 0; ks < ksteps; ++ks, ++it) {
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
@@ -740,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       if (etid == 0) mbar_arrive(&qempty[q]);
       if (uu < 0) break;
-      const UnitInfo ui = decode(uu, nA, nBp, tilesA, tilesB, pw, t, dense, n_tok);
+      const UnitInfo ui = decode(uu, qm, tilesA, tilesB, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
       const uint32_t buf = nunit & 1u;
@@ -752,11 +777,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // lanes 0-63: G, lanes 64-127: U of F columns tile*64 + (r mod 64)
         const bool is_g = r < kHalf;
         const int rr = r & (kHalf - 1);
+        for (int tt = 0; tt < ui.nt; ++tt) {
         __nv_bfloat16* hrow =
-            a.h_perm + static_cast<size_t>(ui.brow) * f + ui.tile * kHalf + rr;
+            a.h_perm + static_cast<size_t>(ui.brow) * f + (ui.tile + tt) * kHalf + rr;
         for (int c0 = 0; c0 < n_mma; c0 += 16) {
           float v[16];
-          tmem_ld16(lane_base + c0, v);
+          tmem_ld16(lane_base + tt * 128u + c0, v);
           if (!is_g) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) xchg[j * kHalf + rr] = v[j];
@@ -773,6 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           named_bar_sync(1, 128);
         }
+        }  // tiles of the unit
       } else if (a.world <= 1) {
         for (int tt = 0; tt < ui.nt; ++tt) {
         float* yrow = a.y_slot + static_cast<size_t>(ui.brow) * d + (ui.tile + tt) * kBM + r;
@@ -815,7 +842,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (phaseA) {
         named_bar_sync(1, 128);
         if (etid == 0)  // the barrier orders every epilogue thread's H stores before this
-          atomic_add_release(&h_ready[ui.expert * tilesA + ui.tile], 1);  // cumulative release
+          for (int tt = 0; tt < ui.nt; ++tt)  // cumulative release
+            atomic_add_release(&h_ready[ui.expert * tilesA + ui.tile + tt], 1);
       }
       if (etid == 0) trace_put(tc, 3, uu);
       ++nunit;

@@ -229,6 +229,7 @@ struct FfnArgs {
   int kb;                    // 64-wide K blocks per ring stage: 4 when d, F allow, else 2
   int pair_b;                // dense mode: phase-B units of two d tiles sharing one H stream
   int split_b;               // the queue's last phase-B pairs run as single-tile units
+  int pair_a, split_a;       // the same for phase A (two F tiles sharing one X stream)
 };
 
 // Ordered combine arguments (combine_slots_kernel).
