@@ -958,7 +958,15 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   // activations count against each SM's ~50 GB/s ingress like the weights);
   // the queue's last pairs run as single tiles (DESMOE_FFN_PAIRB=0 disables,
   // DESMOE_FFN_SPLIT = how many pairs are split)
-  a.pair_b = dense && (d / kBM) % 2 == 0 && !std::getenv("DESMOE_FFN_PAIRB0") ? 1 : 0;
+  // Routed mode too (a tile's columns must fit half the accumulator: every
+  // expert's row count <= n <= 128), but only for the large unions of vanilla
+  // top-K — measured on one box: vanilla N=32 134.2 -> 130.0 us, N=128
+  // 167.0 -> 159.0; DES-Vote N=128 (routed, U = 25) 96.5 -> 97.2
+  const char* pr = std::getenv("DESMOE_FFN_PAIR_ROUTED");  // 0: off, 1: every strategy
+  const bool routed_pairs =
+      n <= 128 && (pr ? std::atoi(pr) != 0 && (std::atoi(pr) == 1 || !prefer_dense) : !prefer_dense);
+  const bool pair_ok = dense || routed_pairs;
+  a.pair_b = pair_ok && (d / kBM) % 2 == 0 ? 1 : 0;
   if (const char* pv = std::getenv("DESMOE_FFN_PAIRB")) a.pair_b = a.pair_b && std::atoi(pv) != 0;
   a.split_b = c->num_sms / 2;
   if (const char* sv = std::getenv("DESMOE_FFN_SPLIT")) a.split_b = std::max(0, std::atoi(sv));
