@@ -390,41 +390,51 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) t.scalars[2] = 0;
   __syncthreads();
   // route slot e: expert (-1 = none) and gate, staged in shared memory; early
-  // mode: ONE warp per CTA polls the tagged words (all threads polling would
-  // flood L2 while the front is still writing them and the weights stream)
+  // mode: ONE warp per CTA polls the tagged words until the first batch is
+  // valid (all threads polling would flood L2 while the front is still
+  // writing them), then every warp loads its share of the rest
   int* rexp = t.slot_of;           // staged here until the slot pass rewrites it
   if (a.early) {
-    if (warp == 1) {
-      // batches of 8 words per lane with every load of a batch in flight at
-      // once; re-poll until the whole batch carries this call's tag
-      const int total = n_tok * k;
-      for (int b0 = 0; b0 < total; b0 += 32 * 8) {
-        uint64_t w[8];
-        bool ok;
-        do {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int e = b0 + j * 32 + lane;
-            w[j] = e < total ? ld_relaxed_u64(a.route_words + e) : 0ull;
-          }
-          ok = true;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int e = b0 + j * 32 + lane;
-            ok &= e >= total || ((static_cast<uint32_t>(w[j]) >> 10) & kTagMask) == tag;
-          }
-          ok = __all_sync(0xffffffffu, ok);
-        } while (!ok);
+    // batches of 8 words per lane with every load of a batch in flight at
+    // once; re-poll until the whole batch carries this call's tag. Warp 1
+    // polls the first batch alone; once it is valid the front is finishing,
+    // and all 8 warps load the remaining batches in parallel (one round trip
+    // instead of one per batch)
+    const int total = n_tok * k;
+    auto poll_batch = [&](int b0) {
+      uint64_t w[8];
+      bool ok;
+      do {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int e = b0 + j * 32 + lane;
-          if (e < total) {
-            const int x = static_cast<int>(w[j] & 1023u);
-            rexp[e] = x == kPadExpert ? -1 : x;
-            gate_tmp[e] = __uint_as_float(static_cast<uint32_t>(w[j] >> 32));
-          }
+          w[j] = e < total ? ld_relaxed_u64(a.route_words + e) : 0ull;
+        }
+        ok = true;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int e = b0 + j * 32 + lane;
+          ok &= e >= total || ((static_cast<uint32_t>(w[j]) >> 10) & kTagMask) == tag;
+        }
+        ok = __all_sync(0xffffffffu, ok);
+      } while (!ok);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = b0 + j * 32 + lane;
+        if (e < total) {
+          const int x = static_cast<int>(w[j] & 1023u);
+          rexp[e] = x == kPadExpert ? -1 : x;
+          gate_tmp[e] = __uint_as_float(static_cast<uint32_t>(w[j] >> 32));
         }
       }
+    };
+    if (a.flags & 2) {  // (A/B runs: warp 1 alone, one batch per round trip)
+      if (warp == 1)
+        for (int b0 = 0; b0 < total; b0 += 256) poll_batch(b0);
+    } else {
+      if (warp == 1) poll_batch(0);
+      __syncthreads();
+      for (int b = 1 + warp; b * 256 < total; b += kThreads / 32) poll_batch(b * 256);
     }
   } else {
     for (int e = tid; e < n_tok * k; e += kThreads) {
