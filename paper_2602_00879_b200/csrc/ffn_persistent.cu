@@ -179,6 +179,40 @@ __device__ int block_exclusive_scan(int* v, int n, int* warp_sums) {
   return total;
 }
 
+// Routed mode: one batch of 256 tagged route words (8 per lane, all in
+// flight at once), re-polled until every word carries this call's tag, then
+// staged as (expert or -1, gate). Out of line: the dense path's code stays
+// compact (its instruction fetches are cold after an L2 flush).
+__device__ __noinline__ void poll_route_batch(const uint64_t* route_words, int total, int b0,
+                                              uint32_t tag, int* rexp, float* gate_tmp) {
+  const int lane = threadIdx.x & 31;
+  uint64_t w[8];
+  bool ok;
+  do {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = b0 + j * 32 + lane;
+      w[j] = e < total ? ld_relaxed_u64(route_words + e) : 0ull;
+    }
+    ok = true;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = b0 + j * 32 + lane;
+      ok &= e >= total || ((static_cast<uint32_t>(w[j]) >> 10) & kTagMask) == tag;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+  } while (!ok);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int e = b0 + j * 32 + lane;
+    if (e < total) {
+      const int x = static_cast<int>(w[j] & 1023u);
+      rexp[e] = x == kPadExpert ? -1 : x;
+      gate_tmp[e] = __uint_as_float(static_cast<uint32_t>(w[j] >> 32));
+    }
+  }
+}
+
 }  // namespace
 
 template <int KB>
@@ -402,31 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // instead of one per batch)
     const int total = n_tok * k;
     auto poll_batch = [&](int b0) {
-      uint64_t w[8];
-      bool ok;
-      do {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int e = b0 + j * 32 + lane;
-          w[j] = e < total ? ld_relaxed_u64(a.route_words + e) : 0ull;
-        }
-        ok = true;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int e = b0 + j * 32 + lane;
-          ok &= e >= total || ((static_cast<uint32_t>(w[j]) >> 10) & kTagMask) == tag;
-        }
-        ok = __all_sync(0xffffffffu, ok);
-      } while (!ok);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int e = b0 + j * 32 + lane;
-        if (e < total) {
-          const int x = static_cast<int>(w[j] & 1023u);
-          rexp[e] = x == kPadExpert ? -1 : x;
-          gate_tmp[e] = __uint_as_float(static_cast<uint32_t>(w[j] >> 32));
-        }
-      }
+      poll_route_batch(a.route_words, total, b0, tag, rexp, gate_tmp);
     };
     if (a.flags & 2) {  // (A/B runs: warp 1 alone, one batch per round trip)
       if (warp == 1)
