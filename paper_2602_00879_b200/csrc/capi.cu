@@ -1020,8 +1020,11 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   mark(c, st);  // profiling only: expert FFN | (EP wait +) combine
   // ordered combine, programmatically serialised behind the FFN kernel
   cudaLaunchConfig_t cc{};
-  cc.gridDim = dim3((n * (d / 4) + 255) / 256);
-  cc.blockDim = dim3(256);
+  int cthreads = 256;  // (DESMOE_COMBINE_THREADS: 128 spreads the row loads over twice the SMs)
+  if (const char* ct = std::getenv("DESMOE_COMBINE_THREADS"))
+    cthreads = std::atoi(ct) == 128 ? 128 : (std::atoi(ct) == 64 ? 64 : 256);
+  cc.gridDim = dim3((n * (d / 4) + cthreads - 1) / cthreads);
+  cc.blockDim = dim3(cthreads);
   cc.stream = st;
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
