@@ -92,6 +92,7 @@ def test_moe_forward_facade(ref):
     (16, 256, 256, 16, "vanilla"),
     (64, 512, 512, 32, "vote"),
     (64, 2048, 1024, 32, "vote"),
+    (64, 2048, 1024, 32, "vanilla"),  # routed mode with pair units
     (256, 1024, 512, 64, "seq"),
     (128, 512, 768, 256, "vote"),
     (256, 2048, 512, 256, "vote"),   # token-split router GEMM at the C3 shape
@@ -134,6 +135,19 @@ def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
     scale = np.abs(want).max()
     assert np.abs(got - want).max() <= 2e-2 * scale
     assert np.abs(got - want).mean() <= 2e-3 * scale
+
+
+@pytest.mark.parametrize("m,d,f,n,strategy", [
+    (64, 512, 512, 32, "vote"),       # dense mode
+    (16, 256, 256, 16, "vanilla"),    # dense mode, vanilla
+    (64, 512, 512, 48, "vanilla"),    # routed mode
+])
+def test_pair_units_without_split(ref, port, monkeypatch, m, d, f, n, strategy):
+    """Every phase-A / phase-B unit a pair (no single-tile tail), at shapes
+    where the default split would leave none."""
+    monkeypatch.setenv("DESMOE_FFN_SPLIT", "0")
+    monkeypatch.setenv("DESMOE_FFN_SPLITA", "0")
+    test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy)
 
 
 def test_layer_host_entry_matches_device_entry():
