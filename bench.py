@@ -118,6 +118,21 @@ def dist_env():
     return ws, rank, local
 
 
+def spawn_ranks(gpus):
+    """`bench.py --gpus N` without a launcher: run N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1 and return its exit status."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        raise SystemExit(rc)
+
+
 def run_reference(args, cfg):
     """Reference arm: the reference's own CPU layer (oracle/_ref)."""
     ws, rank, _ = dist_env()
@@ -142,9 +157,9 @@ def run_reference(args, cfg):
               f"all {n} tokens + moe_forward (reference linear {d}x{d} fp64 experts) on "
               f"{args.ref_ffn_tokens or n} tokens scaled to {n}; gen_trace shared_bias rho="
               f"{cfg['rho']} logits")
-    line = {"metric": METRIC, "value": round(v, 3), "unit": "us/block", "n_gpus": ws,
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "us/block", "n_gpus": max(ws, args.gpus),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v / 1e3, 6),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": config_dict(cfg, "vote"),
             "cpu_baseline": {"value": round(v, 3), "unit": "us/block", "cores": threads,
@@ -192,6 +207,13 @@ def main():
         cfg["block"] = args.block
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        # (the driver may also launch it that way itself)
+        return spawn_ranks(args.gpus)
+    ws = dist_env()[0]
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
 
     import ctypes as C
     import numpy as np
@@ -392,7 +414,7 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "us/block", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1e3, 6),
-        "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
+        "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, rho-correlated hidden states)",
         "config": config_dict(cfg, "vote", ws),

@@ -885,13 +885,56 @@ int launch_router_tiles(const CUtensorMap& wa, const BoxMaps& acts, TileArgs a, 
   return DESMOE_OK;
 }
 
+// Launch plan of the persistent expert FFN: ring stage size (kb K blocks of
+// 64), depth and dynamic shared memory. Every shape check the FFN launch
+// makes lives here, so the layer entry can reject a block BEFORE the front
+// kernel publishes anything (a published list / route with no FFN + combine
+// behind it would be taken as valid by the next call's early-mode FFN).
+struct FfnPlan {
+  int kb = 2, stages = 2, b_rows = 16;
+  size_t smem = 0;
+};
+
+int ffn_plan(const desmoe_experts* ex, int n, int k, FfnPlan* p) {
+  const int m = ex->m, d = ex->d, f = ex->f;
+  if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
+  p->b_rows = b_rows_for(n);
+  // ring stage = kb K blocks of 64: 4 (fewer, larger stages; measured on one
+  // box: vanilla 131.3 -> 129.1 us, DES-Vote 73.8 -> 73.7) when both GEMM K
+  // dims divide and two stages fit, else 2
+  const int kdim_b = ex->kind == DESMOE_FFN_SWIGLU ? f : d;
+  int kb = d % (4 * kBK) == 0 && kdim_b % (4 * kBK) == 0 ? 4 : 2;
+  if (const char* kv = std::getenv("DESMOE_FFN_KB")) kb = std::atoi(kv) == 4 ? 4 : 2;
+  if (kb == 4 && 2 * (4 * kATile + 4 * p->b_rows * 128) + 8192 > kSmemLimit - 256) kb = 2;
+  if (kb == 4 && (d % (4 * kBK) || kdim_b % (4 * kBK))) kb = 2;
+  p->kb = kb;
+  const int stage_bytes = kb * kATile + kb * p->b_rows * 128;
+  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
+                    4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
+  int stages = (kSmemLimit - 256 - fixed) / stage_bytes;  // 256 B: the kernel's static smem
+  // deeper rings only lengthen the queues every other memory access waits
+  // behind: 128 KB of weights in flight per SM measured best (4 x 32 KB / 2 x 64 KB)
+  stages = std::max(2, std::min(stages, 8 / kb));
+  if (const char* sv = std::getenv("DESMOE_FFN_STAGES"))  // tuning experiments
+    stages = std::max(2, std::min(stages, std::atoi(sv)));
+  p->stages = stages;
+  if (4 * (m * ((n + 31) / 32) + 3 * m + n * k) > stage_bytes)
+    return fail(DESMOE_EINVAL, "expert FFN prologue scratch exceeds a pipeline stage");
+  p->smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
+  if (p->smem > static_cast<size_t>(kSmemLimit - 256))
+    return fail(DESMOE_EINVAL, "expert FFN shared-memory plan exceeds 227 KB");
+  return DESMOE_OK;
+}
+
 int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int k,
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
              const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false,
              bool after_front = false, __nv_bfloat16* y_bf16 = nullptr,
-             const void* resid = nullptr, bool prefer_dense = false) {
+             const void* resid = nullptr, bool prefer_dense = false, bool layer_path = false) {
   const int m = ex->m, d = ex->d, f = ex->f;
-  if (n > 256) return fail(DESMOE_EINVAL, "expert FFN supports up to 256 tokens per block");
+  FfnPlan plan;
+  int prc = ffn_plan(ex, n, k, &plan);
+  if (prc) return prc;
   const int words = ffn_counter_words(m, f);
   if (!counters_zeroed) DESMOE_CUDA(cudaMemsetAsync(ex->counters, 0, sizeof(int) * words, st));
   FfnArgs a{};
@@ -901,7 +944,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.m = m;
   a.d = d;
   a.f = f;
-  a.b_rows = b_rows_for(n);
+  a.b_rows = plan.b_rows;
   a.route_idx = route_idx;
   a.route_cnt = route_cnt;
   a.route_gate = route_gate;
@@ -945,14 +988,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
     }
     a.slot_stride = slot_stride;
   }
-  // ring stage = kb K blocks of 64: 4 (fewer, larger stages; measured on one
-  // box: vanilla 131.3 -> 129.1 us, DES-Vote 73.8 -> 73.7) when both GEMM K
-  // dims divide and two stages fit, else 2
-  const int kdim_b = ex->kind == DESMOE_FFN_SWIGLU ? f : d;
-  int kb = d % (4 * kBK) == 0 && kdim_b % (4 * kBK) == 0 ? 4 : 2;
-  if (const char* kv = std::getenv("DESMOE_FFN_KB")) kb = std::atoi(kv) == 4 ? 4 : 2;
-  if (kb == 4 && 2 * (4 * kATile + 4 * a.b_rows * 128) + 8192 > kSmemLimit - 256) kb = 2;
-  if (kb == 4 && (d % (4 * kBK) || kdim_b % (4 * kBK))) kb = 2;
+  const int kb = plan.kb;
   a.kb = kb;
   // dense mode: phase-B units of two d tiles that share one H stream (the
   // activations count against each SM's ~50 GB/s ingress like the weights);
@@ -960,11 +996,14 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   // DESMOE_FFN_SPLIT = how many pairs are split)
   // Routed mode too (a tile's columns must fit half the accumulator: every
   // expert's row count <= n <= 128), but only for the large unions of vanilla
-  // top-K — measured on one box: vanilla N=32 134.2 -> 130.0 us, N=128
-  // 167.0 -> 159.0; DES-Vote N=128 (routed, U = 25) 96.5 -> 97.2
+  // top-K on the layer path — measured on one box: vanilla N=32 134.2 -> 130.0
+  // us, N=128 167.0 -> 159.0; DES-Vote N=128 (routed, U = 25) 96.5 -> 97.2.
+  // The standalone FFN entry (desmoe_expert_ffn / moe_forward) keeps single
+  // tiles unless DESMOE_FFN_PAIR_ROUTED asks otherwise.
   const char* pr = std::getenv("DESMOE_FFN_PAIR_ROUTED");  // 0: off, 1: every strategy
   const bool routed_pairs =
-      n <= 128 && (pr ? std::atoi(pr) != 0 && (std::atoi(pr) == 1 || !prefer_dense) : !prefer_dense);
+      n <= 128 && (pr ? std::atoi(pr) != 0 && (std::atoi(pr) == 1 || !prefer_dense)
+                      : layer_path && !prefer_dense);
   const bool pair_ok = dense || routed_pairs;
   a.pair_b = pair_ok && (d / kBM) % 2 == 0 ? 1 : 0;
   if (const char* pv = std::getenv("DESMOE_FFN_PAIRB")) a.pair_b = a.pair_b && std::atoi(pv) != 0;
@@ -976,22 +1015,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   if (const char* pv = std::getenv("DESMOE_FFN_PAIRA")) a.pair_a = a.pair_a && std::atoi(pv) != 0;
   a.split_a = c->num_sms;
   if (const char* sv = std::getenv("DESMOE_FFN_SPLITA")) a.split_a = std::max(0, std::atoi(sv));
-  const int stage_bytes = kb * kATile + kb * a.b_rows * 128;
-  const int fixed = 1024 + 8 * (2 * 8 + 4 + 8) + 16 + 16 + 48 +
-                    4 * (4 + 3 * m + 3 * n * k) + 16 * 64 * 4 + 64;
-  int stages = (kSmemLimit - 256 - fixed) / stage_bytes;  // 256 B: the kernel's static smem
-  // deeper rings only lengthen the queues every other memory access waits
-  // behind
-  // 128 KB of weights in flight per SM measured best (4 x 32 KB / 2 x 64 KB)
-  stages = std::max(2, std::min(stages, 8 / kb));
-  if (const char* sv = std::getenv("DESMOE_FFN_STAGES"))  // tuning experiments
-    stages = std::max(2, std::min(stages, std::atoi(sv)));
-  a.stages = stages;
-  if (4 * (m * ((n + 31) / 32) + 3 * m + n * k) > stage_bytes)
-    return fail(DESMOE_EINVAL, "expert FFN prologue scratch exceeds a pipeline stage");
-  const size_t smem = static_cast<size_t>(fixed) + static_cast<size_t>(stages) * stage_bytes;
-  if (smem > static_cast<size_t>(kSmemLimit - 256))
-    return fail(DESMOE_EINVAL, "expert FFN shared-memory plan exceeds 227 KB");
+  a.stages = plan.stages;
+  const size_t smem = plan.smem;
   cudaLaunchConfig_t lc{};
   // One CTA per SM. Behind the front kernel (PDL) the FFN CTAs become
   // resident while it runs — except on the front cluster's SMs, where the
@@ -1254,6 +1279,12 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
     c->n_ev = 0;
     c->launches = 0;
   }
+  // every FFN shape check before anything is launched: the front publishes
+  // tagged words the next call's FFN would accept if no FFN + combine (which
+  // advances the call sequence) ran behind it
+  FfnPlan plan;
+  rc = ffn_plan(ex, n, cfg->top_k, &plan);
+  if (rc) return rc;
   mark(c, st);
   bool zeroed = false;
   rc = front_impl(c, ex, x, w_r, n, cfg, st, &zeroed);
@@ -1281,7 +1312,7 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
                             std::getenv("DESMOE_ALWAYS_DENSE");
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
-                front_used, y_bf16, residual ? x : nullptr, prefer_dense);
+                front_used, y_bf16, residual ? x : nullptr, prefer_dense, true);
   if (rc) return rc;
   return DESMOE_OK;
 }

@@ -714,7 +714,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = a0 + KB * kATile;
           if (pair) {
             // tile tt: its KH blocks x the KH shared boxes -> columns [128 tt, 128 tt + n_mma)
-            // (pairs only in dense mode: n_mma <= 64)
+            // of accumulator buffer `buf` (256 columns). Pairs run in dense mode
+            // (n_mma <= 64) and in routed mode for blocks of n <= 128 tokens, so
+            // n_mma <= 128 and tile 1 ends at column 256 of the buffer: buffer 1
+            // spans TMEM columns 256-511, tile 1 of it 384-511
 #pragma unroll
             for (int tt = 0; tt < 2; ++tt)
 #pragma unroll

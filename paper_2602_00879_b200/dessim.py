@@ -597,13 +597,27 @@ class ExpertWeights:
 
     @classmethod
     def swiglu(cls, w_gate, w_up, w_down, experts=None, expert_range=None, ctx=None):
+        import torch
+        if w_gate.dim() != 3:
+            raise ValueError("w_gate must be [experts x ffn x hidden]")
         m, f, d = w_gate.shape
+        for name, t, shape in (("w_gate", w_gate, (m, f, d)), ("w_up", w_up, (m, f, d)),
+                               ("w_down", w_down, (m, d, f))):
+            if tuple(t.shape) != shape:
+                raise ValueError(f"{name} shape {tuple(t.shape)} != {shape}")
+            if t.dtype != torch.bfloat16 or not t.is_cuda:
+                raise ValueError(f"{name} must be a bf16 CUDA tensor")
         return cls(_lib.FFN_SWIGLU, experts or m, d, f,
                    (w_gate.contiguous(), w_up.contiguous(), w_down.contiguous()),
                    expert_range, ctx)
 
     @classmethod
     def linear(cls, w):
+        import torch
+        if w.dim() != 3 or w.shape[1] != w.shape[2]:
+            raise ValueError("w must be [experts x hidden x hidden]")
+        if w.dtype != torch.bfloat16 or not w.is_cuda:
+            raise ValueError("w must be a bf16 CUDA tensor")
         m, d, _ = w.shape
         return cls(_lib.FFN_LINEAR, m, d, d, (w.contiguous(),))
 

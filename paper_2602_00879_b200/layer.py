@@ -34,6 +34,21 @@ class LayerConfig:
                         float(self.vote_beta), _lib.VOTE_ACTIVATED)
 
 
+def _check_act(name, t, n_max, hidden, dtype, device_only=True):
+    """A [n x hidden] activation tensor the C ABI reads / writes as packed
+    `dtype` rows: reject anything else before its pointer crosses the ABI."""
+    import torch
+    if t.dim() != 2 or t.shape[1] != hidden or not (1 <= t.shape[0] <= n_max):
+        raise ValueError(f"{name} must be [n x {hidden}] with 1 <= n <= {n_max}, "
+                         f"got {tuple(t.shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if device_only and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+
+
 class DesMoeLayer:
     """One DES MoE layer. With expert_range=(lo, hi), w_gate/w_up/w_down hold
     only the owned experts of an expert-parallel rank (see ep.py); connect the
@@ -43,7 +58,10 @@ class DesMoeLayer:
                  expert_range=None, own_context=False):
         import torch
         self.cfg = cfg
+        if tuple(w_router.shape) != (cfg.experts, cfg.hidden) or w_router.dtype != torch.bfloat16:
+            raise ValueError(f"w_router must be bf16 [{cfg.experts} x {cfg.hidden}]")
         self.w_router = w_router.contiguous()
+        self.max_tokens = max_tokens
         ctx = None
         if own_context:  # a private C-ABI context (several simulated ranks per thread)
             ctx = _Ctx(torch.cuda.current_device(), max_tokens, max(cfg.experts, 256), 32,
@@ -57,9 +75,13 @@ class DesMoeLayer:
     def forward(self, x, y=None, strategy=None, stream=None):
         """x [n x d] bf16 on the device -> y [n x d] fp32 (stream-ordered)."""
         import torch
+        _check_act("x", x, self.max_tokens, self.cfg.hidden, torch.bfloat16)
         n = x.shape[0]
         if y is None:
             y = torch.empty((n, self.cfg.hidden), dtype=torch.float32, device=x.device)
+        _check_act("y", y, self.max_tokens, self.cfg.hidden, torch.float32)
+        if y.shape[0] != n:
+            raise ValueError("y must have as many rows as x")
         rc = self._route_cfg(strategy)
         st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
         check(lib().desmoe_layer_forward(self.ctx.h, self.experts.h, self.w_router.data_ptr(),
@@ -79,6 +101,13 @@ class DesMoeLayer:
         """Host (pinned) bf16 x -> host fp32 y through desmoe_layer_forward_host
         (H2D copy, layer, D2H copy, synchronise)."""
         import torch
+        _check_act("x_host", x_host, self.max_tokens, self.cfg.hidden, torch.bfloat16, False)
+        _check_act("y_host", y_host, self.max_tokens, self.cfg.hidden, torch.float32, False)
+        if x_host.is_cuda or y_host.is_cuda or y_host.shape[0] != x_host.shape[0]:
+            raise ValueError("x_host / y_host must be host tensors with the same row count")
+        if stats_host is not None and (stats_host.is_cuda or stats_host.dtype != torch.int32
+                                       or stats_host.numel() < 4):
+            raise ValueError("stats_host must be a host int32 tensor of >= 4 entries")
         check(lib().desmoe_layer_forward_host(
             self.ctx.h, self.experts.h, self.w_router.data_ptr(), x_host.data_ptr(),
             x_host.shape[0], C.byref(self._route_cfg(strategy)), y_host.data_ptr(),
@@ -122,6 +151,7 @@ class DesMoeStack:
     def __init__(self, cfg: LayerConfig, layers, max_tokens=256, expert_range=None):
         import torch
         self.cfg = cfg
+        self.max_tokens = max_tokens
         self.ctx = _Ctx(torch.cuda.current_device(), max_tokens, max(cfg.experts, 256), 32,
                         max(cfg.hidden, 4096))
         self.routers, self.experts = [], []
@@ -141,9 +171,13 @@ class DesMoeStack:
         """x [n x d] bf16 -> y [n x d] fp32 after all layers (stream-ordered);
         residual=True: every layer outputs h + MoE(h)."""
         import torch
+        _check_act("x", x, self.max_tokens, self.cfg.hidden, torch.bfloat16)
         n = x.shape[0]
         if y is None:
             y = torch.empty((n, self.cfg.hidden), dtype=torch.float32, device=x.device)
+        _check_act("y", y, self.max_tokens, self.cfg.hidden, torch.float32)
+        if y.shape[0] != n:
+            raise ValueError("y must have as many rows as x")
         rc = self.cfg.route_cfg(strategy)
         st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream()
         check(lib().desmoe_stack_forward(self.ctx.h, self._ex, self._wr, len(self.experts),

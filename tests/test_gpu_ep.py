@@ -15,9 +15,14 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("strategy", ["vote", "vanilla"])
-def test_ep_ranks_match_single_gpu(world, strategy):
-    m, d, f, n, k = 64, 512, 512, 32, 8
-    cfg = LayerConfig(m, k, d, f, strategy=strategy, vote_beta=0.4)
+@pytest.mark.parametrize("m,d,f,n,beta", [
+    (64, 512, 512, 32, 0.4),      # dense FFN mode (DES) / routed pairs (vanilla)
+    (64, 512, 512, 128, 0.4),     # N > 64: routed mode for every strategy
+    (128, 2048, 768, 32, 0.3),    # C4 (SDAR-30B / Qwen3-30B-A3B shape, BASELINE configs[3])
+])
+def test_ep_ranks_match_single_gpu(world, strategy, m, d, f, n, beta):
+    k = 8
+    cfg = LayerConfig(m, k, d, f, strategy=strategy, vote_beta=beta)
     wr = synth.router_weights(m, d, seed=5)
     full = DesMoeLayer(cfg, wr, *synth.swiglu_weights(m, d, f, seed=9))
     ranks = []
@@ -92,3 +97,42 @@ def test_ep_two_processes_ipc():
                        capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     assert r.stdout.count('"vote": true, "vanilla": true') == 2, r.stdout
+
+
+def _run_ep_check(nproc, env_extra):
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = {key: v for key, v in os.environ.items() if key != "DESMOE_EP_SAME_DEVICE"}
+    env.update(env_extra)
+    return subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+                           f"--master-port={port}", os.path.join(root, "tools", "ep_check.py")],
+                          capture_output=True, text=True, timeout=900, env=env)
+
+
+@pytest.mark.parametrize("shape", ["64,512,512,128,0.4", "128,2048,768,32,0.3"])
+def test_ep_two_processes_routed_and_c4(shape):
+    """The cross-process IPC path at N=128 (routed FFN mode, DES-Vote) and at
+    the C4 shape (d=2048), two ranks time-sharing one GPU."""
+    r = _run_ep_check(2, {"DESMOE_EP_SAME_DEVICE": "1", "DESMOE_EP_SHAPE": shape})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert r.stdout.count('"vote": true, "vanilla": true') == 2, r.stdout
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs two GPUs of one NVLink box")
+@pytest.mark.parametrize("shape", ["64,512,512,32,0.4", "128,2048,768,32,0.3"])
+def test_ep_across_devices(shape):
+    """One rank per GPU (NCCL group for the handle all-gather, CUDA IPC peer
+    mappings over NVLink): every rank's output bit-identical to the one-GPU
+    layer."""
+    world = min(torch.cuda.device_count(), 8)
+    r = _run_ep_check(world, {"DESMOE_EP_SHAPE": shape})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert r.stdout.count('"vote": true, "vanilla": true') == world, r.stdout

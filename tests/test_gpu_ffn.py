@@ -8,7 +8,9 @@ Tolerances (stated per north_star "within a stated bf16/fp32 tolerance"):
     moe_forward on the same bf16-rounded values: |err| <= 1e-4 * max|y|
     (fp32 tensor-core accumulation);
   * SwiGLU experts vs the C restatement (fp64 sums, H rounded to bf16):
-    |err| <= 2e-2 * max|y| (H's bf16 rounding may differ by one ulp);
+    max |err| <= 4e-3 * max|y| and mean |err| <= 4e-4 * max|y| (H's bf16
+    rounding may differ by one ulp where the GPU's fp32 accumulation order
+    moves G or U across a rounding boundary; observed max 5e-4);
   * routing IDs computed from the GPU's own logits: identical to the
     reference library fed those logits.
 """
@@ -88,21 +90,32 @@ def test_moe_forward_facade(ref):
     assert np.abs(y - want).max() <= 2e-2 * np.abs(want).max()  # bf16 weights/inputs
 
 
+# BASELINE configs: C1 M=64 d=512; C2 M=64 d=2048 F=1024 N=32;
+# C3 M=256 d=2048 F=512 N=8-256; C4 M=128 d=2048 F=768
+BETA = {64: 0.4, 128: 0.3, 256: 0.15}
+
+
 @pytest.mark.parametrize("m,d,f,n,strategy", [
     (16, 256, 256, 16, "vanilla"),
-    (64, 512, 512, 32, "vote"),
-    (64, 2048, 1024, 32, "vote"),
-    (64, 2048, 1024, 32, "vanilla"),  # routed mode with pair units
+    (64, 512, 512, 32, "vote"),       # C1
+    (64, 2048, 1024, 32, "vote"),     # C2 (the bench workload)
+    (64, 2048, 1024, 32, "seq"),      # C2 DES-Seq
+    (64, 2048, 1024, 32, "vanilla"),  # C2 vanilla: routed mode with pair units
+    (256, 2048, 512, 32, "vote"),     # C3 N=32 (Table 1 LLaDA2.0-mini point)
+    (256, 2048, 512, 8, "vote"),      # C3 N=8
     (256, 1024, 512, 64, "seq"),
+    (128, 2048, 768, 32, "vote"),     # C4
+    (128, 2048, 768, 32, "vanilla"),  # C4 vanilla
     (128, 512, 768, 256, "vote"),
-    (256, 2048, 512, 256, "vote"),   # token-split router GEMM at the C3 shape
+    (256, 2048, 512, 256, "vote"),    # token-split router GEMM at the C3 shape
 ])
-def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
+def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy, rho=0.3):
     torch.manual_seed(0)
     wg, wu, wd = synth.swiglu_weights(m, d, f, seed=11)
     wr = synth.router_weights(m, d, seed=12)
-    x = synth.hidden_states(n, d, seed=13, rho=0.3)
-    cfg = LayerConfig(m, 8, d, f, strategy=strategy, seq_k=3, vote_beta=0.4)
+    x = synth.hidden_states(n, d, seed=13, rho=rho)
+    beta = BETA.get(m, 0.4)
+    cfg = LayerConfig(m, 8, d, f, strategy=strategy, seq_k=3, vote_beta=beta)
     layer = DesMoeLayer(cfg, wr, wg, wu, wd)
     y = layer.forward(x)
     torch.cuda.synchronize()
@@ -122,7 +135,7 @@ def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
         r = ref.topk_route(lg, 8)
         mem = np.unique(r.idx[r.idx >= 0])
     else:
-        mem, r = ref.des_run(lg, 8, strategy, seq_k=3, beta=0.4)
+        mem, r = ref.des_run(lg, 8, strategy, seq_k=3, beta=beta)
     stats = layer.stats.cpu().numpy()
     u, total, _ = ref.moe_latency(r, m)
     assert stats[0] == u and stats[2] == total
@@ -133,8 +146,13 @@ def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
                         wu.float().cpu().numpy(), wd.float().cpu().numpy(), threads=8)
     got = y.cpu().numpy()
     scale = np.abs(want).max()
-    assert np.abs(got - want).max() <= 2e-2 * scale
-    assert np.abs(got - want).mean() <= 2e-3 * scale
+    err_max = np.abs(got - want).max() / scale
+    err_mean = np.abs(got - want).mean() / scale
+    print(f"swiglu m={m} d={d} f={f} n={n} {strategy}: max|err|/max|y| = {err_max:.2e}, "
+          f"mean = {err_mean:.2e}")
+    assert err_max <= 4e-3, err_max
+    assert err_mean <= 4e-4, err_mean
+    return r
 
 
 @pytest.mark.parametrize("m,d,f,n,strategy", [
@@ -148,6 +166,48 @@ def test_pair_units_without_split(ref, port, monkeypatch, m, d, f, n, strategy):
     monkeypatch.setenv("DESMOE_FFN_SPLIT", "0")
     monkeypatch.setenv("DESMOE_FFN_SPLITA", "0")
     test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy)
+
+
+def test_routed_pairs_over_64_tokens_per_expert(ref, port, monkeypatch):
+    """Routed-mode pair units (vanilla, 16 < N <= 128, every unit a pair) where
+    some expert receives more than 64 tokens: the pair's second tile then
+    spans TMEM columns 384-511 of accumulator buffer 1."""
+    monkeypatch.setenv("DESMOE_FFN_SPLIT", "0")
+    monkeypatch.setenv("DESMOE_FFN_SPLITA", "0")
+    r = test_swiglu_layer_matches_oracle(ref, port, 64, 512, 512, 128, "vanilla", rho=0.97)
+    _, _, per = ref.moe_latency(r, 64)
+    assert per.max() > 64, per.max()
+
+
+def test_rejected_call_leaves_no_stale_handoff(ref, port):
+    """A block the expert FFN cannot plan (N=256 with K=12: its prologue
+    tables exceed the plan) is rejected BEFORE the front kernel launches, so a
+    following valid call (graphs off: eager launches) never consumes stale
+    published words from the rejected one."""
+    from paper_2602_00879_b200._lib import DesmoeError
+    m, d, f = 64, 512, 512
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=61)
+    wr = synth.router_weights(m, d, seed=62)
+    layer = DesMoeLayer(LayerConfig(m, 12, d, f, strategy="vote", vote_beta=0.4), wr, wg, wu, wd,
+                        own_context=True)
+    _lib.check(_lib.lib().desmoe_set_graphs(layer.ctx.h, 0))
+    bad = synth.hidden_states(256, d, seed=63, rho=0.3)
+    with pytest.raises((ValueError, DesmoeError), match="expert FFN"):
+        layer.forward(bad)
+    for call in range(3):
+        x = synth.hidden_states(32, d, seed=64 + call, rho=0.3)
+        y = layer.forward(x)
+        torch.cuda.synchronize()
+        layer.check()
+        lg = layer.last_logits(32).double().cpu().numpy()
+        mem, r = ref.des_run(lg, 12, "vote", beta=0.4)
+        idx, gate, cnt, members = layer.last_route(32)
+        assert members == mem.tolist()
+        np.testing.assert_array_equal(idx, r.idx)
+        want = port.moe_ffn(r, x.float().cpu().numpy(), wg.float().cpu().numpy(),
+                            wu.float().cpu().numpy(), wd.float().cpu().numpy(), threads=8)
+        err = np.abs(y.cpu().numpy() - want).max() / np.abs(want).max()
+        assert err <= 4e-3, (call, err)
 
 
 def test_layer_host_entry_matches_device_entry():

@@ -378,3 +378,21 @@ def test_baselines_golden_fixtures(port):
                                     naee_beta=nb, mcmoe_beta=mb, fraction=fr, score=int(sc))
             assert np.array_equal(r.idx, g[f"idx{i}_{j}"]) and np.array_equal(r.cnt, g[f"cnt{i}_{j}"])
             assert np.array_equal(r.gate, g[f"gate{i}_{j}"])
+
+
+def test_exact_logit_split_reconstructs_fp32():
+    """The controlled-logit harness (tests/_exact_logits.py) splits any fp32
+    logit into three bf16 pieces whose fp32 sum in ascending K order is the
+    value itself (the layer-path parity tests rely on it)."""
+    from _exact_logits import bf16_trunc, split3
+    rng = np.random.default_rng(0)
+    cases = [rng.normal(size=(64, 256)) * 1.5, rng.uniform(-1000, -705, size=(8, 64)),
+             rng.uniform(38, 60, size=(8, 64)), np.zeros((4, 4)),
+             (np.float32(1.5) + np.arange(256, dtype=np.float32) * np.float32(2 ** -23))[None, :]]
+    for v in cases:
+        v = np.asarray(v, np.float32)
+        a, b, c = split3(v)
+        for piece in (a, b, c):
+            assert np.array_equal(bf16_trunc(piece), piece)
+        # every prefix / subset sum the split-K GEMM may form is exact too
+        assert np.array_equal((a + b * np.float32(2 ** -8)).astype(np.float32) + c * np.float32(2 ** -16), v)

@@ -29,10 +29,13 @@ def main():
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    m, d, f, n, k = 64, 512, 512, 32, 8
+    # DESMOE_EP_SHAPE="m,d,f,n,beta" (default: 64 experts, d=512, F=512, N=32, 0.4)
+    shape = os.environ.get("DESMOE_EP_SHAPE", "64,512,512,32,0.4").split(",")
+    m, d, f, n = (int(v) for v in shape[:4])
+    beta, k = float(shape[4]), 8
     res = {}
     for strategy in ("vote", "vanilla"):
-        cfg = LayerConfig(m, k, d, f, strategy=strategy, vote_beta=0.4)
+        cfg = LayerConfig(m, k, d, f, strategy=strategy, vote_beta=beta)
         wr = synth.router_weights(m, d, seed=5)
         full = DesMoeLayer(cfg, wr, *synth.swiglu_weights(m, d, f, seed=9), own_context=True)
         lo, hi = ep.partition(m, ws)[rank]
