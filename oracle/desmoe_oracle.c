@@ -494,3 +494,73 @@ void or_router_logits(int n, int m, int d, const float* x, const float* w, doubl
       logits[(size_t)t * m + e] = acc;
     }
 }
+
+/* ---- glibc exp, restated (the reference's std::exp) ----------------------
+ * glibc 2.39 sysdeps/ieee754/dbl-64/e_exp.c (Arm optimized-routines), the
+ * FMA build its x86-64 ifunc selects on FMA + AVX2 hosts, operation for
+ * operation: the CUDA restatement paper_2602_00879_b200/csrc/libm_exp.cuh
+ * follows the same steps. The 2^(k/128) table is generated from first
+ * principles by tools/gen_exp_table.py. This copy exists only to pin the
+ * restatement against the host libm (tests/test_oracle.py). fma() is the
+ * correctly rounded C99 fma; this file is compiled without contraction
+ * (-std=c11), so every other operation rounds exactly once. */
+static const uint64_t kExpTab[256] = {
+#include "../paper_2602_00879_b200/csrc/libm_exp_table.inc"
+};
+
+static double u2d(uint64_t u) { double d; memcpy(&d, &u, 8); return d; }
+static uint64_t d2u(double d) { uint64_t u; memcpy(&u, &d, 8); return u; }
+
+double or_glibc_exp1(double x) {
+  const double inv_ln2n = 0x1.71547652b82fep+7, shift = 0x1.8p52;
+  const double neg_ln2hi = -0x1.62e42fefa0000p-8, neg_ln2lo = -0x1.cf79abc9e3b3ap-47;
+  const double c2 = 0x1.ffffffffffdbdp-2, c3 = 0x1.555555555543cp-3;
+  const double c4 = 0x1.55555cf172b91p-5, c5 = 0x1.1111167a4d017p-7;
+  const uint64_t ix = d2u(x);
+  uint32_t abstop = (uint32_t)(ix >> 52) & 0x7ffu;
+  if (abstop - 0x3c9u >= 0x3fu) {
+    if ((int)abstop - 0x3c9 < 0) return 1.0 + x;
+    if (abstop >= 0x409u) {
+      if (ix == 0xfff0000000000000ull) return 0.0;
+      if (abstop >= 0x7ffu) return 1.0 + x;
+      return (ix >> 63) ? 0.0 : u2d(0x7ff0000000000000ull);
+    }
+    abstop = 0;
+  }
+  const double kd0 = fma(x, inv_ln2n, shift);
+  const uint64_t ki = d2u(kd0);
+  const double kd = kd0 - shift;
+  double r = fma(kd, neg_ln2hi, x);
+  r = fma(kd, neg_ln2lo, r);
+  const uint32_t idx = 2u * (uint32_t)(ki & 127u);
+  const double tail = u2d(kExpTab[idx]);
+  uint64_t sbits = kExpTab[idx + 1] + (ki << 45);
+  const double r2 = r * r;
+  double tmp = fma(fma(r, c3, c2), r2, r + tail);
+  tmp = fma(r2 * r2, fma(r, c5, c4), tmp);
+  if (abstop != 0) return fma(u2d(sbits), tmp, u2d(sbits));
+  if ((ki & 0x80000000ull) == 0) {
+    sbits -= 1009ull << 52;
+    return fma(u2d(sbits), tmp, u2d(sbits)) * 0x1p1009;
+  }
+  sbits += 1022ull << 52;
+  const double scale = u2d(sbits), st = scale * tmp;
+  double y = scale + st;
+  if (y < 1.0) {
+    const double lo0 = (scale - y) + st;
+    const double hi = y + 1.0;
+    const double lo = ((1.0 - hi) + y) + lo0;
+    y = (lo + hi) - 1.0;
+    if (y == 0.0) y = 0.0;
+  }
+  return y * 0x1p-1022;
+}
+
+void or_glibc_exp(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) y[i] = or_glibc_exp1(x[i]);
+}
+
+/* the host libm's exp over an array (the comparison side of the pin) */
+void or_libm_exp(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) y[i] = exp(x[i]);
+}

@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include "libm_exp.cuh"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "desmoe kernels target sm_100a only"
@@ -148,13 +149,16 @@ static __device__ __noinline__ void warp_topk_packed(const double* val, int m, i
   __syncwarp();
 }
 
-// Out-of-line fp64 exp and division (IEEE round-to-nearest, as the reference's
-// std::exp / operator/): the routing kernels execute these once per element
+// Out-of-line fp64 exp and division (as the reference's std::exp /
+// operator/): the routing kernels execute these once per element
 // from many sites; one shared copy keeps their code (and instruction fetch
 // after an L2 flush) small.
-static __device__ __noinline__ double exp_f64(double x) { return exp(x); }
+// exp is glibc's, restated bit for bit (libm_exp.cuh).
+static __device__ __noinline__ double exp_f64(double x) { return glibc_exp(x, kExpTab); }
 static __device__ __noinline__ double div_f64(double a, double b) { return a / b; }
-static __device__ __noinline__ double sigmoid_f64(double x) { return 1.0 / (1.0 + exp(-x)); }
+static __device__ __noinline__ double sigmoid_f64(double x) {
+  return 1.0 / (1.0 + glibc_exp(-x, kExpTab));
+}
 
 // Truncated key of a packed key (drops the index bits).
 __device__ inline uint64_t key_value_part(uint64_t pk) { return pk >> 10; }

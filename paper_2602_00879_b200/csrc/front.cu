@@ -150,7 +150,9 @@ __device__ inline uint32_t fkey(float f) {
 // 128-byte instruction line costs ~0.15 us on this path, so the routing code
 // is written for the smallest executed footprint (rolled loops, no sorting
 // networks), not for the fewest instructions.
-__device__ __noinline__ double f_exp(double x) { return exp(x); }
+__device__ __noinline__ double f_exp(double x, const unsigned long long* tab) {
+  return glibc_exp(x, tab);  // bit-identical to the reference's std::exp (libm_exp.cuh)
+}
 __device__ __noinline__ double f_div(double a, double b) { return a / b; }
 
 // ---------------------------------------------------------------------------
@@ -428,6 +430,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
   __shared__ uint64_t s_ts[40];  // timeline marks (trace buffer only)
   __shared__ uint64_t s_pw[96];  // instruction-cache prewarm scratch
+  // glibc exp's 2^(k/128) table, staged while the router GEMM runs
+  __shared__ unsigned long long s_exptab[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool tracing = a.trace != nullptr;
   if (tracing && tid == 0) s_ts[24] = clock64();
@@ -523,6 +527,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
   }
   if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
+  if (tid < 256) s_exptab[tid] = kExpTab[tid];
   pdl_launch_dependents();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
   const uint32_t tag = a.seq ? hand_tag(*a.seq) : 0u;  // this call's hand-off tag
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       warp_rank_select(reinterpret_cast<const float*>(erow), m, k < m ? k + 1 : k, nullptr, ds);
     } else if (warp == 9) {
       if (lane == 0) {
-        volatile double sink = f_exp(0.0) + f_div(1.0, 2.0);
+        volatile double sink = f_exp(-1.5, s_exptab) + f_div(1.0, 2.0);
         (void)sink;
       }
       dk[lane] = static_cast<uint64_t>(lane);
@@ -834,7 +839,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
         const double x = static_cast<double>(xrow[w]);
         double e = x;
         if (act < 2) {
-          const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x);
+          const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x, s_exptab);
           e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
         }
         erow[j * ew + i] = e;
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       const double x = static_cast<double>(xrow[w]);
       double e = x;
       if (act < 2) {
-        const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x);
+        const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x, s_exptab);
         e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
       }
       erow[j * ew + i] = e;

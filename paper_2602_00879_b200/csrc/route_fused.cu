@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(1024, 1) fused_route_kernel(FusedRouteArgs<T> 
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     if (a.act == 0) {  // softmax: sum in ascending expert order (gating.cpp:30-34)
-      for (int i = lane; i < m; i += 32) row[i] = exp(row[i] - mx);
+      for (int i = lane; i < m; i += 32) row[i] = glibc_exp(row[i] - mx, kExpTab);
       __syncwarp();
       double s = 0.0;
       if (lane == 0)
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(1024, 1) fused_route_kernel(FusedRouteArgs<T> 
       s = __shfl_sync(0xffffffffu, s, 0);
       for (int i = lane; i < m; i += 32) row[i] = row[i] / s;
     } else if (a.act == 1) {
-      for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + exp(-row[i]));
+      for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + glibc_exp(-row[i], kExpTab));
     }
     __syncwarp();
     if (a.probs)

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(GateTopkArgs<T> a) {
   for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
 
   if (a.act == 0) {  // softmax
-    for (int i = lane; i < m; i += 32) row[i] = exp(row[i] - mx);
+    for (int i = lane; i < m; i += 32) row[i] = glibc_exp(row[i] - mx, kExpTab);
     __syncwarp();
     double s = 0.0;
     if (lane == 0) {
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(GateTopkArgs<T> a) {
     s = __shfl_sync(0xffffffffu, s, 0);
     for (int i = lane; i < m; i += 32) row[i] = row[i] / s;
   } else if (a.act == 1) {  // sigmoid
-    for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + exp(-row[i]));
+    for (int i = lane; i < m; i += 32) row[i] = 1.0 / (1.0 + glibc_exp(-row[i], kExpTab));
   }
   __syncwarp();
   if (a.probs) {

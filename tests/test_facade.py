@@ -1,15 +1,18 @@
-"""The reference's OWN unit tests (/root/reference/proj/tests/test_gating.cpp,
-test_des.cpp, test_baselines.cpp, test_trace.cpp, test_analysis.cpp and
-test_metrics.cpp, compiled unchanged by tests/cpp/Makefile; test_analysis.cpp's
+"""The reference's OWN unit tests (/root/reference/proj/tests/test_core.cpp,
+test_gating.cpp, test_des.cpp, test_baselines.cpp, test_trace.cpp,
+test_analysis.cpp and test_metrics.cpp, compiled unchanged by
+tests/cpp/Makefile; test_analysis.cpp's
 one Monte-Carlo oracle comes from the test-only stub
 tests/cpp/stub/dessim/oracle.hpp)
 run against the C++ facade include/dessim/*.hpp -> libdessim_gpu.so ->
 libdesmoe.so.
 
 * CPU: the doctest stand-in runs the same suites against the reference library
-  itself (oracle/_ref) with 99/99 passing, the facade exports the reference's
+  itself (oracle/_ref) with 108/108 passing, the facade exports the reference's
   dessim:: symbols, and without a GPU the facade fails loudly (no CPU path).
 * GPU: every reference test case passes on the B200 path.
+* The reference's acceptance runner (tests/acceptance.cpp, unchanged): all 11
+  criteria PASS on the reference library (CPU control) and on the GPU façade.
 """
 import os
 import subprocess
@@ -20,6 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
 ON_GPU = os.path.join(BUILD, "reference_tests")
 ON_REF = os.path.join(BUILD, "reference_tests_on_ref")
+ACC_GPU = os.path.join(BUILD, "acceptance_gpu")
+ACC_REF = os.path.join(BUILD, "acceptance_ref")
 FACADE = os.path.join(ROOT, "paper_2602_00879_b200", "libdessim_gpu.so")
 
 
@@ -32,7 +37,7 @@ def _run(path):
 def test_doctest_standin_runs_reference_suites_on_reference():
     r = _run(ON_REF)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "| 99 passed | 0 failed" in r.stdout, r.stdout
+    assert "| 108 passed | 0 failed" in r.stdout, r.stdout
 
 
 def test_facade_exports_reference_api():
@@ -68,3 +73,22 @@ def test_reference_unit_tests_pass_on_gpu_facade():
     r = _run(ON_GPU)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     assert "| 0 failed" in r.stdout, r.stdout
+
+
+def test_acceptance_runner_on_reference():
+    r = _run(ACC_REF)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all 11 criteria passed" in r.stdout, r.stdout
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_on_gpu_facade():
+    """acceptance.cpp criteria 1 (budgets), 4 (10^4 random assignments: union
+    == counts), 6 (1000 fused == composed instances, M <= 512), 7 (degenerate
+    limits) and 8 (nesting / monotonicity) — SURVEY 8c — and the rest of the
+    runner, over the GPU façade."""
+    r = _run(ACC_GPU)
+    print(r.stdout)
+    for c in (1, 4, 6, 7, 8):
+        assert f"[PASS] criterion {c}:" in r.stdout, (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0 and "all 11 criteria passed" in r.stdout, (r.stdout + r.stderr)[-4000:]

@@ -109,7 +109,12 @@ BETA = {64: 0.4, 128: 0.3, 256: 0.15}
     (128, 512, 768, 256, "vote"),
     (256, 2048, 512, 256, "vote"),    # token-split router GEMM at the C3 shape
 ])
-def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy, rho=0.3):
+def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
+    swiglu_case(ref, port, m, d, f, n, strategy)
+
+
+def swiglu_case(ref, port, m, d, f, n, strategy, rho=0.3):
+    """Layer output vs the C restatement; returns the reference route."""
     torch.manual_seed(0)
     wg, wu, wd = synth.swiglu_weights(m, d, f, seed=11)
     wr = synth.router_weights(m, d, seed=12)
@@ -165,7 +170,7 @@ def test_pair_units_without_split(ref, port, monkeypatch, m, d, f, n, strategy):
     where the default split would leave none."""
     monkeypatch.setenv("DESMOE_FFN_SPLIT", "0")
     monkeypatch.setenv("DESMOE_FFN_SPLITA", "0")
-    test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy)
+    swiglu_case(ref, port, m, d, f, n, strategy)
 
 
 def test_routed_pairs_over_64_tokens_per_expert(ref, port, monkeypatch):
@@ -174,7 +179,7 @@ def test_routed_pairs_over_64_tokens_per_expert(ref, port, monkeypatch):
     spans TMEM columns 384-511 of accumulator buffer 1."""
     monkeypatch.setenv("DESMOE_FFN_SPLIT", "0")
     monkeypatch.setenv("DESMOE_FFN_SPLITA", "0")
-    r = test_swiglu_layer_matches_oracle(ref, port, 64, 512, 512, 128, "vanilla", rho=0.97)
+    r = swiglu_case(ref, port, 64, 512, 512, 128, "vanilla", rho=0.97)
     _, _, per = ref.moe_latency(r, 64)
     assert per.max() > 64, per.max()
 

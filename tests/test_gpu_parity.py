@@ -22,7 +22,8 @@ fallback paths that random hidden states never hit:
 
 Pass bar: the layer's logits equal the injected fp32 values bit for bit;
 selected expert ids, per-token counts and coreset membership equal the
-reference's; gates within 1e-12 (CUDA's fp64 exp vs glibc's, last bit).
+reference's; gates bit-identical (atol = 0: the kernels' exp is glibc's,
+restated in csrc/libm_exp.cuh, and every sum runs in the reference's order).
 """
 import numpy as np
 import pytest
@@ -235,7 +236,7 @@ def criterion6_instances(ref, count=1000):
         k = 1 + below(min(m, 16))
         act = 1 if below(4) == 0 else 0
         m_core = 1 + below(m)
-        beta = (m_core + 0.5) / m
+        beta = min(1.0, (m_core + 0.5) / m)  # des_run's validate_params caps beta at 1
         L = synth.random_block(n, m, 62000 + i, 1.5).astype(np.float32)
         yield i, m, n, k, act, beta, L
 

@@ -396,3 +396,32 @@ def test_exact_logit_split_reconstructs_fp32():
             assert np.array_equal(bf16_trunc(piece), piece)
         # every prefix / subset sum the split-K GEMM may form is exact too
         assert np.array_equal((a + b * np.float32(2 ** -8)).astype(np.float32) + c * np.float32(2 ** -16), v)
+
+
+def test_glibc_exp_restatement():
+    """oracle/desmoe_oracle.c:or_glibc_exp (the same steps as the kernels'
+    csrc/libm_exp.cuh) equals the host libm's exp bit for bit over every
+    range the routing reaches: softmax arguments down to the subnormal band
+    and full underflow, sigmoid arguments, tiny, special values."""
+    import ctypes as C
+    lib = C.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                              "liboracle.so"))
+    f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+    for name in ("or_glibc_exp", "or_libm_exp"):
+        getattr(lib, name).argtypes = [f64p, f64p, C.c_long]
+        getattr(lib, name).restype = None
+    rng = np.random.default_rng(1)
+    x = np.concatenate([
+        rng.uniform(-1100.0, 0.0, 1_000_000), rng.uniform(-745.2, -708.0, 1_000_000),
+        rng.uniform(-40.0, 40.0, 1_000_000), rng.uniform(-1e-15, 1e-15, 10_000),
+        rng.uniform(700.0, 712.0, 10_000),
+        # fp32 logit differences, as the kernels feed them
+        (rng.normal(size=500_000).astype(np.float32).astype(np.float64)
+         - rng.normal(size=500_000).astype(np.float32).astype(np.float64)),
+        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, -1024.0, -1023.99, -512.0, -511.99,
+                  709.78, 709.79, -745.13, -745.14, 5e-324, -708.3964, -708.3965])])
+    a, b = np.empty_like(x), np.empty_like(x)
+    lib.or_glibc_exp(x, a, len(x))
+    lib.or_libm_exp(x, b, len(x))
+    same = (a.view(np.uint64) == b.view(np.uint64)) | (np.isnan(a) & np.isnan(b))
+    assert same.all(), x[~same][:8]
