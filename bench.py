@@ -343,18 +343,34 @@ def main():
     run("vote", warm[:1], record=False)
     launches = L.desmoe_last_launch_count(layers[0].ctx.h)
 
-    # e2e: host buffers through desmoe_layer_forward_host
+    # e2e: host buffers through the C ABI's desmoe_layer_forward_host — the
+    # call a C/C++ caller of the drop-in makes (include/desmoe.h), here through
+    # ctypes with its arguments built once. Every step: the caller's pinned x
+    # crosses the bus (in-graph ingress kernel), the layer runs, y (fp32) and
+    # the stats are written into pinned host memory, the call returns once the
+    # layer's completion word says they are visible.
     xh = [x.cpu().pin_memory() for _, x in timed]
     yh = torch.empty((n, d), dtype=torch.float32).pin_memory()
     sh = torch.empty(4, dtype=torch.int32).pin_memory()
-    for i, x in warm:
-        layers[i % nl].forward_host(x.cpu().pin_memory(), yh, sh, strategy="vote")
+    rc_vote = lc.route_cfg("vote")
+    sp = C.c_void_p(stream.cuda_stream)
+
+    def host_call(layer, x):
+        r = L.desmoe_layer_forward_host(layer.ctx.h, layer.experts.h, layer.w_router.data_ptr(),
+                                        x.data_ptr(), n, C.byref(rc_vote), yh.data_ptr(),
+                                        sh.data_ptr(), sp)
+        if r:
+            raise RuntimeError(L.desmoe_last_error().decode())
+
+    xw = [x.cpu().pin_memory() for _, x in warm]
+    for i, x in enumerate(xw):
+        host_call(layers[i % nl], x)
     e2e = []
     for i, x in enumerate(xh):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        layers[i % nl].forward_host(x, yh, sh, strategy="vote")
+        host_call(layers[i % nl], x)
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e3)
@@ -433,7 +449,9 @@ def main():
                      "algorithmic_bytes": "U*3*d*F*2 expert-weight bytes per block",
                      "peak_kind": peak_kind},
         "e2e": {"value": round(e2e_us, 3), "unit": "us/block",
-                "h2d_bytes_per_step": n * d * 2, "d2h_bytes_per_step": n * d * 4 + 16},
+                "h2d_bytes_per_step": n * d * 2, "d2h_bytes_per_step": n * d * 4 + 16,
+                "entry": "desmoe_layer_forward_host (C ABI, include/desmoe.h) via ctypes: pinned "
+                         "x in, fp32 y + stats out, returns when they are visible"},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
     }

@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -140,11 +141,19 @@ struct desmoe_ctx {
   void* x_dev = nullptr;
   float* y_dev = nullptr;
   int* stats_dev = nullptr;
-  // pinned, device-mapped [8]: [0..3] the host entry's stats (written by the
+  // pinned, device-mapped [16]: [0..3] the host entry's stats (written by the
   // kernels straight into host memory), [4] the data-check word (c->err is
-  // its device address), read by the host after a synchronisation
+  // its device address), [5] the host entry's call number, [6] the call
+  // number the last combine CTA published once y is visible (the host spins
+  // on it instead of synchronising the stream), [8..9] the device-mapped
+  // address of the caller's pinned x (read by the in-graph ingress kernel)
   int* host_tail = nullptr;
   int* host_tail_dev = nullptr;
+  int host_calls = 0;
+  const void* last_x_host = nullptr;   // pointer-attribute caches of the host entry
+  const void* last_x_mapped = nullptr;
+  const void* last_y_host = nullptr;
+  float* last_y_mapped = nullptr;
   // cached router descriptors
   const void* x_map_ptr = nullptr;
   int x_map_n = -1, x_map_d = -1;
@@ -160,6 +169,7 @@ struct desmoe_ctx {
     float* y;
     int* stats;
     bool prof;
+    bool ingress;  // host-buffer entry: x copied in by the graph's first kernel
   } gkey{};
   int g_n_ev = 0, g_launches = 0;
   // layer stacks (desmoe_stack_forward): bf16 ping-pong activations and graph
@@ -279,11 +289,11 @@ int desmoe_create(desmoe_ctx** out, int device, int max_tokens, int max_experts,
   A(alloc(&c->y_dev, static_cast<size_t>(max_tokens) * max_hidden));
   A(alloc(&c->stats_dev, 4));
   if (e == cudaSuccess)
-    e = cudaHostAlloc(reinterpret_cast<void**>(&c->host_tail), 8 * sizeof(int), cudaHostAllocMapped);
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->host_tail), 16 * sizeof(int), cudaHostAllocMapped);
   if (e == cudaSuccess)
     e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->host_tail_dev), c->host_tail, 0);
   if (e == cudaSuccess) {
-    std::memset(c->host_tail, 0, 8 * sizeof(int));
+    std::memset(c->host_tail, 0, 16 * sizeof(int));
     c->err = c->host_tail_dev + 4;
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
@@ -930,7 +940,8 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
              const int* route_idx, const double* route_gate, const int* route_cnt, float* y,
              const int* n_members, int* stats, cudaStream_t st, bool counters_zeroed = false,
              bool after_front = false, __nv_bfloat16* y_bf16 = nullptr,
-             const void* resid = nullptr, bool prefer_dense = false, bool layer_path = false) {
+             const void* resid = nullptr, bool prefer_dense = false, bool layer_path = false,
+             bool host_link = false) {
   const int m = ex->m, d = ex->d, f = ex->f;
   FfnPlan plan;
   int prc = ffn_plan(ex, n, k, &plan);
@@ -1081,6 +1092,10 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.stats = stats;
   ca.trace = c->trace;
   ca.trace_cap = c->trace_cap;
+  if (host_link) {  // host-buffer entry: publish completion to the spinning host
+    ca.host_call = c->host_tail_dev + 5;
+    ca.host_done = c->host_tail_dev + 6;
+  }
   if (ex->world > 1) {
     ca.flag = ex->ep_flag;
     ca.arrivals = static_cast<unsigned long long>(ex->world) * grid;
@@ -1273,7 +1288,7 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
 int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
                        int n, const desmoe_route_cfg* cfg, float* y, int* stats,
                        cudaStream_t st, __nv_bfloat16* y_bf16 = nullptr, bool reset = true,
-                       bool residual = false) {
+                       bool residual = false, bool ingress = false) {
   int rc;
   if (reset) {
     c->n_ev = 0;
@@ -1285,6 +1300,27 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   FfnPlan plan;
   rc = ffn_plan(ex, n, cfg->top_k, &plan);
   if (rc) return rc;
+  if (ingress) {
+    // host-buffer entry: the caller's pinned x comes in through its device
+    // mapping (address in a host-mapped word), inside the graph
+    const int n16 = n * ex->d / 8;
+    const auto* word = reinterpret_cast<const unsigned long long*>(c->host_tail_dev + 8);
+    auto* dst = static_cast<uint4*>(const_cast<void*>(x));
+    const char* iv = std::getenv("DESMOE_INGRESS");
+    if (iv && std::strcmp(iv, "ld") == 0) {
+      x_ingress_kernel<<<std::max(1, (n16 + 1023) / 1024), 256, 0, st>>>(word, dst, n16);
+    } else {
+      int chunk = 32768;  // measured: 16 KB 11.0 us, >= 32 KB 8.1-8.5 us for 128 KB
+      if (const char* cv = std::getenv("DESMOE_INGRESS_CHUNK"))
+        chunk = std::max(256, std::min(kIngressChunk, std::atoi(cv))) & ~15;
+      const size_t bytes = static_cast<size_t>(n16) * 16;
+      if (static_cast<size_t>(chunk) > bytes) chunk = static_cast<int>(bytes);
+      const int grid = static_cast<int>((bytes + chunk - 1) / chunk);
+      x_ingress_bulk_kernel<<<grid, 32, chunk, st>>>(word, dst, n16, chunk);
+    }
+    DESMOE_LAUNCHED();
+    c->launches += 1;
+  }
   mark(c, st);
   bool zeroed = false;
   rc = front_impl(c, ex, x, w_r, n, cfg, st, &zeroed);
@@ -1312,14 +1348,16 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
                             std::getenv("DESMOE_ALWAYS_DENSE");
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
-                front_used, y_bf16, residual ? x : nullptr, prefer_dense, true);
+                front_used, y_bf16, residual ? x : nullptr, prefer_dense, true,
+                stats != nullptr && stats == c->host_tail_dev);
   if (rc) return rc;
   return DESMOE_OK;
 }
 
 bool same_key(const desmoe_ctx::Key& a, const desmoe_ctx::Key& b) {
   return a.ex == b.ex && a.wr == b.wr && a.x == b.x && a.n == b.n && a.y == b.y &&
-         a.stats == b.stats && a.prof == b.prof && a.cfg.experts == b.cfg.experts &&
+         a.stats == b.stats && a.prof == b.prof && a.ingress == b.ingress &&
+         a.cfg.experts == b.cfg.experts &&
          a.cfg.top_k == b.cfg.top_k && a.cfg.activation == b.cfg.activation &&
          a.cfg.strategy == b.cfg.strategy && a.cfg.seq_k == b.cfg.seq_k &&
          a.cfg.vote_beta == b.cfg.vote_beta && a.cfg.vote_source == b.cfg.vote_source;
@@ -1329,21 +1367,27 @@ bool same_key(const desmoe_ctx::Key& a, const desmoe_ctx::Key& b) {
 
 extern "C" {
 
-int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
-                         int n, const desmoe_route_cfg* cfg, float* y, int* stats, void* stream) {
-  if (!c || !ex || !cfg) return fail(DESMOE_EINVAL, "null argument");
-  if (cfg->experts != ex->m) return fail(DESMOE_EINVAL, "config experts differ from expert bank");
-  int rc = check_block(c, n, cfg->experts);
-  if (rc) return rc;
-  cudaStream_t st = S(stream);
-  if (!c->use_graphs) return layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, st);
-  desmoe_ctx::Key key{ex, w_r, x, n, *cfg, y, stats, c->profiling};
+}  // extern "C"
+
+namespace {
+
+// The layer's launch sequence as ONE CUDA graph, captured the first time a
+// (experts, router, x, n, cfg, y, stats, ingress) tuple is seen and replayed
+// afterwards (eager launches when graphs are off).
+int layer_graph_launch(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
+                       int n, const desmoe_route_cfg* cfg, float* y, int* stats, cudaStream_t st,
+                       bool ingress) {
+  int rc;
+  if (!c->use_graphs)
+    return layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, st, nullptr, true, false, ingress);
+  desmoe_ctx::Key key{ex, w_r, x, n, *cfg, y, stats, c->profiling, ingress};
   if (!c->gexec || !same_key(key, c->gkey)) {
     // validate + capture the whole launch sequence on the context's capture
     // stream, then instantiate (or update) the executable graph
     cudaGraph_t g = nullptr;
     DESMOE_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-    rc = layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, c->cap_stream);
+    rc = layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, c->cap_stream, nullptr, true, false,
+                            ingress);
     cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
     if (rc) {
       if (g) cudaGraphDestroy(g);
@@ -1377,6 +1421,28 @@ int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_
   c->n_ev = c->g_n_ev;
   c->launches = c->g_launches;
   return DESMOE_OK;
+}
+
+// The host-buffer entry's graph: x = the context's device x (filled by the
+// in-graph ingress kernel or a preceding copy), stats into host-mapped memory,
+// completion published to the host.
+int desmoe_layer_forward_host_graph(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, int n,
+                                    const desmoe_route_cfg* cfg, float* y_dev, cudaStream_t st,
+                                    bool ingress) {
+  return layer_graph_launch(c, ex, w_r, c->x_dev, n, cfg, y_dev, c->host_tail_dev, st, ingress);
+}
+
+}  // namespace
+
+extern "C" {
+
+int desmoe_layer_forward(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r, const void* x,
+                         int n, const desmoe_route_cfg* cfg, float* y, int* stats, void* stream) {
+  if (!c || !ex || !cfg) return fail(DESMOE_EINVAL, "null argument");
+  if (cfg->experts != ex->m) return fail(DESMOE_EINVAL, "config experts differ from expert bank");
+  int rc = check_block(c, n, cfg->experts);
+  if (rc) return rc;
+  return layer_graph_launch(c, ex, w_r, x, n, cfg, y, stats, S(stream), false);
 }
 
 int desmoe_layer_logits(desmoe_ctx* c, float* logits_dev, int n, int experts, void* stream) {
@@ -1450,26 +1516,75 @@ int desmoe_layer_forward_host(desmoe_ctx* c, const desmoe_experts* ex, const voi
                               const void* x_host, int n, const desmoe_route_cfg* cfg,
                               float* y_host, int* stats_host, void* stream) {
   if (!c || !ex || !cfg || !x_host || !y_host) return fail(DESMOE_EINVAL, "null argument");
+  if (cfg->experts != ex->m) return fail(DESMOE_EINVAL, "config experts differ from expert bank");
   int rc = check_block(c, n, cfg->experts);
   if (rc) return rc;
   if (ex->d > c->max_d) return fail(DESMOE_EINVAL, "hidden exceeds context capacity");
   cudaStream_t st = S(stream);
   const size_t xb = static_cast<size_t>(n) * ex->d * 2, yb = static_cast<size_t>(n) * ex->d * 4;
-  DESMOE_CUDA(cudaMemcpyAsync(c->x_dev, x_host, xb, cudaMemcpyHostToDevice, st));
-  // pinned (device-mapped) y: the combine writes it straight into host memory
-  // over the bus; pageable y: a device copy then one D2H transfer
-  cudaPointerAttributes pa{};
-  float* y_dev = c->y_dev;
-  if (cudaPointerGetAttributes(&pa, y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-      pa.devicePointer)
-    y_dev = static_cast<float*>(pa.devicePointer);
-  else
+  // pinned (device-mapped) buffers are used in place: x is copied in by the
+  // graph's first kernel, y written by the combine straight into host memory
+  // over the bus. Pageable buffers go through device copies.
+  auto mapped = [](const void* p) -> const void* {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+      return pa.devicePointer;
     cudaGetLastError();
-  rc = desmoe_layer_forward(c, ex, w_r, c->x_dev, n, cfg, y_dev, c->host_tail_dev, stream);
+    return nullptr;
+  };
+  if (x_host != c->last_x_host) {
+    c->last_x_host = x_host;
+    c->last_x_mapped = mapped(x_host);
+  }
+  if (y_host != c->last_y_host) {
+    c->last_y_host = y_host;
+    c->last_y_mapped = static_cast<float*>(const_cast<void*>(mapped(y_host)));
+  }
+  const bool ingress = c->last_x_mapped && !std::getenv("DESMOE_HOST_MEMCPY");
+  float* y_dev = c->last_y_mapped ? c->last_y_mapped : c->y_dev;
+  if (ingress) {
+    const unsigned long long src = reinterpret_cast<unsigned long long>(c->last_x_mapped);
+    std::memcpy(c->host_tail + 8, &src, sizeof(src));
+  } else {
+    DESMOE_CUDA(cudaMemcpyAsync(c->x_dev, x_host, xb, cudaMemcpyHostToDevice, st));
+  }
+  const int call = ++c->host_calls;
+  reinterpret_cast<volatile int*>(c->host_tail)[5] = call;
+  rc = desmoe_layer_forward_host_graph(c, ex, w_r, n, cfg, y_dev, st, ingress);
   if (rc) return rc;
   if (y_dev == c->y_dev)
     DESMOE_CUDA(cudaMemcpyAsync(y_host, c->y_dev, yb, cudaMemcpyDeviceToHost, st));
-  rc = desmoe_check(c, stream);  // one synchronisation; stats and flag are host memory
+  if (y_dev != c->y_dev && !std::getenv("DESMOE_HOST_SYNC")) {
+    // y, stats and the data-check word are host memory the kernels write; the
+    // last combine CTA publishes the call number after a system fence. Spin on
+    // it (the earliest the results are observable); the stream is polled now
+    // and then so a failed launch reports its error instead of spinning.
+    volatile int* done = c->host_tail + 6;
+    for (unsigned spins = 1;; ++spins) {
+      if (*done == call) break;
+      if ((spins & 4095u) == 0) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) {
+          if (*done == call) break;
+          return fail(DESMOE_ECUDA, "layer finished without publishing its completion");
+        }
+        if (q != cudaErrorNotReady)
+          return fail(DESMOE_ECUDA, std::string("layer: ") + cudaGetErrorString(q));
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    volatile int* fw = c->host_tail + 4;
+    const int flag = *fw;
+    rc = DESMOE_OK;
+    if (flag) {
+      *fw = 0;
+      rc = flag == 2 ? fail(DESMOE_ECUDA, "expert-parallel exchange timed out (a peer rank stopped)")
+                     : fail(DESMOE_EINVAL, "non-finite logit");
+    }
+  } else {
+    rc = desmoe_check(c, stream);  // one synchronisation; stats and flag are host memory
+  }
   if (stats_host) std::memcpy(stats_host, const_cast<const int*>(c->host_tail), 4 * sizeof(int));
   return rc;
 }

@@ -1021,6 +1021,23 @@ __device__ __forceinline__ float4 combine4_rows(const float* ys, const int* e, c
   return acc;
 }
 
+// End of a combine CTA (thread 0, after the CTA barrier that follows its y
+// stores): the last CTA advances the call sequence and, for the host-buffer
+// entry, publishes the host's call number once every CTA's y rows are visible
+// system-wide (each CTA fences before it counts itself; fence cumulativity
+// over the barrier covers its other threads' stores).
+__device__ __forceinline__ void combine_retire(const CombineArgs& a) {
+  if (a.host_done) __threadfence_system();
+  if (atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
+    *a.done_ctas = 0;
+    atomicAdd(a.epoch, 1);
+    if (a.host_done) {
+      __threadfence_system();
+      *reinterpret_cast<volatile int*>(a.host_done) = *reinterpret_cast<const volatile int*>(a.host_call);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
   // before the FFN grid completes: the call's tag and this thread's route
   // (the front's tagged words; the previous call's sequence bump completed
@@ -1082,10 +1099,7 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
   for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 81, -1);
-  if (tid == 0 && atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
-    *a.done_ctas = 0;
-    atomicAdd(a.epoch, 1);
-  }
+  if (tid == 0) combine_retire(a);
 }
 
 __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
@@ -1130,10 +1144,59 @@ __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
   // (relaxed atomics suffice: each CTA's epoch read completed before its
   // increment; the bump is published by the kernel's completion)
   if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 81, -1);
-  if (threadIdx.x == 0 && atomicAdd(a.done_ctas, 1) == static_cast<int>(gridDim.x) - 1) {
-    *a.done_ctas = 0;
-    atomicAdd(a.epoch, 1);
-  }
+  if (threadIdx.x == 0) combine_retire(a);
+}
+
+// x ingress of the host-buffer entry: 16-byte loads from the caller's pinned
+// x over the bus, all of a thread's loads in flight at once, then the stores.
+// The front kernel (programmatic launch) prefetches its router weights and
+// sets up meanwhile; its griddepcontrol.wait orders it behind this copy.
+__global__ void __launch_bounds__(256) x_ingress_kernel(const unsigned long long* src_word,
+                                                        uint4* dst, int n16) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint4* src =
+      reinterpret_cast<const uint4*>(*reinterpret_cast<const volatile unsigned long long*>(src_word));
+  constexpr int kU = 4;
+  uint4 v[kU];
+  const int stride = gridDim.x * blockDim.x;
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kU; ++u)
+    if (i0 + u * stride < n16) v[u] = __ldcv(src + i0 + u * stride);
+#pragma unroll
+  for (int u = 0; u < kU; ++u)
+    if (i0 + u * stride < n16) dst[i0 + u * stride] = v[u];
+}
+
+// The same copy through the TMA engine: each CTA moves one chunk of
+// kIngressChunk bytes host -> shared (one bulk request, large bus reads) and
+// shared -> device x (one bulk store).
+__global__ void __launch_bounds__(32) x_ingress_bulk_kernel(const unsigned long long* src_word,
+                                                            uint4* dst, int n16, int chunk) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(128) unsigned char buf[];  // [chunk]
+  __shared__ __align__(8) uint64_t bar;
+  const size_t off = static_cast<size_t>(blockIdx.x) * chunk;
+  const size_t total = static_cast<size_t>(n16) * 16;
+  if (threadIdx.x != 0 || off >= total) return;
+  const uint32_t bytes = static_cast<uint32_t>(total - off < static_cast<size_t>(chunk) ? total - off : chunk);
+  const unsigned char* src =
+      reinterpret_cast<const unsigned char*>(*reinterpret_cast<const volatile unsigned long long*>(src_word));
+  mbar_init(&bar, 1);
+  fence_mbar_init();
+  mbar_arrive_expect_tx(&bar, bytes);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(buf)),
+      "l"(src + off), "r"(bytes), "r"(smem_u32(&bar))
+      : "memory");
+  mbar_wait(&bar, 0);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<unsigned char*>(dst) + off),
+               "r"(smem_u32(buf)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace desmoe

@@ -261,7 +261,21 @@ struct CombineArgs {
   const __nv_bfloat16* resid;  // optional residual stream added before the store (stacks)
   uint64_t* trace;           // optional timeline (events 80 start, 81 end; CTA 0)
   int trace_cap;
+  // host-buffer entry (desmoe_layer_forward_host): after every y row is
+  // visible system-wide the last CTA copies *host_call (the host's call
+  // number, host-mapped) into *host_done (host-mapped), which the host spins on
+  const int* host_call;
+  int* host_done;
 };
+
+// Host-buffer entry's x ingress, the first node of the layer graph: copies
+// the caller's pinned x (its device-mapped address is read from the
+// host-mapped word *src_word, written by the host before the launch, so the
+// graph never changes with the caller's buffer) into the context's device x.
+__global__ void x_ingress_kernel(const unsigned long long* src_word, uint4* dst, int n16);
+constexpr int kIngressChunk = 128 * 1024;  // max bytes per ingress CTA (one bulk request)
+__global__ void x_ingress_bulk_kernel(const unsigned long long* src_word, uint4* dst, int n16,
+                                      int chunk);
 
 // Comparison policies (baselines.cu): method 0 = top-k reduce, 1 = NAEE,
 // 2 = MC-MoE (score 0 = max gate, 1 = -entropy).

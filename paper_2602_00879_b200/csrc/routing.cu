@@ -390,6 +390,7 @@ cudaError_t set_kernel_smem_limits() {
   set(reinterpret_cast<const void*>(tile_gemm_kernel), 227 * 1024);
   set(reinterpret_cast<const void*>(ffn_persistent_kernel<2>), 227 * 1024);
   set(reinterpret_cast<const void*>(ffn_persistent_kernel<4>), 227 * 1024);
+  set(reinterpret_cast<const void*>(x_ingress_bulk_kernel), kIngressChunk);
   const cudaError_t f = set_fused_route_smem_limit(kFusedRouteSmem);
   const cudaError_t g = set_front_smem_limit();
   return e != cudaSuccess ? e : (f != cudaSuccess ? f : g);

@@ -243,6 +243,37 @@ def test_layer_host_entry_matches_device_entry():
     assert torch.equal(yh, y_dev.cpu())
 
 
+def test_host_entry_rotating_buffers(monkeypatch):
+    """Pinned x buffers that change every call (the in-graph ingress reads
+    the address from a host-mapped word: no re-capture), interleaved with
+    device-entry calls on the same context, the memcpy ingress
+    (DESMOE_HOST_MEMCPY) and the stream-synchronising return
+    (DESMOE_HOST_SYNC): every output equals the device entry's."""
+    m, d, f, n = 64, 512, 512, 32
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=71)
+    layer = DesMoeLayer(LayerConfig(m, 8, d, f, strategy="vote", vote_beta=0.4),
+                        synth.router_weights(m, d, seed=72), wg, wu, wd, own_context=True)
+    xs = [synth.hidden_states(n, d, seed=80 + i, rho=0.3) for i in range(6)]
+    want = []
+    for x in xs:
+        want.append(layer.forward(x).cpu())
+        torch.cuda.synchronize()
+    xh = [x.cpu().pin_memory() for x in xs]
+    yh = torch.empty((n, d), dtype=torch.float32).pin_memory()
+    sh = torch.empty(4, dtype=torch.int32).pin_memory()
+    for mode in ("", "DESMOE_HOST_MEMCPY", "DESMOE_HOST_SYNC"):
+        if mode:
+            monkeypatch.setenv(mode, "1")
+        for rep in range(2):
+            for i in range(len(xs)):
+                layer.forward_host(xh[i], yh, sh)
+                assert torch.equal(yh, want[i]), (mode, rep, i)
+                if i % 3 == 0:  # a device-entry call in between (another graph)
+                    assert torch.equal(layer.forward(xs[i]).cpu(), want[i])
+        if mode:
+            monkeypatch.delenv(mode)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("strategy", ["vote", "vanilla"])
 def test_stack_equals_chained_layers(strategy):

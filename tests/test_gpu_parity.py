@@ -134,7 +134,23 @@ def vote_tie_at_boundary(ref, n, m, k, beta, seed):
         order = sorted(range(m), key=lambda e: (-votes[e], e))
         if votes[order[m_core - 1]] == votes[order[m_core]]:
             return L
-    pytest.skip("could not place a vote tie at the boundary")
+    return constructed_vote_tie(n, m, k, m_core, seed)
+
+
+def constructed_vote_tie(n, m, k, m_core, seed):
+    """Every token routes the same row (as at rho = 1): its value order is a
+    random permutation of the experts, with the experts at vote ranks
+    m_core - 1 and m_core given the same logit. For m_core < k both are in
+    every token's top-K, so their votes are equal and non-zero; otherwise
+    only k experts get votes and the boundary tie is between zero-vote
+    experts (filled by lowest index, des.cpp:93)."""
+    rng = np.random.default_rng(seed)
+    vals = np.sort(rng.uniform(-2.0, 2.0, size=m))[::-1].astype(np.float32)
+    vals[m_core] = vals[m_core - 1]
+    perm = rng.permutation(m)
+    row = np.empty(m, np.float32)
+    row[perm] = vals
+    return np.tile(row, (n, 1))
 
 
 # ---- cases ------------------------------------------------------------------------
@@ -182,6 +198,21 @@ def test_vote_ties_at_coreset_boundary(ref, n, m, k, act):
     L = vote_tie_at_boundary(ref, n, m, k, beta, seed=n + m)
     got = check_case(ref, L, k, "vote", beta=beta, act=act)
     assert len(got["members"]) == ref.vote_budget(beta, m)
+
+
+@pytest.mark.parametrize("n,m,k,m_core", [(32, 64, 8, 5), (32, 64, 8, 25), (64, 256, 8, 7),
+                                           (64, 256, 8, 38), (200, 128, 16, 12)])
+@pytest.mark.parametrize("act", [0, 1])
+def test_constructed_vote_ties(ref, n, m, k, m_core, act):
+    """Exactly equal votes at the coreset boundary, non-zero (m_core < K) and
+    zero (m_core > K: lowest-index fill)."""
+    beta = (m_core + 0.5) / m
+    L = constructed_vote_tie(n, m, k, m_core, seed=m_core)
+    mem, votes = ref.vote_coreset(L.astype(np.float64), k, beta, act=act)
+    order = sorted(range(m), key=lambda e: (-votes[e], e))
+    assert votes[order[m_core - 1]] == votes[order[m_core]]  # the tie is at the boundary
+    got = check_case(ref, L, k, "vote", beta=beta, act=act)
+    assert len(got["members"]) == m_core
 
 
 @pytest.mark.parametrize("n,m,k", [(32, 64, 8), (128, 256, 8)])

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--json", default="")
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm before the traced call")
     ap.add_argument("--block", type=int, default=0, help="override the block size N")
+    ap.add_argument("--ffn", type=int, default=0, help="override the expert width F")
     ap.add_argument("--raw", default="", help="also save the raw records (.npz) for offline analysis")
     args = ap.parse_args()
     import torch
@@ -34,6 +35,8 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.block:
         cfg["block"] = args.block
+    if args.ffn:
+        cfg["ffn"] = args.ffn
     n, m, k, d, f = cfg["block"], cfg["experts"], cfg["top_k"], cfg["hidden"], cfg["ffn"]
     wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1000)
     wr = synth.router_weights(m, d, seed=2000)
