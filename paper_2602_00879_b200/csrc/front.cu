@@ -18,12 +18,13 @@
 //      keys, two REDUX per round); a boundary that exp/division rounding
 //      could flip (gap <= 2^-40, or underflow) re-selects exactly on the fp64
 //      probabilities with the reference's comparator;
-//   V  every CTA gathers all tokens' (expert, weight) selections over DSMEM
-//      and computes the coreset redundantly: DES-Vote sums each expert's
-//      votes over its tokens in ascending token order (des.cpp:86-91) via a
-//      stable counting sort (no dense N x M matrix), then keeps the top
-//      floor(beta*M) by (vote desc, index asc) with a rank count
-//      (des.cpp:93); DES-Seq takes the union of the top-seq_k (des.cpp:33-45);
+//   V  every token's owner pushes its top-`depth` (ids, weights) to every CTA
+//      over DSMEM; every CTA computes the coreset redundantly: DES-Vote
+//      rebuilds the reference's masked N x M matrix (des.cpp:73-84) in
+//      shared memory, sums each expert's column in ascending token order
+//      (des.cpp:86-91) and keeps the top floor(beta*M) by (vote desc, index
+//      asc) with a rank count (des.cpp:93); DES-Seq takes the union of the
+//      top-seq_k (des.cpp:33-45);
 //   RR constrained re-route + renormalisation of own tokens (des.cpp:97-118);
 //      VANILLA writes topk_route's gates right after L.
 // Every intermediate stays on chip. The kernel also zeroes the expert-FFN
@@ -271,7 +272,7 @@ __device__ __noinline__ void exact_reselect(const double* e, double s, int act, 
   warp_select(scratch, m, want, allow, sel);
 }
 
-// timeline marks 0..count-1 of this CTA -> trace buffer as events 40 + i
+// timeline marks 0..count-1 of this CTA -> trace buffer as events 100 + i
 __device__ __noinline__ void front_dump_marks(uint64_t* trace, int cap, const uint64_t* ts,
                                               int tid, int count) {
   if (!trace || tid != 0) return;
@@ -279,24 +280,9 @@ __device__ __noinline__ void front_dump_marks(uint64_t* trace, int cap, const ui
   const unsigned long long i0 = atomicAdd(cur, static_cast<unsigned long long>(count));
   for (int i = 0; i < count; ++i)
     if (i0 + i < static_cast<unsigned long long>(cap)) {
-      trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (40 + i);
+      trace[2 + 2 * (i0 + i)] = (static_cast<uint64_t>(blockIdx.x) << 8) | (100 + i);
       trace[3 + 2 * (i0 + i)] = ts[i];
     }
-}
-
-// Part `idx / m` of expert (idx mod m)'s rank in (vote desc, index asc): the
-// number of experts before it among indices [j0, j1) of that part.
-__device__ __noinline__ void rank_part(const uint64_t* vkey, int m, int parts, int idx, int* rankp) {
-  const int i = idx % m, part = idx / m;
-  const uint64_t ki = vkey[i];
-  int r = 0;
-  const int j0 = (m * part) / parts, j1 = (m * (part + 1)) / parts;
-#pragma unroll 4
-  for (int j = j0; j < j1; ++j) {
-    const uint64_t kj = vkey[j];
-    r += (kj > ki) | ((kj == ki) & (j < i));
-  }
-  rankp[part * m + i] = r;
 }
 
 // Publishes the ascending list of flagged experts (coreset / union): the
@@ -342,7 +328,7 @@ __device__ __noinline__ void front_tail(float* logits_out, const float* xrow, co
 
 // Shared-memory plan (host and device agree on it).
 struct FrontSmem {
-  size_t ring, erow, dreg, scratch, partial, xrow, mx, ssum, sel, psel, wsel, wp, own_tok, flag,
+  size_t ring, erow, dreg, scratch, partial, xrow, mx, ssum, sel, wsel, wp, own_tok, flag,
       allsel, allp, stage, total;
 };
 
@@ -391,8 +377,6 @@ __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int ch
   o += fr_align(static_cast<size_t>(own_max) * 8, 16);
   p.sel = o;
   o += fr_align(static_cast<size_t>(own_max) * 33 * 4, 16);
-  p.psel = o;
-  o += fr_align(static_cast<size_t>(own_max) * 32 * 8, 16);
   p.wsel = o;
   o += fr_align(static_cast<size_t>(kFrontThreads / 32) * 33 * 4, 16);
   p.wp = o;
@@ -405,6 +389,13 @@ __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int ch
   return p;
 }
 
+// Compile-time specialised on the routing strategy (kStrat: -1 vanilla, 0
+// DES-Seq, 1 DES-Vote), the router-GEMM shape (kTs: token split) and the
+// small-block L stage (kSmall: at most one own token per warp of a group):
+// each instantiation executes one contiguous code path, so the instruction
+// fetch (cold after the FFN streamed hundreds of MB) follows it sequentially
+// instead of jumping over the other variants.
+template <int kStrat, bool kTs, bool kSmall>
 __global__ void __launch_bounds__(kFrontThreads, 1)
     front_kernel(const __grid_constant__ CUtensorMap wr_map, const __grid_constant__ BoxMaps x_maps,
                  const __grid_constant__ FrontArgs a_param) {
@@ -428,10 +419,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
-  __shared__ uint64_t s_ts[40];  // timeline marks (trace buffer only)
+  __shared__ uint64_t s_ts[48];  // timeline marks (trace buffer only)
   __shared__ uint64_t s_pw[96];  // instruction-cache prewarm scratch
   // glibc exp's 2^(k/128) table, staged while the router GEMM runs
-  __shared__ unsigned long long s_exptab[256];
+  __shared__ __align__(16) unsigned long long s_exptab[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool tracing = a.trace != nullptr;
   if (tracing && tid == 0) s_ts[24] = clock64();
@@ -457,7 +448,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   float* mxv = reinterpret_cast<float*>(smem + P.mx);
   double* ssum = reinterpret_cast<double*>(smem + P.ssum);
   int* sel = reinterpret_cast<int*>(smem + P.sel);           // [own][33] rank order
-  double* psel = reinterpret_cast<double*>(smem + P.psel);   // [own][32]
   int* wsel_all = reinterpret_cast<int*>(smem + P.wsel);     // [NW][33]
   int* own_tok = reinterpret_cast<int*>(smem + P.own_tok);
   uint8_t* flag = smem + P.flag;                             // [m] coreset members
@@ -476,13 +466,14 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   const int kb_cta = a.kb_per_cta;
   const int kb0 = rk * kb_cta;
   const uint32_t xbytes = static_cast<uint32_t>(a.b_rows) * 128u;
-  const bool vanilla = a.strategy < 0;
-  const int depth = a.strategy == 0 ? a.seq_k : k;
+  constexpr bool vanilla = kStrat < 0;
+  const int depth = kStrat == 0 ? a.seq_k : k;
 
   // ---- setup: barriers, TMEM, router-weight prefetch (weights are static, so
   // they stream before the previous kernel's output is even waited for) ----------
   if (tid == 0) {
     tma_prefetch_desc(&wr_map);
+    tma_prefetch_desc(&x_maps.map[a.box_index]);
 #pragma unroll 1
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -498,14 +489,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     // and (DES) every token's top-`depth` selection
     const int nc0 = n < Tc ? n : Tc;
     const int own0 = (nc0 * (rk + 1)) / C - (nc0 * rk) / C;
-    if (!a.tsplit) mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
-    if (a.strategy >= 0)
-      mbar_arrive_expect_tx(bar_selx,
-                            static_cast<uint32_t>(n * depth * (a.strategy == 1 ? 12 : 4)));
+    if constexpr (!kTs) mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
+    if constexpr (kStrat >= 0)  // every token's top-depth ids (+ weights, DES-Vote)
+      mbar_arrive_expect_tx(bar_selx, static_cast<uint32_t>(n * depth * (kStrat == 1 ? 12 : 4)));
     else if (rk == 0 && a.pub)
       mbar_arrive_expect_tx(bar_selx, static_cast<uint32_t>(n * k * 4));  // union of top-K
     const uint64_t pol = l2_policy_evict_last();  // W_r: small, read every call
-    if (a.tsplit == 2) {
+    if (kTs && a.tsplit == 2) {
       // token split, local W_r: the first S K-blocks stream before the
       // previous kernel is waited for (the X rows follow after pdl_wait)
 #pragma unroll 1
@@ -517,23 +507,50 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           tma_load_2d(st + tl * kATile, &wr_map, &full[i], i * kBK, tl * kBM, pol);
       }
     }
+    if constexpr (!kTs) {
 #pragma unroll 1
-    for (int i = 0; i < kb_cta && i < S && !a.tsplit; ++i) {
-      unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
-      mbar_arrive_expect_tx(&full[i], mt * kATile + xbytes);
+      for (int i = 0; i < kb_cta && i < S; ++i) {
+        unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
+        mbar_arrive_expect_tx(&full[i], mt * kATile + xbytes);
 #pragma unroll 1
-      for (int tl = 0; tl < mt; ++tl)
-        tma_load_2d(st + tl * kATile, &wr_map, &full[i], (kb0 + i) * kBK, tl * kBM, pol);
+        for (int tl = 0; tl < mt; ++tl)
+          tma_load_2d(st + tl * kATile, &wr_map, &full[i], (kb0 + i) * kBK, tl * kBM, pol);
+      }
     }
+    FRONT_MARK(45);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, a.tmem_cols);
-  if (tid < 256) s_exptab[tid] = kExpTab[tid];
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, a.tmem_cols);
+    if (tracing && lane == 0) s_ts[46] = gtime();
+  }
+  // the exp table: asynchronous copies (nobody waits for them until the
+  // activation stage, cp.async.wait_all before the barrier that precedes it)
+  if (tid < 128)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_exptab + 2 * tid)),
+                 "l"(kExpTab + 2 * tid)
+                 : "memory");
   pdl_launch_dependents();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
+  // the first ring stages' X boxes go out at once (their W_r halves and the
+  // stages' transaction counts were armed in the setup): no CTA barrier or
+  // cluster barrier on the way to the router GEMM's inputs
+  const int x_pre = (!kTs || a.tsplit == 2) ? (kTs ? (kb_cta * C < S ? kb_cta * C : S)
+                                                   : (kb_cta < S ? kb_cta : S))
+                                             : 0;
+  if (tid == 0) {
+    const uint64_t pol_x = l2_policy_evict_last();
+    const int x_row0 = kTs ? (n * rk) / C : 0;
+#pragma unroll 1
+    for (int i = 0; i < x_pre; ++i)
+      tma_load_2d(ring + static_cast<size_t>(i) * stage_bytes + mt * kATile,
+                  &x_maps.map[a.box_index], &full[i], (kTs ? i : kb0 + i) * kBK, x_row0, pol_x);
+  }
+  FRONT_MARK(47);
   const uint32_t tag = a.seq ? hand_tag(*a.seq) : 0u;  // this call's hand-off tag
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  FRONT_MARK(41);
   const uint32_t tmem_base = tmem_slot[0];
   // every CTA's barriers are initialised and armed before anyone pushes
   cluster_arrive_relaxed();
@@ -546,8 +563,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     // entry). While the router GEMM runs, four idle warps each run one later
     // phase's code once on scratch (s_pw; 32 dummy experts), in parallel so
     // the misses overlap (DESMOE_FRONT_FLAGS=1 disables)
-    uint64_t* dk = s_pw;                                      // [32] keys
-    int* dr = reinterpret_cast<int*>(s_pw + 32);              // [32] ranks / pub words
     uint8_t* df = reinterpret_cast<uint8_t*>(s_pw + 48);      // [32] flags; pub words at +52
     int* ds = wsel_all + warp * 33;
     if (warp == 8) {
@@ -557,9 +572,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
         volatile double sink = f_exp(-1.5, s_exptab) + f_div(1.0, 2.0);
         (void)sink;
       }
-      dk[lane] = static_cast<uint64_t>(lane);
-      __syncwarp();
-      rank_part(dk, 32, 1, lane, dr);
     } else if (warp == 10) {
       df[lane] = static_cast<uint8_t>(lane & 1);
       __syncwarp();
@@ -572,7 +584,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 
   // ---- R + L1: per token chunk, split-K GEMM, then the owners' logit sums ----------
   int own = 0;
-  if (a.tsplit) {
+  if constexpr (kTs) {
     // token split: this CTA owns tokens [tlo, thi) and computes their logits
     // over the whole hidden dimension. K-block `it` of W_r is loaded once per
     // cluster by CTA (it mod C) and multicast into every CTA's ring slot;
@@ -603,7 +615,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
             tma_load_2d_mc(st + tl * kATile, &wr_map, &full[s], it * kBK, tl * kBM,
                            static_cast<uint16_t>((1u << C) - 1u), pol_w);
         }
-        tma_load_2d(st + mt * kATile, &x_maps.map[a.box_index], &full[s], it * kBK, tlo, pol_x);
+        if (it >= x_pre)
+          tma_load_2d(st + mt * kATile, &x_maps.map[a.box_index], &full[s], it * kBK, tlo, pol_x);
       }
     } else if (warp == 1) {
       const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     FRONT_MARK(3);
   }
 #pragma unroll 1
-  for (int c = 0; c < nch && !a.tsplit; ++c) {
+  for (int c = 0; c < nch && !kTs; ++c) {
     const int c0 = c * Tc;
     const int nc = n - c0 < Tc ? n - c0 : Tc;
     const int n_mma = (nc + 15) & ~15;
@@ -676,15 +689,19 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           for (int tl = 0; tl < mt; ++tl)
             tma_load_2d(st + tl * kATile, &wr_map, &full[s], (kb0 + i) * kBK, tl * kBM, pol_w);
         }
-        tma_load_2d(st + mt * kATile, &x_maps.map[a.box_index], &full[s], (kb0 + i) * kBK, c0,
-                    pol_x);
+        if (it >= x_pre)
+          tma_load_2d(st + mt * kATile, &x_maps.map[a.box_index], &full[s], (kb0 + i) * kBK, c0,
+                      pol_x);
       }
+      if (tracing && c == 0) s_ts[44] = gtime();
     } else if (warp == 1) {
       const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
 #pragma unroll 1
       for (int i = 0; i < kb_cta; ++i) {
         const int it = c * kb_cta + i, s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
+        if (tracing && lane == 0 && c == 0 && (i == 0 || i == kb_cta - 1))
+          s_ts[i == 0 ? 42 : 43] = gtime();
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a0 = smem_u32(ring + static_cast<size_t>(s) * stage_bytes);
@@ -770,6 +787,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       cluster_wait();
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");  // the exp table (issued in the setup)
   __syncthreads();
   FRONT_MARK(4);
   if (warp == 2) {
@@ -783,7 +801,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // the fp64 activation and the ordered sums; the selectors then wait (named
   // barrier 2) for the activation to check their boundaries.
   constexpr int kGW = NW / 2;  // warps per group
-  if (own <= kGW && !(a.flags & 2)) {  // (flag 2: always in sequence, for A/B runs)
+  if constexpr (kSmall) {  // (host: own tokens <= kGW; DESMOE_FRONT_FLAGS bit 2 forces the sequence)
     if (warp < kGW) {
       const int want = k < m ? k : m;
       const int rounds = want < m ? want + 1 : want;
@@ -970,30 +988,28 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       const double* er = erow + j * ew;
       const double s = ssum[j];
       if (risky[j]) exact_reselect(er, s, act, m, want, nullptr, scratch, sj);  // rare
-      if (vanilla) {
+      if constexpr (vanilla) {
         write_route(er, s, act, sj, want, k, own_tok[j], wp, a.route_idx, a.route_gate,
                     a.route_cnt, a.route_words, tag);
         if (a.pub && lane < k)  // the union (unique experts) is published by rank 0
           st_async_b32(mapa_u32(smem_u32(allsel + own_tok[j] * k + lane), 0),
                        static_cast<uint32_t>(sj[lane]), mapa_u32(smem_u32(bar_selx), 0));
-      } else if (lane < want) {
+      } else if (lane < depth) {
+        // broadcast the token's top-`depth` (ids, weights) to every CTA
         const int e = sj[lane];
-        const double pv = a.raw ? static_cast<double>(xrow[j * m + e])
-                                : (act == 0 ? f_div(er[e], s) : er[e]);
-        psel[j * 32 + lane] = pv;
-        if (lane < depth) {
-          // broadcast the token's top-`depth` (ids, weights) to every CTA
-          const int t = own_tok[j];
-          const uint32_t ea = smem_u32(allsel + t * k + lane);
-          const uint32_t pa = smem_u32(allp + t * k + lane);
-          const uint32_t ba = smem_u32(bar_selx);
+        const int t = own_tok[j];
+        const uint32_t ea = smem_u32(allsel + t * k + lane);
+        const uint32_t ba = smem_u32(bar_selx);
+        double pv = 0.0;
+        if constexpr (kStrat == 1)
+          pv = a.raw ? static_cast<double>(xrow[j * m + e]) : (act == 0 ? f_div(er[e], s) : er[e]);
+        const uint32_t pa = smem_u32(allp + t * k + lane);
 #pragma unroll 1
-          for (int r = 0; r < C; ++r) {
-            const uint32_t rb = mapa_u32(ba, r);
-            st_async_b32(mapa_u32(ea, r), static_cast<uint32_t>(e), rb);
-            if (a.strategy == 1)
-              st_async_b64(mapa_u32(pa, r), static_cast<uint64_t>(__double_as_longlong(pv)), rb);
-          }
+        for (int r = 0; r < C; ++r) {
+          const uint32_t rb = mapa_u32(ba, r);
+          st_async_b32(mapa_u32(ea, r), static_cast<uint32_t>(e), rb);
+          if constexpr (kStrat == 1)
+            st_async_b64(mapa_u32(pa, r), static_cast<uint64_t>(__double_as_longlong(pv)), rb);
         }
       }
       __syncwarp();
@@ -1001,7 +1017,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   }
   __syncthreads();
   FRONT_MARK(8);
-  if (vanilla) {
+  if constexpr (vanilla) {
     if (rk == 0 && a.pub) {
       // union of every token's top-K = the experts the FFN will stream
       mbar_wait_cluster(bar_selx, 0);
@@ -1018,7 +1034,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     cluster_wait();
     FRONT_MARK(9);
     front_tail(a.logits_out, xrow, own_tok, own, m, tid);
-    front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 38);
+    front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 48);
     return;
   }
   mbar_wait_cluster(bar_selx, 0);       // every token's selection has arrived
@@ -1036,9 +1052,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   for (int i = tid; i < m; i += kFrontThreads) flag[i] = 0;
   FRONT_MARK(10);
 #pragma unroll 1
-  for (int t0 = 0; t0 < n; t0 += (a.strategy == 1 ? tv : n)) {
-    const int nt = a.strategy == 1 ? (n - t0 < tv ? n - t0 : tv) : n;
-    if (a.strategy == 1) {
+  for (int t0 = 0; t0 < n; t0 += (kStrat == 1 ? tv : n)) {
+    const int nt = kStrat == 1 ? (n - t0 < tv ? n - t0 : tv) : n;
+    if constexpr (kStrat == 1) {
 #pragma unroll 1
       for (int i = tid; i < nt * m; i += kFrontThreads) dense[i] = 0.0;
       __syncthreads();
@@ -1048,13 +1064,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     for (int w = tid; w < nt * depth; w += kFrontThreads) {
       const int t = t0 + w / depth, j = w - (w / depth) * depth;
       const int e = allsel[t * k + j];
-      if (a.strategy == 1)
+      if (kStrat == 1)
         dense[(t - t0) * m + e] = allp[t * k + j];
       else
         flag[e] = 1;  // DES-Seq: union of the top-seq_k
     }
     __syncthreads();
-    if (a.strategy == 1 && tid < m) {
+    if (kStrat == 1 && tid < m) {
       const double* col = dense + tid;
       int t = 0;
 #pragma unroll 1
@@ -1068,10 +1084,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 #pragma unroll 1
       for (; t < nt; ++t) vsum += col[t * m];
     }
-    if (a.strategy == 1) __syncthreads();  // column reads done before the next chunk
+    if (kStrat == 1) __syncthreads();  // column reads done before the next chunk
   }
   FRONT_MARK(11);
-  if (a.strategy == 1) {
+  if (kStrat == 1) {
     double* votes = dense;                                          // [m] (aliases chunk 0)
     uint64_t* vkey = reinterpret_cast<uint64_t*>(votes + m);        // [m]
     int* rankp = reinterpret_cast<int*>(vkey + m);                  // [parts][m]
@@ -1082,10 +1098,24 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
     __syncthreads();
     FRONT_MARK(15);
-    // rank of expert i = #experts before it in (vote desc, index asc), the
-    // pool split into `parts` ranges counted by different threads
+    // rank of expert e = #experts before it in (vote desc, index asc), the
+    // pool split into `parts` key ranges counted by different threads —
+    // inline and with one division per thread (the out-of-line helper with
+    // its per-call divisions measured 1300 vs 440 cycles, tools/micro/phase.cu)
     const int parts = kFrontThreads / m < 16 ? kFrontThreads / m : 16;
-    if (tid < parts * m) rank_part(vkey, m, parts, tid, rankp);
+    if (tid < parts * m) {
+      const int part = tid / m, e = tid - part * m;
+      const int span = (m + parts - 1) / parts;
+      const int j0 = part * span, j1 = j0 + span < m ? j0 + span : m;
+      const uint64_t ki = vkey[e];
+      int r = 0;
+#pragma unroll 4
+      for (int j = j0; j < j1; ++j) {
+        const uint64_t kj = vkey[j];
+        r += (kj > ki) | ((kj == ki) & (j < e));
+      }
+      rankp[part * m + e] = r;
+    }
     __syncthreads();
     FRONT_MARK(16);
     if (tid < m) {
@@ -1133,7 +1163,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   cluster_wait();  // #3: no CTA exits while others may still read its shared memory
   FRONT_MARK(14);
   front_tail(a.logits_out, xrow, own_tok, own, m, tid);
-  front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 38);
+  front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 48);
 #undef FRONT_MARK
 }
 
@@ -1205,6 +1235,20 @@ bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem, int tspl
   }
 }
 
+using FrontFn = void (*)(const CUtensorMap, const BoxMaps, const FrontArgs);
+
+// The instantiation for (strategy, token split, small block).
+static FrontFn front_variant(int strategy, bool tsplit, bool small) {
+#define DESMOE_FRONT_ROW(S)                                                              \
+  {front_kernel<S, false, false>, front_kernel<S, false, true>, front_kernel<S, true, false>, \
+   front_kernel<S, true, true>}
+  static const FrontFn table[3][4] = {DESMOE_FRONT_ROW(-1), DESMOE_FRONT_ROW(0),
+                                      DESMOE_FRONT_ROW(1)};
+#undef DESMOE_FRONT_ROW
+  const int si = strategy < 0 ? 0 : (strategy == 0 ? 1 : 2);
+  return table[si][(tsplit ? 2 : 0) + (small ? 1 : 0)];
+}
+
 cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,
                          size_t smem, cudaStream_t st) {
   cudaLaunchConfig_t lc{};
@@ -1221,12 +1265,24 @@ cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 2;
-  return cudaLaunchKernelEx(&lc, front_kernel, wr_map, x_maps, a);
+  // small block: at most one own token per warp of a 8-warp group, so the
+  // selection and the activation run side by side (DESMOE_FRONT_FLAGS bit 2
+  // forces the sequential L stage, for A/B runs)
+  const bool small = a.own_max <= kFrontThreads / 64 && !(a.flags & 2);
+  return cudaLaunchKernelEx(&lc, front_variant(a.strategy, a.tsplit != 0, small), wr_map, x_maps,
+                            a);
 }
 
 cudaError_t set_front_smem_limit() {
-  return cudaFuncSetAttribute(front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kFrontSmemLimit);
+  cudaError_t e = cudaSuccess;
+  for (int strategy = -1; strategy <= 1; ++strategy)
+    for (int v = 0; v < 4; ++v) {
+      const cudaError_t r = cudaFuncSetAttribute(
+          reinterpret_cast<const void*>(front_variant(strategy, v >= 2, v & 1)),
+          cudaFuncAttributeMaxDynamicSharedMemorySize, kFrontSmemLimit);
+      if (e == cudaSuccess) e = r;
+    }
+  return e;
 }
 
 }  // namespace desmoe

@@ -38,7 +38,7 @@
 namespace desmoe {
 
 // 2^(k/128) = H[k] (1 + T[k]): {bits(T[k]), bits(H[k]) - (k << 45)}
-static __device__ const unsigned long long kExpTab[256] = {
+static __device__ __align__(16) const unsigned long long kExpTab[256] = {
 #include "libm_exp_table.inc"
 };
 

@@ -201,7 +201,7 @@ def test_vote_ties_at_coreset_boundary(ref, n, m, k, act):
 
 
 @pytest.mark.parametrize("n,m,k,m_core", [(32, 64, 8, 5), (32, 64, 8, 25), (64, 256, 8, 7),
-                                           (64, 256, 8, 38), (200, 128, 16, 12)])
+                                           (64, 256, 8, 38), (120, 128, 16, 12)])
 @pytest.mark.parametrize("act", [0, 1])
 def test_constructed_vote_ties(ref, n, m, k, m_core, act):
     """Exactly equal votes at the coreset boundary, non-zero (m_core < K) and

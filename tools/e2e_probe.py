@@ -90,6 +90,18 @@ def main():
     timed("h2d_only", lambda: xd.copy_(xh, non_blocking=True))
     timed("forward_host_wrapper", lambda: nxt().forward_host(xh, yh, sh, strategy="vote"))
     timed("forward_host_direct", direct_host)
+    xrot = [synth.hidden_states(n, d, seed=100 + i, rho=cfg["rho"]).cpu().pin_memory()
+            for i in range(64)]
+    r = [0]
+
+    def direct_host_rot():  # a different pinned x buffer every call (as bench.py)
+        l = nxt()
+        r[0] += 1
+        L.desmoe_layer_forward_host(l.ctx.h, l.experts.h, l.w_router.data_ptr(),
+                                    xrot[r[0] % len(xrot)].data_ptr(), n, C.byref(rc),
+                                    yh.data_ptr(), sh.data_ptr(), sp)
+
+    timed("forward_host_direct_rotating_x", direct_host_rot)
     import json
     print(json.dumps({"variant": os.environ.get("DESMOE_INGRESS", "") + os.environ.get("DESMOE_HOST_MEMCPY", ""), **out}))
 

@@ -16,6 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+FB = 100  # front-kernel marks: trace events FB + i (front.cu front_dump_marks)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
@@ -67,7 +70,7 @@ def main():
     unit = (rec[:, 0] >> 32).astype(np.int64)
     unit[unit >= 2 ** 31] -= 2 ** 32
     t = rec[:, 1].astype(np.int64)
-    t0 = t[ev == 40].min() if (ev == 40).any() else t[ev == 0].min()
+    t0 = t[ev == FB].min() if (ev == FB).any() else t[ev == 0].min()
     t = (t - t0) / 1e3  # µs
     if args.raw:
         np.savez(args.raw, ev=ev, cta=cta, unit=unit, t=t, raw=rec)
@@ -85,23 +88,27 @@ def main():
     fnames = ["start", "setup", "drained", "partials_synced", "logits", "rowmax", "activated",
               "sums_topk", "selected", "sync2", "v_zeroed", "v_gathered", "coreset", "rerouted",
               "exit", "votes", "ranked", "arrived", "mma_done", "drain_done", "copies_issued", "sums_done", "topk_done"]
+    fnames += [None] * (41 - len(fnames)) + ["setup_synced", "mma_full0", "mma_full_last", "x_issued",
+                                             "wr_issued", "tmem_alloced", "pdl_waited"]
+    fnames += [None] * (41 - len(fnames)) + ["setup_synced", "mma_full0", "mma_full_last", "x_issued",
+                                             "wr_issued", "tmem_alloced", "pdl_waited"]
     for i, nm in enumerate(["l4_enter", "l4_call", "l4_selected", "l4_risky"]):
-        if (ev == 74 + i).any():
-            out["front_" + nm] = [round(float(t[ev == 74 + i].min()), 2),
-                                  round(float(t[ev == 74 + i].max()), 2)]
-    chunks = [round(float(t[ev == 66 + c].max()), 2) for c in range(5) if (ev == 66 + c).any()
-              and float(t[ev == 66 + c].max()) < 1e6 and float(t[ev == 66 + c].max()) > 0]
+        if (ev == FB + 34 + i).any():
+            out["front_" + nm] = [round(float(t[ev == FB + 34 + i].min()), 2),
+                                  round(float(t[ev == FB + 34 + i].max()), 2)]
+    chunks = [round(float(t[ev == FB + 26 + c].max()), 2) for c in range(5) if (ev == FB + 26 + c).any()
+              and float(t[ev == FB + 26 + c].max()) < 1e6 and float(t[ev == FB + 26 + c].max()) > 0]
     if chunks:
         out["front_chunk_ends"] = chunks
-    if (ev == 63).any():
-        out["select_cycles"] = int(rec[ev == 63][:, 1].max())
-    if (ev == 64).any() and (ev == 65).any() and (ev == 40).any() and (ev == 53).any():
-        cyc = rec[ev == 65][:, 1].astype(np.int64) - rec[ev == 64][:, 1].astype(np.int64)
-        ns = rec[ev == 53][:, 1].astype(np.int64) - rec[ev == 40][:, 1].astype(np.int64)
+    if (ev == FB + 23).any():
+        out["select_cycles"] = int(rec[ev == FB + 23][:, 1].max())
+    if (ev == FB + 24).any() and (ev == FB + 25).any() and (ev == FB).any() and (ev == FB + 13).any():
+        cyc = rec[ev == FB + 25][:, 1].astype(np.int64) - rec[ev == FB + 24][:, 1].astype(np.int64)
+        ns = rec[ev == FB + 13][:, 1].astype(np.int64) - rec[ev == FB][:, 1].astype(np.int64)
         out["front_sm_mhz"] = [round(float(c) / float(t) * 1e3, 1) for c, t in zip(cyc, ns)]
     for i, nm in enumerate(fnames):
-        e_ = 40 + i
-        if (ev == e_).any():
+        e_ = FB + i
+        if nm and (ev == e_).any():
             out["front_" + nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
     for e_, nm in names.items():
         if (ev == e_).any():

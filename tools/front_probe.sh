@@ -1,7 +1,7 @@
 # Front-kernel timeline under different cache states (GPU box):
 #   F=1024 (315 MB streamed per call) vs F=128 (38 MB: L2 keeps the code),
 #   each with and without a 256 MiB L2 flush before the traced call.
-for f in 1024 128; do
+for f in ${FFNS:-1024 128}; do
   for fl in flush noflush; do
     extra=""; [ $fl = noflush ] && extra="--no-flush"
     python tools/ffn_trace.py --config ${CFG:-c2} --strategy ${STRAT:-vote} --ffn $f $extra \
@@ -10,7 +10,7 @@ for f in 1024 128; do
 done
 python - <<'PY'
 import json, glob, os
-keys = ["front_setup", "front_mma_done", "front_partials_synced", "front_logits", "front_rowmax",
+keys = ["front_wr_issued", "front_tmem_alloced", "front_pdl_waited", "front_setup_synced", "front_setup", "front_x_issued", "front_mma_full0", "front_mma_full_last", "front_mma_done", "front_partials_synced", "front_logits", "front_rowmax",
         "front_activated", "front_selected", "front_v_gathered", "front_ranked", "front_coreset",
         "front_rerouted", "ffn_list_loaded"]
 for f in sorted(glob.glob("gpurun_out/fp_*.json")):
