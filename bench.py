@@ -416,17 +416,24 @@ def main():
     v, van = summ["vote"], summ["vanilla"]
     ffn_us = v["phase_us"]["expert_ffn"]
     achieved = v["experts_streamed_rank0"] * wbytes_per_expert / (ffn_us * 1e-6) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     if ws == 1 and not args.block:
-        # DRAM bytes of this kernel on this workload from the committed ncu
-        # --set full capture (tools/ncu_capture.sh -> tools/ncu_summary.py)
-        import glob
-        caps = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{args.config}_r*.json")))
-        if caps:
-            try:
-                traffic = json.load(open(caps[-1])).get("ffn_dram_bytes_per_block")
-            except Exception:
-                traffic = None
+        # DRAM bytes of this kernel on this workload from the ncu --set full
+        # capture of the CURRENT profile tag (profiles/LATEST, written with the
+        # captures by tools/ncu_capture.sh -> tools/ncu_summary.py); a missing
+        # capture for that tag is reported, never silently replaced by an
+        # older one
+        try:
+            tag = open(os.path.join(ROOT, "profiles", "LATEST")).read().split()[0]
+        except OSError:
+            tag = None
+        cap = os.path.join(ROOT, "profiles", f"ncu_{args.config}_{tag}.json")
+        if tag and os.path.exists(cap):
+            traffic = json.load(open(cap)).get("ffn_dram_bytes_per_block")
+            traffic_src = os.path.relpath(cap, ROOT)
+        else:
+            traffic_src = f"no capture for profile tag {tag!r} (profiles/LATEST)"
+            print(f"bench.py: roofline.traffic unavailable: {traffic_src}", file=sys.stderr)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "us/block", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1e3, 6),
@@ -444,6 +451,7 @@ def main():
         "strategies": summ,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": "ffn_persistent_kernel (permute + gather + gate/up + down), "
                                "CUDA events around its launch in the phase pass",
                      "algorithmic_bytes": "U*3*d*F*2 expert-weight bytes per block",
@@ -463,9 +471,14 @@ def main():
             x0 = synth.gen_trace_block(m, n, 42, rho=cfg["rho"])
             sec, _u = ref.time_layer(x0, k, "vote", beta=cfg["beta"], dim=d, reps=1,
                                      threads=threads)
+            # single-block latency on one thread (the reference library is
+            # single-threaded by design); moe_forward on 4 tokens, scaled to N
+            sec1, _u = ref.time_layer(x0, k, "vote", beta=cfg["beta"], dim=d, reps=1,
+                                      threads=1, ffn_tokens=min(4, n))
             line["cpu_baseline"] = {
                 "value": round(sec * 1e6, 1), "unit": "us/block", "cores": threads,
                 "kind": "reference",
+                "latency_1t_us": round(sec1 * 1e6, 1),
                 "sample": f"1 step: {threads} threads x 1 block; reference des_run(vote) + "
                           f"moe_forward with its linear {d}x{d} fp64 experts (the reference has "
                           f"no SwiGLU expert), gen_trace shared_bias logits"}

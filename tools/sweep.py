@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--json", default="")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the reference CPU column")
+    ap.add_argument("--cpu-ffn-tokens", type=int, default=1,
+                    help="tokens the reference's moe_forward runs per sample (time scaled to N)")
     args = ap.parse_args()
     import torch
     from bench import CONFIGS
@@ -36,9 +39,35 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     ph = (C.c_float * 8)()
+    from bench import measured_peaks
+    peak, peak_kind = measured_peaks()
+    threads = os.cpu_count() or 1
+    cpu_model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu_model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ref = None
+    if not args.no_cpu:
+        from oracle.oracle import Ref
+        ref = Ref()
     out = {"method": "CUDA events per block on the layer's stream, L2 flushed before every "
                      "block, median over timed blocks; phases from a second pass with events "
-                     "between kernels", "rows": []}
+                     "between kernels",
+           "roofline": {"peak_GBps": peak, "peak_kind": peak_kind,
+                        "ffn_frac": "U*3*d*F*2 / t_ffn / peak",
+                        "layer_frac": "(U*3*d*F*2 + M*d*2 + N*d*2 + N*d*4) / t_block / peak"},
+           "cpu_reference": None if ref is None else {
+               "kind": "reference (oracle/_ref: the reference's own des_run / topk_route + "
+                       "moe_forward with its linear d x d fp64 experts)",
+               "cores": threads, "cpu_model": cpu_model,
+               "latency_1t": "one block on one thread (taskset-free, steady_clock); moe_forward "
+                             f"on {args.cpu_ffn_tokens} tokens scaled to N",
+               "throughput_all": f"{threads} threads x 1 block each, blocks/s"},
+           "rows": []}
     for name in args.configs.split(","):
         cfg = CONFIGS[name]
         m, k, d, f = cfg["experts"], cfg["top_k"], cfg["hidden"], cfg["ffn"]
@@ -87,6 +116,20 @@ def main():
                         res["unique_experts"] = round(float(np.mean(us)), 2)
                 u = res["unique_experts"]
                 res["expert_weight_GBps"] = round(u * 3 * d * f * 2 / (res["ffn_us"] * 1e-6) / 1e9, 1)
+                res["ffn_frac"] = round(res["expert_weight_GBps"] / peak, 4)
+                layer_bytes = u * 3 * d * f * 2 + m * d * 2 + n * d * 2 + n * d * 4
+                res["layer_frac"] = round(layer_bytes / (res["us_per_block"] * 1e-6) / 1e9 / peak, 4)
+                if ref is not None and strat in ("vanilla", "seq3", "vote"):
+                    lg = synth.gen_trace_block(m, n, 42, rho=cfg["rho"])
+                    rs = {"vanilla": ("vanilla", 1), "seq3": ("seq", 3), "vote": ("vote", 1)}[strat]
+                    kw = dict(seq_k=rs[1], beta=cfg["beta"], dim=d, reps=1,
+                              ffn_tokens=min(n, args.cpu_ffn_tokens))
+                    t1, _ = ref.time_layer(lg, k, rs[0], threads=1, **kw)
+                    ta, _ = ref.time_layer(lg, k, rs[0], threads=threads, **kw)
+                    rt = ref.time_routing(lg, k, rs[0], seq_k=rs[1], beta=cfg["beta"], reps=5)
+                    res["cpu_ref"] = {"layer_us_1t": round(t1 * 1e6, 1),
+                                      "layer_blocks_per_s_all": round(1.0 / ta, 2),
+                                      "routing_us_1t": round(1e6 / rt, 2)}
                 row[strat] = res
             row["vote_latency_reduction"] = round(
                 1 - row["vote"]["us_per_block"] / row["vanilla"]["us_per_block"], 4)
