@@ -1344,8 +1344,14 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   // the routed mode from N = 32 on. Measured (C2): vanilla N=32 131.6 routed
   // vs 133.0 dense, N=64 149.5 vs 153.6, but N=8 96.3 dense vs 100.3 routed;
   // DES-Seq k=2 at N=32 87.5 dense vs 89.4 routed.
-  const bool prefer_dense = cfg->strategy != DESMOE_VANILLA || n <= 16 ||
-                            std::getenv("DESMOE_ALWAYS_DENSE");
+  // Expert parallel (world > 1): always routed. Every output row a rank
+  // computes is pushed to all G ranks over NVLink, and dense mode's U_own x N
+  // rows (every owned expert x every token) would be ~U/K times the N x K
+  // routed rows the combine actually reads: at C2 (U = 25, K = 8) 3.1x the
+  // bytes per rank (DESMOE_EP_DENSE=1 restores dense for A/B).
+  const bool prefer_dense = (cfg->strategy != DESMOE_VANILLA || n <= 16 ||
+                             std::getenv("DESMOE_ALWAYS_DENSE")) &&
+                            (ex->world <= 1 || std::getenv("DESMOE_EP_DENSE"));
   rc = ffn_impl(c, ex, x, n, cfg->top_k, c->route_idx, c->route_gate, c->route_cnt, y,
                 cfg->strategy == DESMOE_VANILLA ? nullptr : c->n_members, stats, st, zeroed,
                 front_used, y_bf16, residual ? x : nullptr, prefer_dense, true,

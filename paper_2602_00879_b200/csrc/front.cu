@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // keeps the shared address space (LDS/STS instead of generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kMaxStages = 12;  // ring stages (the token-split GEMM runs deep rings)
-  __shared__ uint64_t bars[2 * kMaxStages + 3];  // full[], empty[], tdone, recv, selx
+  __shared__ uint64_t bars[2 * kMaxStages + 4];  // full[], empty[], tdone, recv, selx, mask
+  __shared__ uint32_t s_mask[kFrontCta];         // coreset slices (distributed rank)
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
@@ -458,6 +459,12 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   uint64_t* tdone = bars + 2 * kMaxStages;
   uint64_t* bar_recv = bars + 2 * kMaxStages + 1;  // partials pushed to this CTA (one phase per chunk)
   uint64_t* bar_selx = bars + 2 * kMaxStages + 2;  // every token's selection pushed to this CTA
+  uint64_t* bar_mask = bars + 2 * kMaxStages + 3;  // every CTA's coreset slice pushed to this CTA
+  // DES-Vote over a large pool: the O(m^2) rank count is split over the
+  // cluster (CTA r ranks experts [r*ms, (r+1)*ms) against all m votes) and the
+  // slices' membership masks are exchanged; small pools rank redundantly
+  const int ms = (m + C - 1) / C;
+  const bool dist_rank = kStrat == 1 && m > kDistRankMin && !(a.flags & 4);  // bit 2: A/B off
   int* allsel = reinterpret_cast<int*>(smem + P.allsel);       // [n][k]
   double* allp = reinterpret_cast<double*>(smem + P.allp);     // [n][k]
   const int ocm = (Tc + C - 1) / C;                            // recv rows per sender
@@ -483,7 +490,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     mbar_init(tdone, 1);
     mbar_init(bar_recv, 1);
     mbar_init(bar_selx, 1);
+    mbar_init(bar_mask, 1);
     fence_mbar_init();
+    if (dist_rank) mbar_arrive_expect_tx(bar_mask, static_cast<uint32_t>(C * 4));
     s_bad = 0;
     // arm: chunk 0's partials for this CTA's own tokens from all C senders,
     // and (DES) every token's top-`depth` selection
@@ -1102,27 +1111,51 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     // pool split into `parts` key ranges counted by different threads —
     // inline and with one division per thread (the out-of-line helper with
     // its per-call divisions measured 1300 vs 440 cycles, tools/micro/phase.cu)
-    const int parts = kFrontThreads / m < 16 ? kFrontThreads / m : 16;
-    if (tid < parts * m) {
-      const int part = tid / m, e = tid - part * m;
+    const int e0 = dist_rank ? rk * ms : 0;
+    const int me = dist_rank ? (m - e0 < ms ? (m - e0 > 0 ? m - e0 : 0) : ms) : m;
+    const int span_e = dist_rank ? ms : m;  // experts ranked by this CTA (stride of rankp)
+    const int pmax = kFrontThreads / span_e < 16 ? kFrontThreads / span_e : 16;
+    const int parts = dist_rank ? kFrontThreads / span_e : pmax;
+    if (tid < parts * span_e) {
+      const int part = tid / span_e, el = tid - part * span_e;
+      const int e = e0 + el;
       const int span = (m + parts - 1) / parts;
       const int j0 = part * span, j1 = j0 + span < m ? j0 + span : m;
-      const uint64_t ki = vkey[e];
       int r = 0;
+      if (el < me) {
+        const uint64_t ki = vkey[e];
 #pragma unroll 4
-      for (int j = j0; j < j1; ++j) {
-        const uint64_t kj = vkey[j];
-        r += (kj > ki) | ((kj == ki) & (j < e));
+        for (int j = j0; j < j1; ++j) {
+          const uint64_t kj = vkey[j];
+          r += (kj > ki) | ((kj == ki) & (j < e));
+        }
       }
-      rankp[part * m + e] = r;
+      rankp[part * span_e + el] = r;
     }
     __syncthreads();
     FRONT_MARK(16);
-    if (tid < m) {
-      int r = 0;
+    if (!dist_rank) {
+      if (tid < m) {
+        int r = 0;
 #pragma unroll 1
-      for (int q = 0; q < parts; ++q) r += rankp[q * m + tid];
-      flag[tid] = static_cast<uint8_t>(r < a.m_core);
+        for (int q = 0; q < parts; ++q) r += rankp[q * m + tid];
+        flag[tid] = static_cast<uint8_t>(r < a.m_core);
+      }
+    } else {
+      // this CTA's slice -> one membership word pushed to every CTA (ms <= 32)
+      if (warp == 0) {
+        int r = 0;
+        if (lane < me) {
+#pragma unroll 1
+          for (int q = 0; q < parts; ++q) r += rankp[q * ms + lane];
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, lane < me && r < a.m_core);
+        if (lane < C)
+          st_async_b32(mapa_u32(smem_u32(s_mask + rk), lane), word,
+                       mapa_u32(smem_u32(bar_mask), lane));
+      }
+      mbar_wait_cluster(bar_mask, 0);
+      if (tid < m) flag[tid] = static_cast<uint8_t>((s_mask[tid / ms] >> (tid % ms)) & 1u);
     }
   }
   const int nm = __syncthreads_count(tid < m && flag[tid]);  // m <= 256 < kFrontThreads

@@ -56,6 +56,7 @@ cudaError_t set_fused_route_smem_limit(int bytes);
 // ---- front: router GEMM + routing in one thread-block cluster (front.cu) ----
 constexpr int kFrontCta = 8;        // cluster size (portable maximum)
 constexpr int kFrontThreads = 512;
+constexpr int kDistRankMin = 64;  // DES-Vote pools above this size rank across the cluster
 constexpr int kFrontSmemLimit = 223 * 1024;  // dynamic; + 4 KB static (exp table) = 227 KB
 
 struct FrontArgs {

@@ -136,3 +136,42 @@ def test_ep_across_devices(shape):
     r = _run_ep_check(world, {"DESMOE_EP_SHAPE": shape})
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     assert r.stdout.count('"vote": true, "vanilla": true') == world, r.stdout
+
+
+@pytest.mark.parametrize("strategy", ["vote", "vanilla"])
+def test_ep_stack_matches_single_gpu(strategy):
+    """desmoe_stack_forward with expert-parallel layers (SURVEY §8f row 1 +
+    §8e): G = 2 simulated ranks, each a whole stack of expert shards (one
+    graph per rank), every layer's shards wired across the ranks; each rank's
+    residual-stream output equals the single-rank stack bit for bit."""
+    from paper_2602_00879_b200.layer import DesMoeStack
+    m, d, f, n, k, layers, world = 64, 512, 512, 32, 8, 3, 2
+    cfg = LayerConfig(m, k, d, f, strategy=strategy, vote_beta=0.4)
+    params = [(synth.router_weights(m, d, seed=70 + l), *synth.swiglu_weights(m, d, f, seed=80 + l))
+              for l in range(layers)]
+    full = DesMoeStack(cfg, params)
+    stacks = []
+    for lo, hi in ep.partition(m, world):
+        shard = [(wr, *synth.swiglu_weights(m, d, f, seed=80 + l, lo=lo, hi=hi))
+                 for l, (wr, *_rest) in enumerate(params)]
+        stacks.append(DesMoeStack(cfg, shard, expert_range=(lo, hi)))
+    for l in range(layers):
+        ep.connect_local([s.experts[l] for s in stacks])
+    streams = [torch.cuda.Stream() for _ in stacks]
+    ys = [torch.empty((n, d), dtype=torch.float32, device="cuda") for _ in stacks]
+    for call in range(3):
+        x = synth.hidden_states(n, d, seed=300 + call, rho=0.3)
+        want = full.forward(x, residual=True).clone()
+        want_stats = full.stats.cpu()
+        torch.cuda.synchronize()
+        for r, s in enumerate(stacks):
+            streams[r].wait_stream(torch.cuda.current_stream())
+            s.forward(x, ys[r], stream=streams[r], residual=True)
+        torch.cuda.synchronize()
+        owned = torch.zeros(layers, dtype=torch.int64)
+        for r, s in enumerate(stacks):
+            assert torch.equal(ys[r], want), (call, r, (ys[r] - want).abs().max().item())
+            st = s.stats.cpu()
+            assert torch.equal(st[:, :3], want_stats[:, :3])
+            owned += st[:, 3].long()
+        assert torch.equal(owned, want_stats[:, 0].long())
