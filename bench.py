@@ -19,7 +19,11 @@ layers of a rotated set with distinct weights (>= 1 GiB of experts), as in a
 real stack, so every expert weight a block streams comes from HBM;
 `value_l2_flushed` repeats the measurement with a 256 MiB L2 flush before
 every block. `e2e` = the same through the host-buffer C-ABI entry
-(desmoe_layer_forward_host: pinned H2D of X, layer, D2H of Y, synchronise).
+(desmoe_layer_forward_host: the caller's pinned X copied in inside the layer
+graph, layer, fp32 Y written into the caller's pinned memory, return once it
+is visible), timed with the host's steady_clock around each C call
+(tools/e2e/libe2etimer.so); `e2e.cuda_event_value` is the same call bracketed
+by CUDA events on the stream.
 `--impl reference` times the reference library's own CPU layer
 (oracle/_ref: des_run + moe_forward with its linear dim x dim experts) on the
 host cores.
@@ -365,7 +369,10 @@ def main():
     xw = [x.cpu().pin_memory() for _, x in warm]
     for i, x in enumerate(xw):
         host_call(layers[i % nl], x)
-    e2e = []
+    # (1) CUDA events on the stream around the call (the event after the call
+    # is submitted only once the host holds the result, so it adds the
+    # stream's submission latency)
+    e2e_ev = []
     for i, x in enumerate(xh):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -373,18 +380,41 @@ def main():
         host_call(layers[i % nl], x)
         e1.record(stream)
         e1.synchronize()
-        e2e.append(e0.elapsed_time(e1) * 1e3)
+        e2e_ev.append(e0.elapsed_time(e1) * 1e3)
+    # (2) the headline: host clock (steady_clock, in C) around each C-ABI call
+    # (tools/e2e/libe2etimer.so), the latency a C/C++ caller of the drop-in sees
+    e2e_kind = "host steady_clock around each desmoe_layer_forward_host call (C)"
+    try:
+        T = C.CDLL(os.path.join(ROOT, "tools", "e2e", "libe2etimer.so"))
+    except OSError as exc:
+        raise SystemExit(f"tools/e2e/libe2etimer.so missing ({exc}): run __graft_entry__.build()")
+    ctx_arr = (C.c_void_p * nl)(*[lay.ctx.h.value for lay in layers])
+    ex_arr = (C.c_void_p * nl)(*[lay.experts.h.value for lay in layers])
+    wr_arr = (C.c_void_p * nl)(*[lay.w_router.data_ptr() for lay in layers])
+    x_arr = (C.c_void_p * len(xh))(*[x.data_ptr() for x in xh])
+    outs = (C.c_double * len(xh))()
+    T.e2e_time_host_calls.restype = C.c_int
+    for _ in range(2):  # the first pass warms the call path; the second is kept
+        r = T.e2e_time_host_calls(ctx_arr, ex_arr, wr_arr, nl, x_arr, len(xh), n, C.byref(rc_vote),
+                                  C.c_void_p(yh.data_ptr()), C.c_void_p(sh.data_ptr()), sp,
+                                  len(xh), outs)
+        if r:
+            raise RuntimeError(L.desmoe_last_error().decode())
+    e2e = [outs[i] for i in range(len(xh))]
     e2e_us = float(np.mean(e2e))
+    e2e_event_us = float(np.mean(e2e_ev))
 
     # max over ranks (µs per block for the timed steps)
     t_vote, p_vote, s_vote = results["vote"]
     tot_us = float(t_vote.sum())
     if ws > 1:
-        tt = torch.tensor([tot_us, e2e_us * len(e2e), flushed["vanilla"], flushed["vote"]],
+        tt = torch.tensor([tot_us, e2e_us * len(e2e), flushed["vanilla"], flushed["vote"],
+                           e2e_event_us],
                           dtype=torch.float64, device="cpu" if same_dev else "cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         tot_us, e2e_tot = float(tt[0]), float(tt[1])
         flushed = {"vanilla": float(tt[2]), "vote": float(tt[3])}
+        e2e_event_us = float(tt[4])
         e2e_us = e2e_tot / len(e2e)
     if rank != 0:
         if ws > 1:
@@ -458,8 +488,11 @@ def main():
                      "peak_kind": peak_kind},
         "e2e": {"value": round(e2e_us, 3), "unit": "us/block",
                 "h2d_bytes_per_step": n * d * 2, "d2h_bytes_per_step": n * d * 4 + 16,
-                "entry": "desmoe_layer_forward_host (C ABI, include/desmoe.h) via ctypes: pinned "
-                         "x in, fp32 y + stats out, returns when they are visible"},
+                "timer": e2e_kind,
+                "median": round(float(np.median(e2e)), 3),
+                "cuda_event_value": round(e2e_event_us, 3),
+                "entry": "desmoe_layer_forward_host (C ABI, include/desmoe.h): pinned x in, fp32 "
+                         "y + stats out, returns when they are visible in host memory"},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
     }

@@ -308,6 +308,41 @@ def test_stack_equals_chained_layers(strategy):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["vote", "seq"])
+def test_stack_matches_oracle_chain(ref, port, strategy):
+    """The 24-layer-stack path (desmoe_stack_forward, residual stream) against
+    a chain of CPU checkers, layer by layer on a 3-layer C3 shape (M=256,
+    d=2048, SwiGLU F=512, N=32): router logits = fp64 GEMM of the bf16 values
+    (Port.router_logits), routing = the reference's own des_run (oracle/_ref),
+    experts = the C restatement's SwiGLU (Port.moe_ffn), hand-over
+    h_{l+1} = bf16(h_l + MoE(h_l)). Per-layer unique experts / coreset /
+    selections equal the reference's; the final fp32 output agrees within the
+    bf16 tolerance (SURVEY §8c parity plan 3)."""
+    from paper_2602_00879_b200.layer import DesMoeStack
+    m, d, f, n, k, L, beta = 256, 2048, 512, 32, 8, 3, 0.15
+    cfg = LayerConfig(m, k, d, f, strategy=strategy, seq_k=3, vote_beta=beta)
+    params = [(synth.router_weights(m, d, seed=90 + l), *synth.swiglu_weights(m, d, f, seed=95 + l))
+              for l in range(L)]
+    stack = DesMoeStack(cfg, params)
+    x = synth.hidden_states(n, d, seed=11, rho=0.3)
+    y_gpu = stack.forward(x, residual=True).cpu().numpy()
+    stats = stack.stats.cpu().numpy()
+    h = x.float().cpu().numpy()
+    for l, (wr, wg, wu, wd) in enumerate(params):
+        logits = port.router_logits(h, wr.float().cpu().numpy())
+        mem, route = ref.des_run(logits, k, strategy, seq_k=3, beta=beta)
+        u, total, _ = ref.moe_latency(route, m)
+        assert stats[l].tolist()[:3] == [u, len(mem), total], (l, stats[l], u, len(mem), total)
+        moe = port.moe_ffn(route, h, wg.float().cpu().numpy(), wu.float().cpu().numpy(),
+                           wd.float().cpu().numpy(), threads=8)
+        out = (moe + h).astype(np.float32)
+        h = bf16_round(out) if l + 1 < L else out
+    err = float(np.abs(y_gpu - h).max() / np.abs(h).max())
+    print(f"stack vs oracle chain ({strategy}): max rel err {err:.2e}")
+    assert err <= 1e-2, err
+
+
+@pytest.mark.gpu
 def test_layer_config_changes_take_effect():
     """LayerConfig is mutable (bench.py switches seq_k between DES-Seq k=3 and
     k=2 on one layer): every call must route with the current fields."""
