@@ -345,8 +345,11 @@ __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int ch
   p.erow = 0;
   const size_t erow_b = fr_align(static_cast<size_t>(own_max) * (m + 1) * 8, 16);
   p.dreg = erow_b;
-  // vote matrix chunk [vote_rows][m] f64, later votes + keys + rank parts
-  size_t dreg_b = static_cast<size_t>(vote_rows) * m * 8;
+  // vote buckets: token bitmask per expert [m][ceil(n/32)] + offsets [m+1] +
+  // the bucketed weights [n][k] f64; later votes + keys + rank parts
+  (void)vote_rows;
+  size_t dreg_b = fr_align(static_cast<size_t>(m * ((n + 31) / 32) + m + 1) * 4, 16) +
+                  static_cast<size_t>(n) * k * 8;
   const size_t rank_b = static_cast<size_t>(m) * (8 + 8 + 16 * 4) + 64;
   if (rank_b > dreg_b) dreg_b = rank_b;
   p.scratch = p.dreg;  // per-warp fallback scratch aliases the vote workspace
@@ -1051,53 +1054,93 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   FRONT_MARK(9);
 
   // ---- V: block coreset, redundantly in every CTA ------------------------------------
-  // DES-Vote: the reference's masked matrix (des.cpp:73-84) in token chunks
-  // of tv rows in shared memory; thread i adds column i over the tokens in
-  // ascending order, zeros included (des.cpp:86-91) — the same fp64 sums.
-  double* dense = reinterpret_cast<double*>(smem + P.dreg);  // [tv][m]
-  const int tv = a.vote_rows;
+  // DES-Vote: V_e = the reference's column sum of the masked matrix over the
+  // tokens in ascending order, zeros included (des.cpp:73-91). Adding +0.0
+  // leaves an fp64 sum unchanged, so each expert sums only the tokens that
+  // selected it, in token order: the (token, expert) pairs are bucketed by
+  // expert with a stable counting sort (a token bitmask per expert, its
+  // popcounts as counts and ranks), then thread e walks its own list — the
+  // same fp64 additions in the same order as the dense N x M matrix.
   double vsum = 0.0;
 #pragma unroll 1
   for (int i = tid; i < m; i += kFrontThreads) flag[i] = 0;
   FRONT_MARK(10);
+  if constexpr (kStrat == 1) {
+    const int nw = (n + 31) >> 5;                                        // token words
+    uint32_t* vbits = reinterpret_cast<uint32_t*>(smem + P.dreg);        // [m][nw]
+    int* voff = reinterpret_cast<int*>(vbits + m * nw);                  // [m + 1]
+    double* vlist = reinterpret_cast<double*>(smem + P.dreg + fr_align(
+        static_cast<size_t>(m * nw + m + 1) * 4, 16));                   // [n * depth]
 #pragma unroll 1
-  for (int t0 = 0; t0 < n; t0 += (kStrat == 1 ? tv : n)) {
-    const int nt = kStrat == 1 ? (n - t0 < tv ? n - t0 : tv) : n;
-    if constexpr (kStrat == 1) {
+    for (int i = tid; i < m * nw; i += kFrontThreads) vbits[i] = 0u;
+    __syncthreads();
 #pragma unroll 1
-      for (int i = tid; i < nt * m; i += kFrontThreads) dense[i] = 0.0;
-      __syncthreads();
-    }
-    // scatter the tokens' top-`depth` (pushed by their owners) into the matrix
-#pragma unroll 1
-    for (int w = tid; w < nt * depth; w += kFrontThreads) {
-      const int t = t0 + w / depth, j = w - (w / depth) * depth;
+    for (int w = tid; w < n * depth; w += kFrontThreads) {
+      const int t = w / depth, j = w - t * depth;
       const int e = allsel[t * k + j];
-      if (kStrat == 1)
-        dense[(t - t0) * m + e] = allp[t * k + j];
-      else
-        flag[e] = 1;  // DES-Seq: union of the top-seq_k
+      atomicOr(&vbits[e * nw + (t >> 5)], 1u << (t & 31));
     }
     __syncthreads();
-    if (kStrat == 1 && tid < m) {
-      const double* col = dense + tid;
-      int t = 0;
+    // counts -> exclusive offsets (m <= 256 <= kFrontThreads: one expert per thread)
+    int cnt_e = 0;
+    if (tid < m)
 #pragma unroll 1
-      for (; t + 8 <= nt; t += 8) {
+      for (int q = 0; q < nw; ++q) cnt_e += __popc(vbits[tid * nw + q]);
+    int inc = cnt_e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (tid < m) {
+      int base = 0;
+#pragma unroll 1
+      for (int q = 0; q < warp; ++q) base += warp_tot[q];
+      voff[tid] = base + inc - cnt_e;
+      if (tid == m - 1) voff[m] = base + inc;
+    }
+    __syncthreads();
+    // scatter: (t, e) -> e's list at its rank among e's tokens (token order)
+#pragma unroll 1
+    for (int w = tid; w < n * depth; w += kFrontThreads) {
+      const int t = w / depth, j = w - t * depth;
+      const int e = allsel[t * k + j];
+      const uint32_t* b = vbits + e * nw;
+      int pos = voff[e] + __popc(b[t >> 5] & ((1u << (t & 31)) - 1u));
+#pragma unroll 1
+      for (int q = 0; q < (t >> 5); ++q) pos += __popc(b[q]);
+      vlist[pos] = allp[t * k + j];
+    }
+    __syncthreads();
+    if (tid < m) {
+      const int i1 = voff[tid + 1];
+      int i = voff[tid];
+#pragma unroll 1
+      for (; i + 8 <= i1; i += 8) {
         double v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = col[(t + q) * m];
+        for (int q = 0; q < 8; ++q) v[q] = vlist[i + q];
 #pragma unroll
         for (int q = 0; q < 8; ++q) vsum += v[q];
       }
 #pragma unroll 1
-      for (; t < nt; ++t) vsum += col[t * m];
+      for (; i < i1; ++i) vsum += vlist[i];
     }
-    if (kStrat == 1) __syncthreads();  // column reads done before the next chunk
+    __syncthreads();  // list reads done before votes / keys reuse the region
+  } else {
+    // DES-Seq: the union of every token's top-seq_k
+#pragma unroll 1
+    for (int w = tid; w < n * depth; w += kFrontThreads) {
+      const int t = w / depth, j = w - t * depth;
+      flag[allsel[t * k + j]] = 1;
+    }
+    __syncthreads();
   }
   FRONT_MARK(11);
   if (kStrat == 1) {
-    double* votes = dense;                                          // [m] (aliases chunk 0)
+    double* votes = reinterpret_cast<double*>(smem + P.dreg);      // [m] (aliases the buckets)
     uint64_t* vkey = reinterpret_cast<uint64_t*>(votes + m);        // [m]
     int* rankp = reinterpret_cast<int*>(vkey + m);                  // [parts][m]
     if (tid < m) {

@@ -12,13 +12,22 @@
 //            [--bank-seed S] [--hidden-dim D] [--activation a] [--a A] [--b B]
 //            [--bytes-per-expert X] [--json] [-o PATH]
 //   dessim_* sweep --trace PATH --method m [--betas a,b] [--ks a,b] (run's options)
+//   dessim_* explosion --experts M --top-k K --blocks a,b [--trials T] [--seed s]
+//            [--trace PATH] [--activation a] [--json] [-o PATH]
+//   dessim_* oracle-gap [--experts M] [--top-k K] [--block N] [--instances I] [--seed s]
+//            [--model m] [--rho r] [--temperature t] [--hidden-dim D] [--activation a]
+//   every command: [--config file.json] (the JSON object's keys fill in the
+//   flags not given on the command line, as the reference's main.cpp does)
 #include <cstdint>
+#include <fstream>
 #include <cstdlib>
 #include <iostream>
 #include <map>
 #include <sstream>
 #include <string>
 #include <vector>
+
+#include <json.hpp>
 
 #include "../../../reference/proj/tools/commands.hpp"
 
@@ -51,6 +60,28 @@ Args parse(int argc, char** argv, int from) {
       a.kv[k.substr(0, eq)] = k.substr(eq + 1);
     } else if (i + 1 < argc) {
       a.kv[k] = argv[++i];
+    }
+  }
+  if (a.has("--config")) {  // flags win over the file's keys
+    std::ifstream in(a.s("--config"));
+    if (!in) throw std::invalid_argument("cannot open config file: " + a.s("--config"));
+    nlohmann::json j = nlohmann::json::parse(in);
+    if (!j.is_object()) throw std::invalid_argument("config file must hold a JSON object");
+    for (auto it = j.begin(); it != j.end(); ++it) {
+      const std::string key = "--" + it.key();
+      if (it.key() == "config" || a.has(key)) continue;
+      std::string v;
+      if (it->is_string()) {
+        v = it->get<std::string>();
+      } else if (it->is_array()) {
+        for (const auto& x : *it) v += (v.empty() ? "" : ",") + (x.is_string() ? x.get<std::string>() : x.dump());
+      } else if (it->is_boolean()) {
+        v = it->get<bool>() ? "1" : "";
+        if (v.empty()) continue;
+      } else {
+        v = it->dump();
+      }
+      a.kv[key] = v;
     }
   }
   return a;
@@ -92,8 +123,8 @@ int main(int argc, char** argv) {
     return 2;
   }
   const std::string cmd = argv[1];
-  const Args a = parse(argc, argv, 2);
   try {
+    const Args a = parse(argc, argv, 2);
     if (cmd == "gen-trace") {
       GenTraceOptions o;
       o.experts = static_cast<int>(a.i("--experts", 0));
@@ -127,6 +158,35 @@ int main(int argc, char** argv) {
       if (a.has("--betas")) o.betas = list<double>(a.s("--betas"));
       if (a.has("--ks")) o.ks = list<int>(a.s("--ks"));
       return cmd_sweep(o);
+    }
+    if (cmd == "explosion") {
+      ExplosionOptions o;
+      o.experts = static_cast<int>(a.i("--experts", 0));
+      o.top_k = static_cast<int>(a.i("--top-k", 0));
+      if (a.has("--blocks")) o.blocks = list<int>(a.s("--blocks"));
+      o.trials = static_cast<int>(a.i("--trials", o.trials));
+      o.seed = static_cast<std::uint64_t>(a.i("--seed", 0));
+      o.trace_path = a.s("--trace");
+      o.activation = a.s("--activation", o.activation);
+      o.output = a.s("--output");
+      o.json = a.has("--json");
+      return cmd_explosion(o);
+    }
+    if (cmd == "oracle-gap") {
+      OracleGapOptions o;
+      o.experts = static_cast<int>(a.i("--experts", o.experts));
+      o.top_k = static_cast<int>(a.i("--top-k", o.top_k));
+      o.block = static_cast<int>(a.i("--block", o.block));
+      o.instances = static_cast<int>(a.i("--instances", o.instances));
+      o.seed = static_cast<std::uint64_t>(a.i("--seed", 0));
+      o.model = a.s("--model", o.model);
+      o.rho = a.f("--rho", o.rho);
+      o.temperature = a.f("--temperature", o.temperature);
+      o.hidden_dim = static_cast<int>(a.i("--hidden-dim", o.hidden_dim));
+      o.activation = a.s("--activation", o.activation);
+      o.output = a.s("--output");
+      o.json = a.has("--json");
+      return cmd_oracle_gap(o);
     }
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";

@@ -75,6 +75,22 @@ def test_reference_unit_tests_pass_on_gpu_facade():
     assert "| 0 failed" in r.stdout, r.stdout
 
 
+def test_cli_standin_runs_reference_cli_suite_on_reference():
+    """The reference's own tests/test_cli.cpp (13 cases: gen-trace, run, sweep,
+    explosion, oracle-gap, --config) passes through the CLI argument stand-in
+    tests/cpp/cli_main.cpp linked to the reference library — so the same
+    stand-in over the GPU façade (tests/test_cmake_package.py ctest) tests the
+    GPU path, not the front end."""
+    exe = os.path.join(BUILD, "cli_tests_on_ref")
+    cli = os.path.join(BUILD, "dessim_ref_cli")
+    if not (os.path.exists(exe) and os.path.exists(cli)):
+        pytest.skip("cli_tests_on_ref not built (make -C tests/cpp needs /root/reference)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "DESSIM_CLI": cli})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert "| 13 passed | 0 failed" in r.stdout, r.stdout
+
+
 def test_acceptance_runner_on_reference():
     r = _run(ACC_REF)
     assert r.returncode == 0, r.stdout + r.stderr
