@@ -53,4 +53,4 @@ def test_reference_ctest_passes_on_gpu_package():
                        capture_output=True, text=True, timeout=1200)
     print(r.stdout[-3000:])
     assert r.returncode == 0, (r.stdout + r.stderr)[-6000:]
-    assert "100% tests passed, 0 tests failed out of 3" in r.stdout, r.stdout[-3000:]
+    assert "100% tests passed" in r.stdout and "out of 3" in r.stdout, r.stdout[-3000:]

@@ -310,14 +310,17 @@ def test_stack_equals_chained_layers(strategy):
 @pytest.mark.gpu
 @pytest.mark.parametrize("strategy", ["vote", "seq"])
 def test_stack_matches_oracle_chain(ref, port, strategy):
-    """The 24-layer-stack path (desmoe_stack_forward, residual stream) against
-    a chain of CPU checkers, layer by layer on a 3-layer C3 shape (M=256,
-    d=2048, SwiGLU F=512, N=32): router logits = fp64 GEMM of the bf16 values
-    (Port.router_logits), routing = the reference's own des_run (oracle/_ref),
-    experts = the C restatement's SwiGLU (Port.moe_ffn), hand-over
-    h_{l+1} = bf16(h_l + MoE(h_l)). Per-layer unique experts / coreset /
-    selections equal the reference's; the final fp32 output agrees within the
-    bf16 tolerance (SURVEY §8c parity plan 3)."""
+    """The stack path (desmoe_stack_forward, residual stream) layer by layer
+    against CPU checkers on a 3-layer C3 shape (M=256, d=2048, SwiGLU F=512,
+    N=32). Every layer l sees the GPU stack's own bf16 hand-over h_l (the
+    stack's output equals chaining the layers one by one, bit for bit); on
+    that h_l the checkers run router logits = fp64 GEMM of the bf16 values
+    (Port.router_logits), routing = the reference's own des_run (oracle/_ref)
+    and experts = the C restatement's SwiGLU (Port.moe_ffn). Per layer: unique
+    experts / coreset / selections equal the reference's and h_l + MoE(h_l)
+    agrees within the bf16 tolerance (SURVEY §8c parity plan 3). (A chain fed
+    with its OWN outputs drifts by bf16 ulps per layer, which moves logit
+    near-ties: that tests the arithmetic's chaos, not the kernels.)"""
     from paper_2602_00879_b200.layer import DesMoeStack
     m, d, f, n, k, L, beta = 256, 2048, 512, 32, 8, 3, 0.15
     cfg = LayerConfig(m, k, d, f, strategy=strategy, seq_k=3, vote_beta=beta)
@@ -325,21 +328,28 @@ def test_stack_matches_oracle_chain(ref, port, strategy):
               for l in range(L)]
     stack = DesMoeStack(cfg, params)
     x = synth.hidden_states(n, d, seed=11, rho=0.3)
-    y_gpu = stack.forward(x, residual=True).cpu().numpy()
+    y_stack = stack.forward(x, residual=True).clone()
     stats = stack.stats.cpu().numpy()
-    h = x.float().cpu().numpy()
+    h = x
     for l, (wr, wg, wu, wd) in enumerate(params):
-        logits = port.router_logits(h, wr.float().cpu().numpy())
+        layer = DesMoeLayer(cfg, wr, wg, wu, wd, own_context=True)
+        y = layer.forward(h) + h.float()
+        torch.cuda.synchronize()
+        assert layer.stats.cpu().tolist()[:3] == stats[l].tolist()[:3]
+        hn = h.float().cpu().numpy()
+        logits = port.router_logits(hn, wr.float().cpu().numpy())
         mem, route = ref.des_run(logits, k, strategy, seq_k=3, beta=beta)
         u, total, _ = ref.moe_latency(route, m)
         assert stats[l].tolist()[:3] == [u, len(mem), total], (l, stats[l], u, len(mem), total)
-        moe = port.moe_ffn(route, h, wg.float().cpu().numpy(), wu.float().cpu().numpy(),
+        moe = port.moe_ffn(route, hn, wg.float().cpu().numpy(), wu.float().cpu().numpy(),
                            wd.float().cpu().numpy(), threads=8)
-        out = (moe + h).astype(np.float32)
-        h = bf16_round(out) if l + 1 < L else out
-    err = float(np.abs(y_gpu - h).max() / np.abs(h).max())
-    print(f"stack vs oracle chain ({strategy}): max rel err {err:.2e}")
-    assert err <= 1e-2, err
+        want = moe + hn
+        got = y.cpu().numpy()
+        err = float(np.abs(got - want).max() / np.abs(want).max())
+        print(f"stack layer {l} ({strategy}) vs reference routing + C SwiGLU: max rel err {err:.2e}")
+        assert err <= 4e-3, (l, err)
+        h = y.to(torch.bfloat16)
+    assert torch.equal(y_stack, y)
 
 
 @pytest.mark.gpu
