@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   constexpr int kMaxStages = 12;  // ring stages (the token-split GEMM runs deep rings)
   __shared__ uint64_t bars[2 * kMaxStages + 4];  // full[], empty[], tdone, recv, selx, mask
   __shared__ uint32_t s_mask[kFrontCta];         // coreset slices (distributed rank)
+  __shared__ uint32_t s_tag;                     // this call's hand-off tag
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
   __shared__ int warp_tot[kFrontThreads / 32 + 1];
@@ -558,7 +559,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
                   &x_maps.map[a.box_index], &full[i], (kTs ? i : kb0 + i) * kBK, x_row0, pol_x);
   }
   FRONT_MARK(47);
-  const uint32_t tag = a.seq ? hand_tag(*a.seq) : 0u;  // this call's hand-off tag
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -568,6 +568,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   cluster_arrive_relaxed();
   cluster_wait();
   FRONT_MARK(1);
+  // this call's hand-off tag: an L2 round trip (the sequence word the last
+  // combine advanced), taken by a warp idle during the router GEMM and read
+  // from shared memory after the GEMM's barrier (loaded by every thread at
+  // this point, it stalled all 16 warps, the MMA issuer included, ~1 us)
+  if (tid == 96) s_tag = a.seq ? hand_tag(*a.seq) : 0u;
   if (!(a.flags & 1) && warp >= 8 && warp < 12) {
     // instruction-cache prewarm: the layer's FFN streams hundreds of MB
     // between two calls, so this kernel's code comes back from far memory and
@@ -690,16 +695,22 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     if (warp == 0 && lane == 0) {
       const uint64_t pol_w = l2_policy_evict_last();
       const uint64_t pol_x = l2_policy_evict_last();
+      // a ring with one stage per K block holds this CTA's whole W_r slice:
+      // it stays resident over the token chunks, which reload only their X
+      // boxes (C3 N=64: the second chunk re-streamed 128 KB of W_r, ~4 us)
+      const bool w_resident = S == kb_cta;
 #pragma unroll 1
       for (int i = 0; i < kb_cta; ++i) {
         const int it = c * kb_cta + i, s = it % S;
         unsigned char* st = ring + static_cast<size_t>(s) * stage_bytes;
         if (it >= S) {
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], mt * kATile + xbytes);
+          mbar_arrive_expect_tx(&full[s], w_resident ? xbytes : mt * kATile + xbytes);
+          if (!w_resident) {
 #pragma unroll 1
-          for (int tl = 0; tl < mt; ++tl)
-            tma_load_2d(st + tl * kATile, &wr_map, &full[s], (kb0 + i) * kBK, tl * kBM, pol_w);
+            for (int tl = 0; tl < mt; ++tl)
+              tma_load_2d(st + tl * kATile, &wr_map, &full[s], (kb0 + i) * kBK, tl * kBM, pol_w);
+          }
         }
         if (it >= x_pre)
           tma_load_2d(st + mt * kATile, &x_maps.map[a.box_index], &full[s], (kb0 + i) * kBK, c0,
@@ -802,6 +813,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   asm volatile("cp.async.wait_all;" ::: "memory");  // the exp table (issued in the setup)
   __syncthreads();
   FRONT_MARK(4);
+  const uint32_t tag = s_tag;
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, a.tmem_cols);
@@ -923,8 +935,29 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     __syncthreads();
     FRONT_MARK(5);
     // ---- L3: activation in fp64, data-parallel over (own token, expert) ----------
+    // softmax: four exps per thread in flight, inlined (many per thread here,
+    // so the out-of-line call's serialised latency chains dominated)
+    int w0 = tid;
+    if (act == 0) {
 #pragma unroll 1
-    for (int w = tid; w < own * m; w += kFrontThreads) {
+      for (; w0 + 3 * kFrontThreads < own * m; w0 += 4 * kFrontThreads) {
+        double ex[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int w = w0 + u * kFrontThreads;
+          const int j = w / m;
+          ex[u] = glibc_exp(static_cast<double>(xrow[w]) - static_cast<double>(mxv[j]), s_exptab);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int w = w0 + u * kFrontThreads;
+          const int j = w / m, i = w - j * m;
+          erow[j * ew + i] = ex[u];
+        }
+      }
+    }
+#pragma unroll 1
+    for (int w = w0; w < own * m; w += kFrontThreads) {
       const int j = w / m, i = w - j * m;
       const double x = static_cast<double>(xrow[w]);
       double e = x;
@@ -1045,8 +1078,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     cluster_arrive_relaxed();
     cluster_wait();
     FRONT_MARK(9);
-    front_tail(a.logits_out, xrow, own_tok, own, m, tid);
-    front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 48);
+    if (a.logits_out) front_tail(a.logits_out, xrow, own_tok, own, m, tid);
+    if (tracing) front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 48);
     return;
   }
   mbar_wait_cluster(bar_selx, 0);       // every token's selection has arrived
@@ -1238,8 +1271,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   if (tracing && tid == 0) s_ts[25] = clock64();
   cluster_wait();  // #3: no CTA exits while others may still read its shared memory
   FRONT_MARK(14);
-  front_tail(a.logits_out, xrow, own_tok, own, m, tid);
-  front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 48);
+  // (guarded here: a call into an out-of-line function fetches its code even
+  // when it returns at once — measured as 5 % of the kernel's warp samples)
+  if (a.logits_out) front_tail(a.logits_out, xrow, own_tok, own, m, tid);
+  if (tracing) front_dump_marks(a.trace, a.trace_cap, s_ts, tid, 48);
 #undef FRONT_MARK
 }
 
