@@ -1237,6 +1237,12 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   // blocks: no exchange, no token chunking; each CTA streams all of W_r).
   // Measured crossover (tools/sweep.py): token split wins from N*M = 32768.
   int tsplit = static_cast<long>(n) * m >= 32768 ? 2 : 0;
+  // larger blocks / pools: the router GEMM runs ahead in its own clusters
+  // (router_cluster_kernel: one 8-CTA cluster per 32 tokens x 128 experts),
+  // the front reads the logits (DESMOE_FRONT_ROUTER=0/1 overrides)
+  bool router = n > kRouterTc || m > 128;
+  if (const char* rv = std::getenv("DESMOE_FRONT_ROUTER")) router = std::atoi(rv) != 0;
+  if (router && (d / kBK) / kFrontCta <= 8) tsplit = 3;
   if (const char* ts = std::getenv("DESMOE_FRONT_TSPLIT")) tsplit = std::atoi(ts);
   if (!front_plan(n, m, k, d, &a, &smem, tsplit) && !front_plan(n, m, k, d, &a, &smem, 0))
     return DESMOE_OK;
@@ -1278,6 +1284,26 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
   if (const char* ff = std::getenv("DESMOE_FRONT_FLAGS")) a.flags = std::atoi(ff);
+  if (a.tsplit == 3) {
+    RouterArgs ra{};
+    ra.n = n;
+    ra.m = m;
+    ra.d = d;
+    ra.tc = kRouterTc;
+    ra.mtiles = (m + kBM - 1) / kBM;
+    ra.kb_cta = (d / kBK) / kFrontCta;
+    ra.b_rows = b_rows_for(n < kRouterTc ? n : kRouterTc);
+    int bi = 0;
+    while ((16 << bi) < ra.b_rows) ++bi;
+    ra.box_index = bi;
+    ra.logits = c->logits32;
+    cudaError_t re = launch_router_cluster(c->wr_map, c->x_maps, ra, st);
+    if (re != cudaSuccess)
+      return fail(DESMOE_ECUDA, std::string("router kernel: ") + cudaGetErrorString(re));
+    c->launches += 1;
+    a.logits_in = c->logits32;
+    a.logits_out = nullptr;  // the router kernel wrote them
+  }
   cudaError_t e = launch_front(c->wr_map, c->x_maps, a, smem, st);
   if (e != cudaSuccess) return fail(DESMOE_ECUDA, std::string("front kernel: ") + cudaGetErrorString(e));
   c->launches += 1;

@@ -393,12 +393,13 @@ __host__ __device__ inline FrontSmem front_smem_plan(int n, int m, int k, int ch
 }
 
 // Compile-time specialised on the routing strategy (kStrat: -1 vanilla, 0
-// DES-Seq, 1 DES-Vote), the router-GEMM shape (kTs: token split) and the
+// DES-Seq, 1 DES-Vote), the router-GEMM shape (kG: 0 split-K over the
+// cluster, 1 token split, 2 logits in from router_cluster_kernel) and the
 // small-block L stage (kSmall: at most one own token per warp of a group):
 // each instantiation executes one contiguous code path, so the instruction
 // fetch (cold after the FFN streamed hundreds of MB) follows it sequentially
 // instead of jumping over the other variants.
-template <int kStrat, bool kTs, bool kSmall>
+template <int kStrat, int kG, bool kSmall>
 __global__ void __launch_bounds__(kFrontThreads, 1)
     front_kernel(const __grid_constant__ CUtensorMap wr_map, const __grid_constant__ BoxMaps x_maps,
                  const __grid_constant__ FrontArgs a_param) {
@@ -429,6 +430,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // glibc exp's 2^(k/128) table, staged while the router GEMM runs
   __shared__ __align__(16) unsigned long long s_exptab[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr bool kTs = kG == 1;   // token-split GEMM
+  constexpr bool kLin = kG == 2;  // logits in (router_cluster_kernel ran ahead)
   const bool tracing = a.trace != nullptr;
   if (tracing && tid == 0) s_ts[24] = clock64();
 #define FRONT_MARK(ev)                          \
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     // and (DES) every token's top-`depth` selection
     const int nc0 = n < Tc ? n : Tc;
     const int own0 = (nc0 * (rk + 1)) / C - (nc0 * rk) / C;
-    if constexpr (!kTs) mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
+    if constexpr (kG == 0) mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * own0 * m4 * 4));
     if constexpr (kStrat >= 0)  // every token's top-depth ids (+ weights, DES-Vote)
       mbar_arrive_expect_tx(bar_selx, static_cast<uint32_t>(n * depth * (kStrat == 1 ? 12 : 4)));
     else if (rk == 0 && a.pub)
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           tma_load_2d(st + tl * kATile, &wr_map, &full[i], i * kBK, tl * kBM, pol);
       }
     }
-    if constexpr (!kTs) {
+    if constexpr (kG == 0) {
 #pragma unroll 1
       for (int i = 0; i < kb_cta && i < S; ++i) {
         unsigned char* st = ring + static_cast<size_t>(i) * stage_bytes;
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
     FRONT_MARK(45);
   }
-  if (warp == 2) {
+  if (warp == 2 && !kLin) {
     tmem_alloc(tmem_slot, a.tmem_cols);
     if (tracing && lane == 0) s_ts[46] = gtime();
   }
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // the first ring stages' X boxes go out at once (their W_r halves and the
   // stages' transaction counts were armed in the setup): no CTA barrier or
   // cluster barrier on the way to the router GEMM's inputs
-  const int x_pre = (!kTs || a.tsplit == 2) ? (kTs ? (kb_cta * C < S ? kb_cta * C : S)
+  const int x_pre = kLin ? 0 : (!kTs || a.tsplit == 2) ? (kTs ? (kb_cta * C < S ? kb_cta * C : S)
                                                    : (kb_cta < S ? kb_cta : S))
                                              : 0;
   if (tid == 0) {
@@ -688,7 +691,27 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     FRONT_MARK(3);
   }
 #pragma unroll 1
-  for (int c = 0; c < nch && !kTs; ++c) {
+  if constexpr (kLin) {
+    // logits from router_cluster_kernel (complete since griddepcontrol.wait):
+    // this CTA owns tokens [n rk / C, n (rk + 1) / C), as in the token split
+    const int tlo = (n * rk) / C, thi = (n * (rk + 1)) / C;
+    own = thi - tlo;
+    const float* src = a.logits_in + static_cast<size_t>(tlo) * m;
+    if ((m & 3) == 0) {
+      const int cnt4 = own * m / 4;
+#pragma unroll 1
+      for (int w = tid; w < cnt4; w += kFrontThreads)
+        reinterpret_cast<float4*>(xrow)[w] = __ldcg(reinterpret_cast<const float4*>(src) + w);
+    } else {
+#pragma unroll 1
+      for (int w = tid; w < own * m; w += kFrontThreads) xrow[w] = __ldcg(src + w);
+    }
+    if (tid < own) own_tok[tid] = tlo + tid;
+    FRONT_MARK(2);
+    FRONT_MARK(3);
+  }
+#pragma unroll 1
+  for (int c = 0; c < nch && kG == 0; ++c) {
     const int c0 = c * Tc;
     const int nc = n - c0 < Tc ? n - c0 : Tc;
     const int n_mma = (nc + 15) & ~15;
@@ -814,7 +837,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __syncthreads();
   FRONT_MARK(4);
   const uint32_t tag = s_tag;
-  if (warp == 2) {
+  if (warp == 2 && !kLin) {
     tc_fence_after();
     tmem_dealloc(tmem_base, a.tmem_cols);
   }
@@ -1278,10 +1301,184 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
 #undef FRONT_MARK
 }
 
+// ---------------------------------------------------------------------------
+// Router GEMM for large blocks, ahead of the front kernel (logits-in mode).
+// In the front, large blocks either re-stream W_r per token chunk (split-K)
+// or stream all of W_r into each of the 8 SMs (token split): ~12-17 us at
+// M = 256, N >= 64, bound by per-SM ingress. Here one 8-CTA cluster per
+// (32-token tile, 128-expert tile) splits K over its CTAs (each loads a 1/8
+// slice of one W_r tile, <= 64 KB, plus its X boxes), drains TMEM into a
+// stage and pushes each owner CTA its token rows with one bulk DSMEM copy;
+// the owner sums the 8 partials in fixed CTA order (deterministic logits)
+// and writes them to global memory. C3 N = 256: 16 clusters on 128 SMs.
+// The front (programmatic launch) sets up meanwhile and reads the logits
+// after griddepcontrol.wait.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1)
+    router_cluster_kernel(const __grid_constant__ CUtensorMap wr_map,
+                          const __grid_constant__ BoxMaps x_maps, const RouterArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bars[8 + 2];  // full[kb_cta <= 8], tdone, recv
+  __shared__ uint32_t tmem_slot[2];
+  constexpr int C = kFrontCta;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rk = static_cast<int>(cluster_rank());
+  const int cl = static_cast<int>(blockIdx.x) / C;
+  const int tt = cl / a.mtiles, mtile = cl - tt * a.mtiles;
+  const int t0 = tt * a.tc;
+  const int nt = a.n - t0 < a.tc ? a.n - t0 : a.tc;  // tokens of this cluster
+  const int e0 = mtile * kBM;
+  const int me = a.m - e0 < kBM ? a.m - e0 : kBM;     // experts of this tile
+  const int kb = a.kb_cta, kb0 = rk * kb;
+  const int ocm = (a.tc + C - 1) / C;                 // owner rows per sender
+  const uint32_t xbytes = static_cast<uint32_t>(a.b_rows) * 128u;
+  const int stage_bytes = kATile + a.b_rows * 128;
+  unsigned char* ring = smem;                                                   // [kb][W tile | X box]
+  float* stage = reinterpret_cast<float*>(smem + static_cast<size_t>(kb) * stage_bytes);  // [tc][128]
+  float* recv = stage + a.tc * kBM;                                             // [C][ocm][128]
+  uint64_t* full = bars;
+  uint64_t* tdone = bars + 8;
+  uint64_t* bar_recv = bars + 9;
+  const int lo = (nt * rk) / C, hi = (nt * (rk + 1)) / C;  // this CTA's owner rows
+  if (tid == 0) {
+    tma_prefetch_desc(&wr_map);
+    tma_prefetch_desc(&x_maps.map[a.box_index]);
+    for (int i = 0; i < kb; ++i) mbar_init(&full[i], 1);
+    mbar_init(tdone, 1);
+    mbar_init(bar_recv, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar_recv, static_cast<uint32_t>(C * (hi - lo) * kBM * 4));
+    const uint64_t pol = l2_policy_evict_last();  // W_r: re-read by every token tile
+    for (int i = 0; i < kb; ++i) {  // static weights: before the previous kernel is waited for
+      mbar_arrive_expect_tx(&full[i], kATile + xbytes);
+      tma_load_2d(ring + static_cast<size_t>(i) * stage_bytes, &wr_map, &full[i], (kb0 + i) * kBK,
+                  e0, pol);
+    }
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 32u < static_cast<uint32_t>(a.b_rows) ? a.b_rows : 32u);
+  pdl_launch_dependents();
+  pdl_wait();  // x is complete from here on
+  if (tid == 0) {
+    const uint64_t pol_x = l2_policy_evict_last();
+    for (int i = 0; i < kb; ++i)
+      tma_load_2d(ring + static_cast<size_t>(i) * stage_bytes + kATile, &x_maps.map[a.box_index],
+                  &full[i], (kb0 + i) * kBK, t0, pol_x);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot[0];
+  // every CTA's recv barrier is armed before anyone pushes
+  cluster_arrive_relaxed();
+  cluster_wait();
+  const int n_mma = (nt + 15) & ~15;
+  if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
+    for (int i = 0; i < kb; ++i) {
+      mbar_wait(&full[i], 0);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a0 = smem_u32(ring + static_cast<size_t>(i) * stage_bytes);
+        const uint32_t b0 = a0 + kATile;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          tc_mma_bf16(tmem_base, sw128_kmajor_desc(a0 + kk * 32), sw128_kmajor_desc(b0 + kk * 32),
+                      idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        if (i == kb - 1) tc_commit(tdone);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // drain: partial[token][expert] of this CTA's K slice
+    mbar_wait(tdone, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lb = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    for (int cc = 0; cc < n_mma; cc += 16) {
+      float v[16];
+      tmem_ld16(lb + cc, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (cc + j < nt) stage[(cc + j) * kBM + r] = v[j];
+    }
+    tc_fence_before();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    named_bar_sync(1, 128);
+    if (warp == 4 && lane < C) {
+      // one bulk copy per owner: its token rows -> recv[rk] there
+      const int lo_q = (nt * lane) / C, hi_q = (nt * (lane + 1)) / C;
+      const uint32_t bytes = static_cast<uint32_t>((hi_q - lo_q) * kBM * 4);
+      if (bytes)
+        bulk_s2cluster(mapa_u32(smem_u32(recv + rk * ocm * kBM), lane),
+                       smem_u32(stage + lo_q * kBM), bytes, mapa_u32(smem_u32(bar_recv), lane));
+    }
+  }
+  mbar_wait_cluster(bar_recv, 0);  // all C partials of this CTA's rows arrived
+  // owner sums in fixed CTA order -> logits
+  const int cnt = (hi - lo) * me;
+  for (int w = tid; w < cnt; w += blockDim.x) {
+    const int j = w / me, e = w - j * me;
+    float acc = 0.0f;
+#pragma unroll
+    for (int r = 0; r < C; ++r) acc += recv[(r * ocm + j) * kBM + e];
+    a.logits[static_cast<size_t>(t0 + lo + j) * a.m + e0 + e] = acc;
+  }
+  // no CTA exits while a peer's bulk copy may still read its stage
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 32u < static_cast<uint32_t>(a.b_rows) ? a.b_rows : 32u);
+  }
+}
+
+size_t router_cluster_smem(const RouterArgs& a) {
+  return 1024 + static_cast<size_t>(a.kb_cta) * (kATile + a.b_rows * 128) +
+         static_cast<size_t>(a.tc) * kBM * 4 +
+         static_cast<size_t>(kFrontCta) * ((a.tc + kFrontCta - 1) / kFrontCta) * kBM * 4;
+}
+
+cudaError_t launch_router_cluster(const CUtensorMap& wr_map, const BoxMaps& x_maps,
+                                  const RouterArgs& a, cudaStream_t st) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(kFrontCta * a.mtiles * ((a.n + a.tc - 1) / a.tc));
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = router_cluster_smem(a);
+  lc.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kFrontCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 2;
+  return cudaLaunchKernelEx(&lc, router_cluster_kernel, wr_map, x_maps, a);
+}
+
 // Host plan: token chunk, pipeline depth, shared memory. Returns false when
 // the shape is outside the kernel's envelope.
 bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem, int tsplit) {
   if (n < 1 || n > 256 || m < 1 || m > 256 || k < 1 || k > 32 || k > m) return false;
+  if (tsplit == 3) {
+    // logits in (router_cluster_kernel): no ring, no partial exchange
+    const int own_max = (n + kFrontCta - 1) / kFrontCta;
+    const FrontSmem p = front_smem_plan(n, m, k, n, own_max, 0, 0, n, 3);
+    if (p.total > static_cast<size_t>(kFrontSmemLimit)) return false;
+    a->tsplit = 3;
+    a->chunk = n;
+    a->own_max = own_max;
+    a->stages = 0;
+    a->b_rows = 16;
+    a->box_index = 0;
+    a->kb_per_cta = (d / kBK) / kFrontCta;
+    a->tmem_cols = 0;
+    a->vote_rows = n;
+    *smem = p.total;
+    return true;
+  }
   if (d % (kBK * kFrontCta)) return false;
   const int mt = (m + kBM - 1) / kBM;
   const int kb_cta = (d / kBK) / kFrontCta;
@@ -1349,15 +1546,16 @@ bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem, int tspl
 using FrontFn = void (*)(const CUtensorMap, const BoxMaps, const FrontArgs);
 
 // The instantiation for (strategy, token split, small block).
-static FrontFn front_variant(int strategy, bool tsplit, bool small) {
-#define DESMOE_FRONT_ROW(S)                                                              \
-  {front_kernel<S, false, false>, front_kernel<S, false, true>, front_kernel<S, true, false>, \
-   front_kernel<S, true, true>}
-  static const FrontFn table[3][4] = {DESMOE_FRONT_ROW(-1), DESMOE_FRONT_ROW(0),
+// kG: 0 split-K, 1 token split, 2 logits in (FrontArgs::tsplit 0 / 1-2 / 3)
+static FrontFn front_variant(int strategy, int kg, bool small) {
+#define DESMOE_FRONT_ROW(S)                                                      \
+  {front_kernel<S, 0, false>, front_kernel<S, 0, true>, front_kernel<S, 1, false>, \
+   front_kernel<S, 1, true>, front_kernel<S, 2, false>, front_kernel<S, 2, true>}
+  static const FrontFn table[3][6] = {DESMOE_FRONT_ROW(-1), DESMOE_FRONT_ROW(0),
                                       DESMOE_FRONT_ROW(1)};
 #undef DESMOE_FRONT_ROW
   const int si = strategy < 0 ? 0 : (strategy == 0 ? 1 : 2);
-  return table[si][(tsplit ? 2 : 0) + (small ? 1 : 0)];
+  return table[si][2 * kg + (small ? 1 : 0)];
 }
 
 cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,
@@ -1380,20 +1578,23 @@ cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const
   // selection and the activation run side by side (DESMOE_FRONT_FLAGS bit 2
   // forces the sequential L stage, for A/B runs)
   const bool small = a.own_max <= kFrontThreads / 64 && !(a.flags & 2);
-  return cudaLaunchKernelEx(&lc, front_variant(a.strategy, a.tsplit != 0, small), wr_map, x_maps,
-                            a);
+  const int kg = a.tsplit == 3 ? 2 : (a.tsplit != 0 ? 1 : 0);
+  return cudaLaunchKernelEx(&lc, front_variant(a.strategy, kg, small), wr_map, x_maps, a);
 }
 
 cudaError_t set_front_smem_limit() {
   cudaError_t e = cudaSuccess;
   for (int strategy = -1; strategy <= 1; ++strategy)
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 6; ++v) {
       const cudaError_t r = cudaFuncSetAttribute(
-          reinterpret_cast<const void*>(front_variant(strategy, v >= 2, v & 1)),
+          reinterpret_cast<const void*>(front_variant(strategy, v / 2, v & 1)),
           cudaFuncAttributeMaxDynamicSharedMemorySize, kFrontSmemLimit);
       if (e == cudaSuccess) e = r;
     }
-  return e;
+  const cudaError_t r = cudaFuncSetAttribute(reinterpret_cast<const void*>(router_cluster_kernel),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+  return e == cudaSuccess ? r : e;
 }
 
 }  // namespace desmoe

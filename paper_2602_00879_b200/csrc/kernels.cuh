@@ -63,7 +63,7 @@ struct FrontArgs {
   int n, m, k, act, strategy, seq_k, m_core, raw;
   int b_rows, box_index, kb_per_cta, stages, tmem_cols;
   int chunk, own_max;  // token chunk of the split-K GEMM; own tokens per CTA bound
-  int tsplit;          // 1: token-split router GEMM (multicast W_r, no partial exchange)
+  int tsplit;          // 1/2: token-split router GEMM; 3: logits in (router_cluster_kernel)
   int vote_rows;       // token rows of the shared-memory vote matrix chunk
   int* route_idx;      // [n x k]
   double* route_gate;  // [n x k]
@@ -72,6 +72,7 @@ struct FrontArgs {
   int* n_members;      // [1]
   double* votes;       // [m] optional
   float* logits_out;   // [n x m] optional fp32 logits
+  const float* logits_in;  // [n x m] fp32 logits (tsplit == 3: router_cluster_kernel ran ahead)
   int* err;
   uint64_t* trace;     // optional timeline (events 40+)
   int trace_cap;
@@ -82,6 +83,22 @@ struct FrontArgs {
   uint64_t* route_words;   // [n x k] {gate f32 | tag | expert}, expert kPadExpert = none
   int flags;               // experiments (DESMOE_FRONT_FLAGS)
 };
+
+// Router GEMM ahead of the front kernel for large blocks (front.cu,
+// router_cluster_kernel): one 8-CTA cluster per (token tile, 128-expert tile),
+// split-K over the cluster, partials summed by their owner CTA in fixed CTA
+// order; logits [n x m] fp32 to global memory, read by the front in its
+// logits-in mode (FrontArgs::tsplit == 3).
+struct RouterArgs {
+  int n, m, d;
+  int tc;        // tokens per cluster
+  int mtiles;    // 128-expert tiles (clusters per token tile)
+  int kb_cta;    // 64-wide K blocks per CTA (d / 64 / 8)
+  int b_rows;    // X box rows (>= tc)
+  int box_index;
+  float* logits;  // [n x m]
+};
+constexpr int kRouterTc = 32;  // tokens per router cluster
 
 // Tagged hand-off words (front -> FFN). A word is valid for the current call
 // when its 22-bit tag equals the call sequence number (mod 2^22); every word
@@ -315,6 +332,8 @@ __global__ void ep_wait_kernel(CombineArgs a);
 cudaError_t launch_front(const CUtensorMap& wr_map, const BoxMaps& x_maps, const FrontArgs& a,
                          size_t smem, cudaStream_t st);
 cudaError_t set_front_smem_limit();
+cudaError_t launch_router_cluster(const CUtensorMap& wr_map, const BoxMaps& x_maps,
+                                  const RouterArgs& a, cudaStream_t st);
 
 // ---- exact fp64 gating primitives (gating_exact.cu) ----
 __global__ void select_top_kernel(const double* __restrict__ values, int m, int k,
