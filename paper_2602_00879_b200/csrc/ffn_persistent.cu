@@ -1039,6 +1039,10 @@ __device__ __forceinline__ void combine_retire(const CombineArgs& a) {
 }
 
 __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
+  // the next layer's router / front may launch at once: they prefetch their
+  // static router weights and set up under this kernel, and their own
+  // griddepcontrol.wait orders every read of this kernel's output
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // before the FFN grid completes: the call's tag and this thread's route
   // (the front's tagged words; the previous call's sequence bump completed
   // before this call's front started), so after the wait only the rows'
@@ -1103,6 +1107,7 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
 }
 
 __global__ void __launch_bounds__(256) combine_slots_kernel(CombineArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (as combine_dense_kernel)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 80, -1);
   __shared__ int s_epoch;

@@ -2,6 +2,9 @@
 // a single 8-CTA thread-block CLUSTER (one CTA per SM, 16 warps each), for
 // every block size N <= 256 and pool size M <= 256.
 //
+//   (blocks > 32 tokens or pools > 128 experts: R runs ahead in
+//      router_cluster_kernel, one cluster per 32 tokens x 128 experts, and
+//      this kernel reads the logits: FrontArgs::tsplit == 3)
 //   R  router GEMM, split-K over the cluster, token-chunked so the partials
 //      fit in shared memory: for each chunk of Tc tokens, CTA r multiplies
 //      W_r[:, K-slice r] by X[chunk, K-slice r] on tcgen05 (swap-AB: 128
@@ -19,12 +22,15 @@
 //      could flip (gap <= 2^-40, or underflow) re-selects exactly on the fp64
 //      probabilities with the reference's comparator;
 //   V  every token's owner pushes its top-`depth` (ids, weights) to every CTA
-//      over DSMEM; every CTA computes the coreset redundantly: DES-Vote
-//      rebuilds the reference's masked N x M matrix (des.cpp:73-84) in
-//      shared memory, sums each expert's column in ascending token order
-//      (des.cpp:86-91) and keeps the top floor(beta*M) by (vote desc, index
-//      asc) with a rank count (des.cpp:93); DES-Seq takes the union of the
-//      top-seq_k (des.cpp:33-45);
+//      over DSMEM; every CTA computes the votes redundantly: the reference
+//      sums each column of its masked N x M matrix (des.cpp:73-91) in
+//      ascending token order, zeros included; zeros leave an fp64 sum
+//      unchanged, so the (token, expert) pairs are bucketed by expert with a
+//      stable counting sort and each expert sums its own bucket in token
+//      order — the same additions, no N x M matrix. The coreset = top
+//      floor(beta*M) by (vote desc, index asc) via a rank count (des.cpp:93),
+//      split over the cluster for pools > 64 (membership words exchanged
+//      over DSMEM); DES-Seq takes the union of the top-seq_k (des.cpp:33-45);
 //   RR constrained re-route + renormalisation of own tokens (des.cpp:97-118);
 //      VANILLA writes topk_route's gates right after L.
 // Every intermediate stays on chip. The kernel also zeroes the expert-FFN
@@ -326,6 +332,49 @@ __device__ __noinline__ void front_tail(float* logits_out, const float* xrow, co
 
 }  // namespace
 
+// L3 activation over the CTA's (own token, expert) pairs, threads t0, t0 +
+// stride, ...: softmax numerators exp(x - max) (gating.cpp:24-38) four per
+// thread in flight and inlined (an out-of-line call per element serialised
+// its latency chain: C3 N=256 -1.4 us), sigmoid / identity through the
+// out-of-line helpers; the reference's fp64 operations either way.
+// (kUnroll: the large-block path. Small blocks run a few exps per thread
+// once, where the 4-wide inlined body's instruction fetch cost more than it
+// saved: C3 N = 32 / 64 activation +1.4 / +1.0 us.)
+template <bool kUnroll>
+__device__ __forceinline__ void activate_rows(const float* xrow, const float* mxv, double* erow,
+                                              int ew, int own, int m, int act,
+                                              const unsigned long long* tab, int t0, int stride) {
+  int w0 = t0;
+  if (kUnroll && act == 0) {
+#pragma unroll 1
+    for (; w0 + 3 * stride < own * m; w0 += 4 * stride) {
+      double ex[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int w = w0 + u * stride;
+        ex[u] = glibc_exp(static_cast<double>(xrow[w]) - static_cast<double>(mxv[w / m]), tab);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int w = w0 + u * stride;
+        const int j = w / m, i = w - j * m;
+        erow[j * ew + i] = ex[u];
+      }
+    }
+  }
+#pragma unroll 1
+  for (int w = w0; w < own * m; w += stride) {
+    const int j = w / m, i = w - j * m;
+    const double x = static_cast<double>(xrow[w]);
+    double e = x;
+    if (act < 2) {
+      const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x, tab);
+      e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
+    }
+    erow[j * ew + i] = e;
+  }
+}
+
 // Shared-memory plan (host and device agree on it).
 struct FrontSmem {
   size_t ring, erow, dreg, scratch, partial, xrow, mx, ssum, sel, wsel, wp, own_tok, flag,
@@ -545,8 +594,12 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_exptab + 2 * tid)),
                  "l"(kExpTab + 2 * tid)
                  : "memory");
-  pdl_launch_dependents();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
+  // the expert-FFN kernel may launch now — not earlier: it reads the call
+  // sequence word the previous call's combine advances, and that combine
+  // lets the next kernels launch at ITS start (cross-layer overlap in a
+  // stack), so only this wait orders the FFN behind it
+  pdl_launch_dependents();
   // the first ring stages' X boxes go out at once (their W_r halves and the
   // stages' transaction counts were armed in the setup): no CTA barrier or
   // cluster barrier on the way to the router GEMM's inputs
@@ -898,17 +951,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       named_bar_sync(3, kFrontThreads / 2);
       if (tracing && gt == 0) s_ts[5] = gtime();
       // L3: activation in fp64, data-parallel over (own token, expert)
-#pragma unroll 1
-      for (int w = gt; w < own * m; w += kFrontThreads / 2) {
-        const int j = w / m, i = w - j * m;
-        const double x = static_cast<double>(xrow[w]);
-        double e = x;
-        if (act < 2) {
-          const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x, s_exptab);
-          e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
-        }
-        erow[j * ew + i] = e;
-      }
+      activate_rows<false>(xrow, mxv, erow, ew, own, m, act, s_exptab, gt, kFrontThreads / 2);
       named_bar_sync(3, kFrontThreads / 2);
       named_bar_arrive(2, kFrontThreads);  // hand the activation to the selectors
       if (tracing && gt == 0) s_ts[6] = gtime();
@@ -958,38 +1001,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     __syncthreads();
     FRONT_MARK(5);
     // ---- L3: activation in fp64, data-parallel over (own token, expert) ----------
-    // softmax: four exps per thread in flight, inlined (many per thread here,
-    // so the out-of-line call's serialised latency chains dominated)
-    int w0 = tid;
-    if (act == 0) {
-#pragma unroll 1
-      for (; w0 + 3 * kFrontThreads < own * m; w0 += 4 * kFrontThreads) {
-        double ex[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int w = w0 + u * kFrontThreads;
-          const int j = w / m;
-          ex[u] = glibc_exp(static_cast<double>(xrow[w]) - static_cast<double>(mxv[j]), s_exptab);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int w = w0 + u * kFrontThreads;
-          const int j = w / m, i = w - j * m;
-          erow[j * ew + i] = ex[u];
-        }
-      }
-    }
-#pragma unroll 1
-    for (int w = w0; w < own * m; w += kFrontThreads) {
-      const int j = w / m, i = w - j * m;
-      const double x = static_cast<double>(xrow[w]);
-      double e = x;
-      if (act < 2) {
-        const double ex = f_exp(act == 0 ? x - static_cast<double>(mxv[j]) : -x, s_exptab);
-        e = act == 0 ? ex : f_div(1.0, 1.0 + ex);  // softmax numerator / sigmoid
-      }
-      erow[j * ew + i] = e;
-    }
+    activate_rows<true>(xrow, mxv, erow, ew, own, m, act, s_exptab, tid, kFrontThreads);
     __syncthreads();
     FRONT_MARK(6);
     // ---- L4: ordered softmax sums (one lane per token, last warp) || top-K (others)
