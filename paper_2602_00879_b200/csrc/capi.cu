@@ -200,7 +200,8 @@ struct desmoe_experts {
   int* ep_state = nullptr;                  // [0] call seq (EP epoch), [1] combine CTAs done
   // front -> FFN hand-off words (tagged with the call seq, see kernels.cuh)
   uint64_t* route_words = nullptr;          // [max_n * max_k]
-  uint32_t* pub = nullptr;                  // [1 + max_m]
+  uint32_t* pub = nullptr;                  // [1 + max_m] (+ route_done)
+  uint32_t* route_done = nullptr;           // [kFrontCta], inside the pub allocation
   float* peer_slot[kMaxWorld] = {};
   unsigned long long* peer_flag[kMaxWorld] = {};
   void* ipc_mapped[2 * kMaxWorld] = {};     // peer buffers opened by desmoe_ep_import
@@ -782,8 +783,12 @@ int desmoe_experts_create_ep(desmoe_ctx* c, int kind, int m, int lo, int hi, int
   if (e == cudaSuccess) e = cudaMemset(ex->ep_state, 0, 256);
   if (e == cudaSuccess) e = cudaMalloc(&ex->route_words, slots * sizeof(uint64_t));
   if (e == cudaSuccess) e = cudaMemset(ex->route_words, 0xFF, slots * sizeof(uint64_t));
-  if (e == cudaSuccess) e = cudaMalloc(&ex->pub, (static_cast<size_t>(c->max_m) + 1) * 4);
-  if (e == cudaSuccess) e = cudaMemset(ex->pub, 0xFF, (static_cast<size_t>(c->max_m) + 1) * 4);
+  // published list [1 + max_m], then (own 128-byte line) the front CTAs'
+  // route-complete words [kFrontCta]
+  const size_t pub_words = (static_cast<size_t>(c->max_m) + 1 + 31) / 32 * 32 + 32;
+  if (e == cudaSuccess) e = cudaMalloc(&ex->pub, pub_words * 4);
+  if (e == cudaSuccess) e = cudaMemset(ex->pub, 0xFF, pub_words * 4);
+  ex->route_done = ex->pub + pub_words - 32;
   if (e != cudaSuccess) {
     desmoe_experts_destroy(ex);
     return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
@@ -989,6 +994,7 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   if (const char* fl = std::getenv("DESMOE_FFN_FLAGS")) a.flags |= std::atoi(fl);  // experiments
   a.pub = ex->pub;
   a.route_words = ex->route_words;
+  a.route_done = ex->route_done;
   a.wa_base = ex->packed_a;
   a.wc_base = ex->packed_b;
   const size_t slot_stride = static_cast<size_t>(c->max_n) * c->max_k * d;
@@ -1280,6 +1286,7 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   a.seq = ex->ep_state;
   a.pub = ex->pub;
   a.route_words = ex->route_words;
+  a.route_done = ex->route_done;
   a.err = c->err;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;

@@ -478,6 +478,10 @@ __device__ inline uint32_t ld_acquire_u32(const uint32_t* p) {
   return v;
 }
 
+__device__ inline void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ inline void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

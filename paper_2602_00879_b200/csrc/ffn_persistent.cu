@@ -441,6 +441,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (a.flags & 2) {  // (A/B runs: warp 1 alone, one batch per round trip)
       if (warp == 1)
         for (int b0 = 0; b0 < total; b0 += 256) poll_batch(b0);
+    } else if (a.route_done && !(a.flags & 4)) {
+      // one lane waits for the 8 front CTAs' route-complete words
+      // — one 32-byte sector, polled with a short back-off — then every
+      // warp loads its share of the route words once (their tags are
+      // re-checked, so a stale word can never be taken)
+      if (tid == 32) {
+#pragma unroll 1
+        for (;;) {
+          bool all = true;
+#pragma unroll
+          for (int r = 0; r < kFrontCta; ++r)
+            all &= ld_relaxed_u32(a.route_done + r) == tag;
+          if (all) break;
+          __nanosleep(64);
+        }
+      }
+      __syncthreads();
+      for (int b = warp; b * 256 < total; b += kThreads / 32) poll_batch(b * 256);
     } else {
       if (warp == 1) poll_batch(0);
       __syncthreads();

@@ -222,8 +222,8 @@ __device__ __noinline__ void write_route(const double* e, double s, int act, con
   const int lane = threadIdx.x & 31;
   const int my = lane < cnt ? selr[lane] : 0x7fffffff;
   int pos = 0;  // ascending position among the selected (indices are distinct)
-#pragma unroll
-  for (int j = 0; j < 32; ++j) pos += __shfl_sync(0xffffffffu, my, j) < my;  // pads are INT_MAX
+#pragma unroll 1
+  for (int j = 0; j < cnt; ++j) pos += __shfl_sync(0xffffffffu, my, j) < my;  // (cnt <= 32)
   if (lane >= cnt) pos = lane;  // padding slots cnt .. k-1
   double p = 0.0;
   if (lane < cnt) {
@@ -252,19 +252,56 @@ __device__ __noinline__ void write_route(const double* e, double s, int act, con
 }
 
 // True if the boundary between ranks b-1 and b of `sel` could order
-// differently on the reference's fp64 gate values (gating.cpp:49-52): equal
-// truncated keys (index-ordered by the fast path), a logit gap exp/division
-// rounding could close (<= 2^-40) or an underflowing rejected gate (softmax),
-// or gates within 2^-40 relative of each other (sigmoid/identity).
-__device__ inline bool risky_boundary(const float* x, const double* e, int act, const int* sel,
-                                      int b) {
+// differently on the reference's fp64 gate values (gating.cpp:49-52): a
+// logit gap exp/division rounding could close (<= 2^-40) or an underflowing
+// rejected gate (softmax), or gates within 2^-40 relative of each other
+// (sigmoid/identity).
+__device__ inline bool fp64_risky(const float* x, const double* e, int act, const int* sel, int b) {
   const int hi = sel[b - 1], lo = sel[b];
-  if ((sel_key(x[hi], hi) >> 8) == (sel_key(x[lo], lo) >> 8)) return true;
   if (act == 0) {
     const double gap = static_cast<double>(x[hi]) - static_cast<double>(x[lo]);
     return !(gap > 0x1.0p-40) || !(e[lo] > 0x1.0p-960);
   }
   return near_tie(e[hi], e[lo]);
+}
+// ... or, for the fast selection's keys, equal truncated keys (index-ordered
+// by the fast path).
+__device__ inline bool risky_boundary(const float* x, const double* e, int act, const int* sel,
+                                      int b) {
+  const int hi = sel[b - 1], lo = sel[b];
+  if ((sel_key(x[hi], hi) >> 8) == (sel_key(x[lo], lo) >> 8)) return true;
+  return fp64_risky(x, e, act, sel, b);
+}
+
+// The first `rounds` entries of (fp32 logit desc, index asc) order, exactly:
+// full 32-bit logit keys, then the lowest index among the keys that won —
+// two REDUX per round. For boundaries the truncated keys cannot order.
+__device__ __noinline__ void warp_rank_select_exact32(const float* x, int m, int rounds,
+                                                      const uint8_t* allow, int* sel) {
+  const int lane = threadIdx.x & 31;
+  uint32_t k[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int i = lane + 32 * s;
+    k[s] = (i < m && (!allow || allow[i])) ? fkey(x[i]) : 0u;  // fkey > 0 for every float
+  }
+#pragma unroll 1
+  for (int r = 0; r < rounds; ++r) {
+    uint32_t best = k[0];
+#pragma unroll
+    for (int s = 1; s < 8; ++s) best = k[s] > best ? k[s] : best;
+    const uint32_t win = __reduce_max_sync(0xffffffffu, best);
+    uint32_t idx = 0xffffffffu;
+#pragma unroll
+    for (int s = 7; s >= 0; --s)
+      if (win && k[s] == win) idx = static_cast<uint32_t>(lane + 32 * s);
+    const uint32_t wi = __reduce_min_sync(0xffffffffu, idx);
+    if (lane == 0) sel[r] = win ? static_cast<int>(wi) : -1;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (win && static_cast<uint32_t>(lane + 32 * s) == wi) k[s] = 0u;
+  }
+  __syncwarp();
 }
 
 // Exact re-selection on the reference's probabilities p = e / s (softmax) or
@@ -276,6 +313,22 @@ __device__ __noinline__ void exact_reselect(const double* e, double s, int act, 
   for (int i = lane; i < m; i += 32) scratch[i] = act == 0 ? f_div(e[i], s) : e[i];
   __syncwarp();
   warp_select(scratch, m, want, allow, sel);
+}
+
+// A boundary the fast selection could not order (risky_boundary): re-select
+// on exact fp32 logit keys first (m <= 256); only a boundary that is still
+// ambiguous on the fp64 gates (equal logits, gap <= 2^-40, underflow) pays
+// for the full fp64 re-selection (measured ~13 us for one token at M = 256,
+// where the fp32 re-selection costs ~1 us). `b2` < want: a second boundary
+// (DES-Seq's seq_k) that must be exact too.
+__device__ __noinline__ void fix_boundary(const float* x, const double* e, double s, int act,
+                                          int m, int want, int b2, const uint8_t* allow,
+                                          double* scratch, int* sel) {
+  warp_rank_select_exact32(x, m, want < m ? want + 1 : want, allow, sel);
+  bool r = false;
+  if (want < m && sel[want] >= 0) r = fp64_risky(x, e, act, sel, want);
+  if (b2 > 0 && b2 < want) r |= fp64_risky(x, e, act, sel, b2);
+  if (r) exact_reselect(e, s, act, m, want, allow, scratch, sel);
 }
 
 // timeline marks 0..count-1 of this CTA -> trace buffer as events 100 + i
@@ -629,11 +682,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // from shared memory after the GEMM's barrier (loaded by every thread at
   // this point, it stalled all 16 warps, the MMA issuer included, ~1 us)
   if (tid == 96) s_tag = a.seq ? hand_tag(*a.seq) : 0u;
-  if (!(a.flags & 1) && warp >= 8 && warp < 12) {
+  if (!(a.flags & 1) && warp >= 8 && warp < 13) {
     // instruction-cache prewarm: the layer's FFN streams hundreds of MB
     // between two calls, so this kernel's code comes back from far memory and
     // every new code region costs a miss chain (~2 µs measured at the top-K
-    // entry). While the router GEMM runs, four idle warps each run one later
+    // entry). While the router GEMM runs, five idle warps each run one later
     // phase's code once on scratch (s_pw; 32 dummy experts), in parallel so
     // the misses overlap (DESMOE_FRONT_FLAGS=1 disables)
     uint8_t* df = reinterpret_cast<uint8_t*>(s_pw + 48);      // [32] flags; pub words at +52
@@ -649,9 +702,16 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       df[lane] = static_cast<uint8_t>(lane & 1);
       __syncwarp();
       publish_list(df, 32, 0u, reinterpret_cast<uint32_t*>(s_pw + 52), nullptr, nullptr);
-    } else {
+    } else if (warp == 11) {
       write_route(erow, 1.0, 2, ds, 0, 0, 0, reinterpret_cast<double*>(s_pw + 64), nullptr,
                   nullptr, ds, nullptr, 0u);
+    } else {
+      // the exact near-tie re-selection (fp64 gates + the reference's
+      // comparator): rare, but cold it cost a block ~9 us (C3 N = 64, one
+      // token whose K-th and (K+1)-th logits share their top 24 key bits)
+      warp_rank_select_exact32(reinterpret_cast<const float*>(erow), 32, 9, nullptr, ds);
+      exact_reselect(reinterpret_cast<const double*>(s_pw), 1.0, 0, 32, 8, nullptr,
+                     reinterpret_cast<double*>(s_pw), ds);
     }
   }
 
@@ -1067,7 +1127,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       int* sj = sel + j * 33;
       const double* er = erow + j * ew;
       const double s = ssum[j];
-      if (risky[j]) exact_reselect(er, s, act, m, want, nullptr, scratch, sj);  // rare
+      if (risky[j])  // rare
+        fix_boundary(xrow + j * m, er, s, act, m, want, vanilla ? 0 : depth, nullptr, scratch, sj);
       if constexpr (vanilla) {
         write_route(er, s, act, sj, want, k, own_tok[j], wp, a.route_idx, a.route_gate,
                     a.route_cnt, a.route_words, tag);
@@ -1098,6 +1159,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   __syncthreads();
   FRONT_MARK(8);
   if constexpr (vanilla) {
+    if (tid == 0 && a.route_done)  // route words out (a hint: see the DES path's RR)
+      st_relaxed_u32(a.route_done + rk, tag);
     if (rk == 0 && a.pub) {
       // union of every token's top-K = the experts the FFN will stream
       mbar_wait_cluster(bar_selx, 0);
@@ -1278,8 +1341,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     int* wsel = wsel_all + warp * 33;
     double* wp = reinterpret_cast<double*>(smem + P.wp) + warp * 32;
     double* scratch = reinterpret_cast<double*>(smem + P.scratch) + warp * m;
+    if (tracing && tid < 3) s_ts[38 + tid] = 0;
+    __syncthreads();
 #pragma unroll 1
     for (int j = warp; j < own; j += NW) {
+      const long long rr0 = clock64();
       const int* sj = sel + j * 33;
       const float* xr = xrow + j * m;
       const double* er = erow + j * ew;
@@ -1292,16 +1358,32 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
         __syncwarp();
       }
       const int cnt = k < nm ? k : nm;
+      bool r = false;
       if (!covered) {
         const int rounds = cnt < nm ? cnt + 1 : cnt;
         warp_rank_select(xr, m, rounds, flag, wsel);  // rank order
-        const bool r = cnt < nm && risky_boundary(xr, er, act, wsel, cnt);
-        if (r) exact_reselect(er, s, act, m, cnt, flag, scratch, wsel);  // rare
+        r = cnt < nm && risky_boundary(xr, er, act, wsel, cnt);
+        if (r) fix_boundary(xr, er, s, act, m, cnt, 0, flag, scratch, wsel);  // rare
       }
       write_route(er, s, act, wsel, cnt, k, own_tok[j], wp, a.route_idx, a.route_gate,
                   a.route_cnt, a.route_words, tag);
+      if (tracing && lane == 0) {  // (timeline: slowest token, uncovered / exact masks)
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_ts[38]),
+                  static_cast<unsigned long long>(clock64() - rr0));
+        if (!covered) atomicOr(reinterpret_cast<unsigned long long*>(&s_ts[39]), 1ull << j);
+        if (r) atomicOr(reinterpret_cast<unsigned long long*>(&s_ts[40]), 1ull << j);
+      }
     }
   }
+  // this CTA's route words are all out: one release word for the expert-FFN
+  // kernel (routed mode), which polls these 8 words, not the N*K route words
+  // (140 CTAs re-reading the same 2-16 KB of route words flooded their L2
+  // lines: the routed prologue took 11-20 us after the front had finished)
+  // (No fence: a GPU-scope MEMBAR here cost one CTA up to 10 us. The word is
+  // only a hint — the route words carry the tag themselves and the FFN
+  // re-polls any word whose tag is not yet this call's.)
+  __syncthreads();
+  if (tid == 0 && a.route_done) st_relaxed_u32(a.route_done + rk, tag);
   FRONT_MARK(13);
   if (tracing && tid == 0) s_ts[25] = clock64();
   cluster_wait();  // #3: no CTA exits while others may still read its shared memory

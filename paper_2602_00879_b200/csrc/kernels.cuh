@@ -81,6 +81,7 @@ struct FrontArgs {
   const int* seq;          // [1] bumped by the combine kernel after every call
   uint32_t* pub;           // [1 + m] {tag | count}, {tag | expert} ...
   uint64_t* route_words;   // [n x k] {gate f32 | tag | expert}, expert kPadExpert = none
+  uint32_t* route_done;    // [kFrontCta] tag, stored (release) once a CTA's route words are out
   int flags;               // experiments (DESMOE_FRONT_FLAGS)
 };
 
@@ -239,6 +240,7 @@ struct FfnArgs {
   int early;
   const uint32_t* pub;
   const uint64_t* route_words;
+  const uint32_t* route_done;  // [kFrontCta] the front CTAs' route-complete tags
   const void* wa_base;       // packed gate/up tiles (L2 prefetch of the first unit)
   const void* wc_base;       // packed W_d / W_lin tiles
   int flags;                 // experiments: 1 = no L2 prefetch of the first unit

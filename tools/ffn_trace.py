@@ -106,10 +106,18 @@ def main():
         cyc = rec[ev == FB + 25][:, 1].astype(np.int64) - rec[ev == FB + 24][:, 1].astype(np.int64)
         ns = rec[ev == FB + 13][:, 1].astype(np.int64) - rec[ev == FB][:, 1].astype(np.int64)
         out["front_sm_mhz"] = [round(float(c) / float(t) * 1e3, 1) for c, t in zip(cyc, ns)]
+    by_cta = {}
     for i, nm in enumerate(fnames):
         e_ = FB + i
         if nm and (ev == e_).any():
             out["front_" + nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
+            sel_ = ev == e_
+            by_cta[nm] = {int(c): round(float(x), 2) for c, x in zip(cta[sel_], t[sel_])}
+    for e_, nm in ((FB + 38, "rr_max_cycles"), (FB + 39, "rr_uncovered_mask"), (FB + 40, "rr_exact_mask")):
+        sel_ = ev == e_
+        if sel_.any():
+            by_cta[nm] = {int(c): int(x) for c, x in zip(cta[sel_], rec[sel_][:, 1])}
+    out["front_by_cta"] = by_cta
     for e_, nm in names.items():
         if (ev == e_).any():
             out[nm] = [round(float(t[ev == e_].min()), 2), round(float(t[ev == e_].max()), 2)]
