@@ -682,11 +682,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // from shared memory after the GEMM's barrier (loaded by every thread at
   // this point, it stalled all 16 warps, the MMA issuer included, ~1 us)
   if (tid == 96) s_tag = a.seq ? hand_tag(*a.seq) : 0u;
-  if (!(a.flags & 1) && warp >= 8 && warp < 13) {
+  if (!(a.flags & 1) && warp >= 8 && warp < 12) {
     // instruction-cache prewarm: the layer's FFN streams hundreds of MB
     // between two calls, so this kernel's code comes back from far memory and
     // every new code region costs a miss chain (~2 µs measured at the top-K
-    // entry). While the router GEMM runs, five idle warps each run one later
+    // entry). While the router GEMM runs, four idle warps each run one later
     // phase's code once on scratch (s_pw; 32 dummy experts), in parallel so
     // the misses overlap (DESMOE_FRONT_FLAGS=1 disables)
     uint8_t* df = reinterpret_cast<uint8_t*>(s_pw + 48);      // [32] flags; pub words at +52
@@ -702,17 +702,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       df[lane] = static_cast<uint8_t>(lane & 1);
       __syncwarp();
       publish_list(df, 32, 0u, reinterpret_cast<uint32_t*>(s_pw + 52), nullptr, nullptr);
-    } else if (warp == 11) {
+    } else {
       write_route(erow, 1.0, 2, ds, 0, 0, 0, reinterpret_cast<double*>(s_pw + 64), nullptr,
                   nullptr, ds, nullptr, 0u);
-    } else {
-      // the exact near-tie re-selection (fp64 gates + the reference's
-      // comparator): rare, but cold it cost a block ~9 us (C3 N = 64, one
-      // token whose K-th and (K+1)-th logits share their top 24 key bits)
-      warp_rank_select_exact32(reinterpret_cast<const float*>(erow), 32, 9, nullptr, ds);
-      exact_reselect(reinterpret_cast<const double*>(s_pw), 1.0, 0, 32, 8, nullptr,
-                     reinterpret_cast<double*>(s_pw), ds);
     }
+    // (The exact near-tie path is not prewarmed: a fifth prewarm warp running
+    // it cost the coreset 2-2.7 us at C2/C3 N = 32 — that warp joins the
+    // activation late — more than its rare cold misses.)
   }
 
   // ---- R + L1: per token chunk, split-K GEMM, then the owners' logit sums ----------

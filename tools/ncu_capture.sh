@@ -19,4 +19,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffn_
   -s 15 -c 1 -f -o $OUT/ffn_${CFG}_${TAG} $B > $OUT/ncu_ffn_${CFG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:front_kernel \
   -s 15 -c 1 -f -o $OUT/front_${CFG}_${TAG} $B > $OUT/ncu_front_${CFG}.log 2>&1
+# the router GEMM kernel that runs ahead of the front for blocks > 32 tokens
+# or pools > 128 experts (C3)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:router_cluster_kernel \
+  -s 15 -c 1 -f -o $OUT/router_${CFG}_${TAG} $B > $OUT/ncu_router_${CFG}.log 2>&1
 ls -la $OUT
