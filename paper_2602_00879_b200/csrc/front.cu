@@ -682,7 +682,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // from shared memory after the GEMM's barrier (loaded by every thread at
   // this point, it stalled all 16 warps, the MMA issuer included, ~1 us)
   if (tid == 96) s_tag = a.seq ? hand_tag(*a.seq) : 0u;
-  if (!(a.flags & 1) && warp >= 8 && warp < 12) {
+  // (logits-in mode has no GEMM to hide the prewarm behind: skipped)
+  if (!kLin && !(a.flags & 1) && warp >= 8 && warp < 12) {
     // instruction-cache prewarm: the layer's FFN streams hundreds of MB
     // between two calls, so this kernel's code comes back from far memory and
     // every new code region costs a miss chain (~2 µs measured at the top-K
