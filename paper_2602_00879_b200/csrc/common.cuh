@@ -492,6 +492,13 @@ __device__ inline int ld_acquire(const int* p) {
   return v;
 }
 
+// release increment without a returned value: the thread does not wait for
+// the atomic's response (under a full TMA ring every response to an SM
+// queues behind the weights in flight, ~3-4 us)
+__device__ inline void red_add_release(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ inline int atomic_add_release(int* p, int v) {
   int old;
   asm volatile("atom.add.release.gpu.global.s32 %0, [%1], %2;"

@@ -240,6 +240,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int b_box_bytes = a.b_rows * 128;
   const int stage_bytes = KB * kATile + KB * b_box_bytes;
 
+  // phase-A H hand-off: the epilogue passes (expert tile, tiles) through a
+  // 2-slot mailbox to warp 2, which does the GPU-scope release of the
+  // readiness flags (a release waits for the SM's outstanding memory
+  // traffic, ~3-4 us behind a full TMA ring: off the epilogue's path)
+  __shared__ uint64_t s_hfull[2], s_hempty[2];
+  __shared__ int s_hinfo[2];
+  const bool h_delegate = !(a.flags & 8);
   // ---- shared-memory carve-up --------------------------------------------
   unsigned char* ring = smem;
   unsigned char* p = ring + static_cast<size_t>(S) * stage_bytes;
@@ -289,6 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int q = 0; q < kQ; ++q) {
       mbar_init(&qfull[q], 1);
       mbar_init(&qempty[q], 3);  // MMA lane + activation producer + epilogue
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_hfull[b], 1);
+      mbar_init(&s_hempty[b], 1);
     }
     fence_mbar_init();
   }
@@ -581,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (!dense && tid == 0 && static_cast<int>(blockIdx.x) < a.gather_ctas) {
     if (a.trace) s_pts[3] = gtime();
     __threadfence();
-    atomic_add_release(x_ready, 1);
+    red_add_release(x_ready, 1);
     if (a.trace) s_pts[4] = gtime();
     trace_put(tc, 1, -1);
   }
@@ -793,19 +804,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.stats[2] = sel;
       }
     }
+    if (h_delegate && swiglu) {
+      // phase-A releases, in the epilogue's order (see s_hinfo)
+      for (uint32_t kk = 0;; ++kk) {
+        const int sl = kk & 1;
+        mbar_wait(&s_hfull[sl], (kk >> 1) & 1u);
+        const int info = s_hinfo[sl];
+        if (info < 0) break;
+        if (lane == 0) {
+          __threadfence();  // the epilogue's H stores (observed through the mailbox)
+          for (int tt = 0; tt < (info >> 24); ++tt) red_add_release(&h_ready[(info & 0xFFFFFF) + tt], 1);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_hempty[sl]);
+      }
+    }
   } else if (warp >= 4) {
     // ============ epilogue ============
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;  // accumulator row = weight row within the tile
     const int etid = tid - 128;    // 0..127
-    uint32_t nunit = 0;
+    uint32_t nunit = 0, na = 0;
+    auto h_mail = [&](int info) {  // etid 0: hand a phase-A unit (or the end) to warp 2
+      const int sl = na & 1;
+      mbar_wait(&s_hempty[sl], ((na >> 1) & 1u) ^ 1u);
+      s_hinfo[sl] = info;
+      mbar_arrive(&s_hfull[sl]);
+      ++na;
+    };
     for (int qi = 0;; ++qi) {
       const int q = qi % kQ;
       mbar_wait(&qfull[q], (qi / kQ) & 1);
       const int uu = unit_q[q];
       named_bar_sync(1, 128);
       if (etid == 0) mbar_arrive(&qempty[q]);
-      if (uu < 0) break;
+      if (uu < 0) {
+        if (h_delegate && swiglu && etid == 0) h_mail(-1);
+        break;
+      }
       const UnitInfo ui = decode(uu, qm, tilesA, tilesB, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
@@ -882,9 +918,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[buf]);
       if (phaseA) {
         named_bar_sync(1, 128);
-        if (etid == 0)  // the barrier orders every epilogue thread's H stores before this
-          for (int tt = 0; tt < ui.nt; ++tt)  // cumulative release
-            atomic_add_release(&h_ready[ui.expert * tilesA + ui.tile + tt], 1);
+        // the barrier orders every epilogue thread's H stores before this
+        if (etid == 0) {
+          if (h_delegate)
+            h_mail((ui.nt << 24) | (ui.expert * tilesA + ui.tile));
+          else
+            for (int tt = 0; tt < ui.nt; ++tt)  // cumulative release
+              red_add_release(&h_ready[ui.expert * tilesA + ui.tile + tt], 1);
+        }
       }
       if (etid == 0) trace_put(tc, 3, uu);
       ++nunit;
