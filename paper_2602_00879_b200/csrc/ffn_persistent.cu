@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // timeline (desmoe_set_trace): tid 0 = prologue + scheduler, 96 = activation
   // producer, 128 = epilogue; atomic-free after the claim here
   TraceCursor tc{nullptr, 0, 0};
-  if (a.trace && (tid == 0 || tid == 96 || tid == 128)) tc = trace_open(a.trace, a.trace_cap, 96);
+  if (a.trace && (tid == 0 || tid == 32 || tid == 96 || tid == 128))
+    tc = trace_open(a.trace, a.trace_cap, 96);
   if (tid == 0) trace_put(tc, 0, -1);
   const bool swiglu = a.mode == 0;
   const bool dense = a.dense != 0;
@@ -240,13 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int b_box_bytes = a.b_rows * 128;
   const int stage_bytes = KB * kATile + KB * b_box_bytes;
 
-  // phase-A H hand-off: the epilogue passes (expert tile, tiles) through a
-  // 2-slot mailbox to warp 2, which does the GPU-scope release of the
-  // readiness flags (a release waits for the SM's outstanding memory
-  // traffic, ~3-4 us behind a full TMA ring: off the epilogue's path)
-  __shared__ uint64_t s_hfull[2], s_hempty[2];
-  __shared__ int s_hinfo[2];
-  const bool h_delegate = !(a.flags & 8);
   // ---- shared-memory carve-up --------------------------------------------
   unsigned char* ring = smem;
   unsigned char* p = ring + static_cast<size_t>(S) * stage_bytes;
@@ -297,10 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&qfull[q], 1);
       mbar_init(&qempty[q], 3);  // MMA lane + activation producer + epilogue
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_hfull[b], 1);
-      mbar_init(&s_hempty[b], 1);
-    }
+
     fence_mbar_init();
   }
   __shared__ uint64_t s_pts[8];  // prologue timeline (trace buffer only)
@@ -726,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = nunit >> 1;
       mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
       tc_fence_after();
+      if (lane == 0) trace_put(tc, 9, uu);  // accumulator free: the unit's MMAs may start
       const uint32_t d_acc = tmem_base + buf * 256u;
       const bool pair = ui.nt == 2;
       const int ksteps = (phaseA ? ksA : ksB) * ui.nt;
@@ -771,6 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
+      if (lane == 0) trace_put(tc, 10, uu);  // the unit's last MMA issued
       ++nunit;
     }
   } else if (warp == 2) {
@@ -804,44 +797,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.stats[2] = sel;
       }
     }
-    if (h_delegate && swiglu) {
-      // phase-A releases, in the epilogue's order (see s_hinfo)
-      for (uint32_t kk = 0;; ++kk) {
-        const int sl = kk & 1;
-        mbar_wait(&s_hfull[sl], (kk >> 1) & 1u);
-        const int info = s_hinfo[sl];
-        if (info < 0) break;
-        if (lane == 0) {
-          __threadfence();  // the epilogue's H stores (observed through the mailbox)
-          for (int tt = 0; tt < (info >> 24); ++tt) red_add_release(&h_ready[(info & 0xFFFFFF) + tt], 1);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_hempty[sl]);
-      }
-    }
+
   } else if (warp >= 4) {
     // ============ epilogue ============
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;  // accumulator row = weight row within the tile
     const int etid = tid - 128;    // 0..127
-    uint32_t nunit = 0, na = 0;
-    auto h_mail = [&](int info) {  // etid 0: hand a phase-A unit (or the end) to warp 2
-      const int sl = na & 1;
-      mbar_wait(&s_hempty[sl], ((na >> 1) & 1u) ^ 1u);
-      s_hinfo[sl] = info;
-      mbar_arrive(&s_hfull[sl]);
-      ++na;
-    };
+    uint32_t nunit = 0;
     for (int qi = 0;; ++qi) {
       const int q = qi % kQ;
       mbar_wait(&qfull[q], (qi / kQ) & 1);
       const int uu = unit_q[q];
       named_bar_sync(1, 128);
       if (etid == 0) mbar_arrive(&qempty[q]);
-      if (uu < 0) {
-        if (h_delegate && swiglu && etid == 0) h_mail(-1);
-        break;
-      }
+      if (uu < 0) break;
       const UnitInfo ui = decode(uu, qm, tilesA, tilesB, t, dense, n_tok);
       const bool phaseA = ui.phase == 0;
       const int n_mma = (ui.count + 15) & ~15;
@@ -849,6 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = nunit >> 1;
       mbar_wait(&tfull[buf], use & 1u);
       tc_fence_after();
+      if (etid == 0) trace_put(tc, 8, uu);  // accumulator ready
       const uint32_t lane_base = tmem_base + buf * 256u + (static_cast<uint32_t>(q4 * 32) << 16);
       if (phaseA) {
         // lanes 0-63: G, lanes 64-127: U of F columns tile*64 + (r mod 64)
@@ -916,16 +886,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (etid == 0) trace_put(tc, 11, uu);  // accumulator drained
       if (phaseA) {
         named_bar_sync(1, 128);
         // the barrier orders every epilogue thread's H stores before this
-        if (etid == 0) {
-          if (h_delegate)
-            h_mail((ui.nt << 24) | (ui.expert * tilesA + ui.tile));
-          else
-            for (int tt = 0; tt < ui.nt; ++tt)  // cumulative release
-              red_add_release(&h_ready[ui.expert * tilesA + ui.tile + tt], 1);
-        }
+        if (etid == 0)
+          for (int tt = 0; tt < ui.nt; ++tt)  // cumulative release
+            red_add_release(&h_ready[ui.expert * tilesA + ui.tile + tt], 1);
       }
       if (etid == 0) trace_put(tc, 3, uu);
       ++nunit;
