@@ -164,6 +164,7 @@ struct desmoe_ctx {
   cudaGraphExec_t gexec = nullptr;
   struct Key {
     const void *ex, *wr, *x;
+    unsigned long long ex_uid;  // experts handle identity (a freed handle's address can be reused)
     int n;
     desmoe_route_cfg cfg;
     float* y;
@@ -195,6 +196,9 @@ struct desmoe_experts {
   // expert parallelism: exchange buffers this rank exposes to its peers, and
   // the peers' buffers as mapped in this process
   int world = 1, rank = 0;
+  // unique per handle and per expert-parallel (re)connection: captured graphs
+  // are keyed on it, not on the handle's address alone
+  unsigned long long uid = 0;
   float* ep_slot = nullptr;                 // [2][max_n*max_k][d] fp32 (parity halves)
   unsigned long long* ep_flag = nullptr;    // arrival counter (peers add to it)
   int* ep_state = nullptr;                  // [0] call seq (EP epoch), [1] combine CTAs done
@@ -218,6 +222,13 @@ struct desmoe_experts {
 namespace desmoe {
 int set_last_error(int code, const std::string& msg) { return fail(code, msg); }
 }  // namespace desmoe
+
+namespace {
+unsigned long long next_uid() {
+  static std::atomic<unsigned long long> n{0};
+  return ++n;
+}
+}  // namespace
 
 extern "C" {
 
@@ -765,6 +776,7 @@ int desmoe_experts_create_ep(desmoe_ctx* c, int kind, int m, int lo, int hi, int
   if (!wg || (kind == DESMOE_FFN_SWIGLU && (!wu || !wd)))
     return fail(DESMOE_EINVAL, "missing expert weights");
   auto* ex = new desmoe_experts();
+  ex->uid = next_uid();
   ex->ctx = c;
   ex->kind = kind;
   ex->m = m;
@@ -1394,7 +1406,8 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
 }
 
 bool same_key(const desmoe_ctx::Key& a, const desmoe_ctx::Key& b) {
-  return a.ex == b.ex && a.wr == b.wr && a.x == b.x && a.n == b.n && a.y == b.y &&
+  return a.ex == b.ex && a.ex_uid == b.ex_uid && a.wr == b.wr && a.x == b.x && a.n == b.n &&
+         a.y == b.y &&
          a.stats == b.stats && a.prof == b.prof && a.ingress == b.ingress &&
          a.cfg.experts == b.cfg.experts &&
          a.cfg.top_k == b.cfg.top_k && a.cfg.activation == b.cfg.activation &&
@@ -1419,7 +1432,7 @@ int layer_graph_launch(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   int rc;
   if (!c->use_graphs)
     return layer_forward_impl(c, ex, w_r, x, n, cfg, y, stats, st, nullptr, true, false, ingress);
-  desmoe_ctx::Key key{ex, w_r, x, n, *cfg, y, stats, c->profiling, ingress};
+  desmoe_ctx::Key key{ex, w_r, x, ex->uid, n, *cfg, y, stats, c->profiling, ingress};
   if (!c->gexec || !same_key(key, c->gkey)) {
     // validate + capture the whole launch sequence on the context's capture
     // stream, then instantiate (or update) the executable graph
@@ -1433,23 +1446,20 @@ int layer_graph_launch(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
       return rc;
     }
     if (ce != cudaSuccess) return fail(DESMOE_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-    bool updated = false;
+    // always a fresh instantiation: cudaGraphExecUpdate accepted a graph
+    // with the same node count but other kernels (in-envelope front path ->
+    // split router/routing path for another shape) and kept the old nodes'
+    // cluster launch attributes — the new routing kernels never wrote the
+    // route (tests/test_gpu_ffn.py::test_recreated_expert_bank_...)
     if (c->gexec) {
-      cudaGraphExecUpdateResultInfo info;
-      updated = cudaGraphExecUpdate(c->gexec, g, &info) == cudaSuccess;
-      if (!updated) {
-        cudaGetLastError();
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
-      }
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
     }
-    if (!updated) {
-      cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
-      if (ie != cudaSuccess) {
-        cudaGraphDestroy(g);
-        c->gexec = nullptr;
-        return fail(DESMOE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
-      }
+    cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
+    if (ie != cudaSuccess) {
+      cudaGraphDestroy(g);
+      c->gexec = nullptr;
+      return fail(DESMOE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
     }
     cudaGraphDestroy(g);
     c->gkey = key;
@@ -1736,6 +1746,7 @@ int desmoe_ep_connect(desmoe_experts* ex, int world, int rank, void* const* peer
     }
   }
   ex->world = world;
+  ex->uid = next_uid();  // graphs captured before this (re)connection are stale
   ex->rank = rank;
   ex->ctx->gkey.ex = nullptr;  // force a re-capture of the layer graph
   return DESMOE_OK;
@@ -1828,6 +1839,7 @@ int desmoe_stack_forward(desmoe_ctx* c, desmoe_experts* const* experts, const vo
   key.reserve(2 * layers + 8);
   for (int l = 0; l < layers; ++l) {
     key.push_back(experts[l]);
+    key.push_back(reinterpret_cast<const void*>(static_cast<uintptr_t>(experts[l]->uid)));
     key.push_back(w_router[l]);
   }
   key.push_back(x);

@@ -92,7 +92,7 @@ def test_moe_forward_facade(ref):
 
 # BASELINE configs: C1 M=64 d=512; C2 M=64 d=2048 F=1024 N=32;
 # C3 M=256 d=2048 F=512 N=8-256; C4 M=128 d=2048 F=768
-BETA = {64: 0.4, 128: 0.3, 256: 0.15}
+BETA = {64: 0.4, 128: 0.3, 256: 0.15, 512: 0.075}
 
 
 @pytest.mark.parametrize("m,d,f,n,strategy", [
@@ -108,6 +108,14 @@ BETA = {64: 0.4, 128: 0.3, 256: 0.15}
     (128, 2048, 768, 32, "vanilla"),  # C4 vanilla
     (128, 512, 768, 256, "vote"),
     (256, 2048, 512, 256, "vote"),    # token-split router GEMM at the C3 shape
+    # outside the front kernel's envelope (M > 256, d not a multiple of 512):
+    # split-K router GEMM + single-CTA routing kernels
+    (512, 1024, 256, 32, "vote"),
+    (512, 1024, 256, 64, "vanilla"),
+    (64, 640, 256, 32, "vote"),
+    (64, 640, 256, 32, "seq"),
+    (64, 640, 256, 32, "vanilla"),
+    (256, 1280, 512, 32, "vanilla"),
 ])
 def test_swiglu_layer_matches_oracle(ref, port, m, d, f, n, strategy):
     swiglu_case(ref, port, m, d, f, n, strategy)
@@ -370,3 +378,28 @@ def test_layer_config_changes_take_effect():
     torch.cuda.synchronize()
     core1 = int(layer.stats[1].item())
     assert core1 < core3, (core1, core3)
+
+
+@pytest.mark.gpu
+def test_recreated_expert_bank_does_not_replay_stale_graph(ref):
+    """Captured layer graphs are keyed on a per-handle id, not the handle's
+    address: a bank destroyed and re-created (the allocator hands back the
+    same address) with other shapes and another strategy must not replay the
+    previous call's graph (seen as U = the previous coreset size)."""
+    import gc
+    for (m, d, f, strat) in [(256, 1536, 512, "vote"), (256, 1280, 512, "vanilla"),
+                             (256, 1536, 512, "vanilla"), (256, 1280, 512, "vote")]:
+        wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1)
+        wr = synth.router_weights(m, d, seed=2)
+        layer = DesMoeLayer(LayerConfig(m, 8, d, f, strategy=strat, vote_beta=0.15), wr, wg, wu, wd)
+        x = synth.hidden_states(32, d, seed=5, rho=0.3)
+        for _ in range(2):
+            layer.forward(x)
+        torch.cuda.synchronize()
+        lg = layer.last_logits(32).double().cpu().numpy()
+        r = ref.topk_route(lg, 8) if strat == "vanilla" else ref.des_run(lg, 8, "vote", beta=0.15)[1]
+        u, total, _ = ref.moe_latency(r, m)
+        st = layer.stats.cpu().tolist()
+        assert st[0] == u and st[2] == total, (m, d, strat, st, u, total)
+        del layer, wg, wu, wd
+        gc.collect()
