@@ -1239,7 +1239,11 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   *used = false;
   const int m = cfg->experts, k = cfg->top_k, d = ex->d;
   if (std::getenv("DESMOE_NO_FRONT")) return DESMOE_OK;
-  if (n > 256 || m > 256 || (d / kBK) % kFrontCta != 0 || d % kBK) return DESMOE_OK;
+  // pools of 257-512 experts: only in the logits-in mode (router kernel ahead)
+  if (n > 256 || m > 512 || (d / kBK) % kFrontCta != 0 || d % kBK) return DESMOE_OK;
+  if (m > 256 && ((d / kBK) / kFrontCta > 8 || std::getenv("DESMOE_FRONT_ROUTER") ||
+                  std::getenv("DESMOE_FRONT_TSPLIT")))
+    return DESMOE_OK;
   if (cfg->strategy == DESMOE_VANILLA) {
     if (k < 1 || k > m) return fail(DESMOE_EINVAL, "top_k out of range");
   } else {
@@ -1405,6 +1409,16 @@ int layer_forward_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
   return DESMOE_OK;
 }
 
+// Same launch sequence (kernels, grids, cluster shapes): only the buffers
+// may differ, so an instantiated graph can be updated in place.
+bool same_shape(const desmoe_ctx::Key& a, const desmoe_ctx::Key& b) {
+  return a.ex == b.ex && a.ex_uid == b.ex_uid && a.n == b.n && a.prof == b.prof &&
+         a.ingress == b.ingress && a.cfg.experts == b.cfg.experts &&
+         a.cfg.top_k == b.cfg.top_k && a.cfg.activation == b.cfg.activation &&
+         a.cfg.strategy == b.cfg.strategy && a.cfg.seq_k == b.cfg.seq_k &&
+         a.cfg.vote_beta == b.cfg.vote_beta && a.cfg.vote_source == b.cfg.vote_source;
+}
+
 bool same_key(const desmoe_ctx::Key& a, const desmoe_ctx::Key& b) {
   return a.ex == b.ex && a.ex_uid == b.ex_uid && a.wr == b.wr && a.x == b.x && a.n == b.n &&
          a.y == b.y &&
@@ -1446,20 +1460,29 @@ int layer_graph_launch(desmoe_ctx* c, const desmoe_experts* ex, const void* w_r,
       return rc;
     }
     if (ce != cudaSuccess) return fail(DESMOE_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-    // always a fresh instantiation: cudaGraphExecUpdate accepted a graph
-    // with the same node count but other kernels (in-envelope front path ->
-    // split router/routing path for another shape) and kept the old nodes'
-    // cluster launch attributes — the new routing kernels never wrote the
-    // route (tests/test_gpu_ffn.py::test_recreated_expert_bank_...)
-    if (c->gexec) {
-      cudaGraphExecDestroy(c->gexec);
-      c->gexec = nullptr;
+    // In-place update only when the launch sequence is the same (new
+    // buffers, same shapes / strategy / bank): cudaGraphExecUpdate accepted a
+    // graph with the same node count but other kernels (in-envelope front
+    // path -> split router/routing path for another shape) and kept the old
+    // nodes' cluster launch attributes — the new routing kernels never wrote
+    // the route (tests/test_gpu_ffn.py::test_recreated_expert_bank_...).
+    bool updated = false;
+    if (c->gexec && same_shape(key, c->gkey)) {
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(c->gexec, g, &info) == cudaSuccess;
+      if (!updated) cudaGetLastError();
     }
-    cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
-    if (ie != cudaSuccess) {
-      cudaGraphDestroy(g);
-      c->gexec = nullptr;
-      return fail(DESMOE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    if (!updated) {
+      if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+      cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
+      if (ie != cudaSuccess) {
+        cudaGraphDestroy(g);
+        c->gexec = nullptr;
+        return fail(DESMOE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+      }
     }
     cudaGraphDestroy(g);
     c->gkey = key;

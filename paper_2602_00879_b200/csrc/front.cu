@@ -164,29 +164,38 @@ __device__ __noinline__ double f_div(double a, double b) { return a / b; }
 
 // ---------------------------------------------------------------------------
 // Warp selection: the first `rounds` entries of (logit desc, index asc) order
-// among i < m (m <= 256) allowed by `allow` (nullptr = all). Every
+// among i < m (m <= 512) allowed by `allow` (nullptr = all). Every
 // activation is monotone in the logit, so the logit order is the order of
 // the reference's gate values except where rounding makes gates tie — the
 // caller's boundary check (risky_boundary) sends those to the exact path.
 // One 32-bit key per candidate: the order key of the fp32 logit with its 8
-// low bits replaced by (255 - index), so ONE REDUX per round picks (logit
-// desc, index asc) — exact unless two logits agree in their top 24 key bits,
-// which the boundary check also catches. P keys per lane (m <= 32 P).
+// low bits replaced by (255 - index) (9 bits, 511 - index, for pools of
+// 257-512), so ONE REDUX per round picks (logit desc, index asc) — exact
+// unless two logits agree in their top 24 (23) key bits, which the boundary
+// check also catches. P keys per lane (m <= 32 P).
 // sel[r] (shared) = index, or -1 once the candidates run out.
 // ---------------------------------------------------------------------------
 __device__ inline uint32_t sel_key(float x, int i) {
   return (fkey(x) & 0xFFFFFF00u) | static_cast<uint32_t>(255 - i);
+}
+// pools of 257-512 experts (logits-in front): 9 index bits, 23 key bits
+__device__ inline int key_ibits(int m) { return m > 256 ? 9 : 8; }
+__device__ inline uint32_t sel_key_b(float x, int i, int ib) {
+  const uint32_t lo = (1u << ib) - 1u;
+  return (fkey(x) & ~lo) | (lo - static_cast<uint32_t>(i));
 }
 
 template <int P>
 __device__ __noinline__ void warp_rank_select_p(const float* x, int m, int rounds,
                                                 const uint8_t* allow, int* sel) {
   const int lane = threadIdx.x & 31;
+  const int ib = P > 8 ? 9 : 8;  // index bits of the key (m <= 32 P)
+  const uint32_t lo = (1u << ib) - 1u;
   uint32_t k[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) {
     const int i = lane + 32 * s;
-    k[s] = (i < m && (!allow || allow[i])) ? sel_key(x[i], i) : 0u;
+    k[s] = (i < m && (!allow || allow[i])) ? sel_key_b(x[i], i, ib) : 0u;
   }
 #pragma unroll 1
   for (int r = 0; r < rounds; ++r) {
@@ -194,7 +203,7 @@ __device__ __noinline__ void warp_rank_select_p(const float* x, int m, int round
 #pragma unroll
     for (int s = 1; s < P; ++s) best = k[s] > best ? k[s] : best;
     const uint32_t win = __reduce_max_sync(0xffffffffu, best);
-    if (lane == 0) sel[r] = win ? 255 - static_cast<int>(win & 0xFFu) : -1;
+    if (lane == 0) sel[r] = win ? static_cast<int>(lo - (win & lo)) : -1;
 #pragma unroll
     for (int s = 0; s < P; ++s) k[s] = k[s] == win ? 0u : k[s];
   }
@@ -207,8 +216,10 @@ __device__ inline void warp_rank_select(const float* x, int m, int rounds, const
     warp_rank_select_p<2>(x, m, rounds, allow, sel);
   else if (m <= 128)
     warp_rank_select_p<4>(x, m, rounds, allow, sel);
-  else
+  else if (m <= 256)
     warp_rank_select_p<8>(x, m, rounds, allow, sel);
+  else
+    warp_rank_select_p<16>(x, m, rounds, allow, sel);
 }
 
 // Writes a token's route from a rank-ordered selection: experts ascending,
@@ -267,9 +278,10 @@ __device__ inline bool fp64_risky(const float* x, const double* e, int act, cons
 // ... or, for the fast selection's keys, equal truncated keys (index-ordered
 // by the fast path).
 __device__ inline bool risky_boundary(const float* x, const double* e, int act, const int* sel,
-                                      int b) {
+                                      int b, int m) {
   const int hi = sel[b - 1], lo = sel[b];
-  if ((sel_key(x[hi], hi) >> 8) == (sel_key(x[lo], lo) >> 8)) return true;
+  // (the fast keys keep the top 32 - key_ibits(m) bits of the fp32 order key)
+  if (((fkey(x[hi]) ^ fkey(x[lo])) >> key_ibits(m)) == 0) return true;
   return fp64_risky(x, e, act, sel, b);
 }
 
@@ -279,9 +291,9 @@ __device__ inline bool risky_boundary(const float* x, const double* e, int act, 
 __device__ __noinline__ void warp_rank_select_exact32(const float* x, int m, int rounds,
                                                       const uint8_t* allow, int* sel) {
   const int lane = threadIdx.x & 31;
-  uint32_t k[8];
+  uint32_t k[16];  // m <= 512
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < 16; ++s) {
     const int i = lane + 32 * s;
     k[s] = (i < m && (!allow || allow[i])) ? fkey(x[i]) : 0u;  // fkey > 0 for every float
   }
@@ -289,16 +301,16 @@ __device__ __noinline__ void warp_rank_select_exact32(const float* x, int m, int
   for (int r = 0; r < rounds; ++r) {
     uint32_t best = k[0];
 #pragma unroll
-    for (int s = 1; s < 8; ++s) best = k[s] > best ? k[s] : best;
+    for (int s = 1; s < 16; ++s) best = k[s] > best ? k[s] : best;
     const uint32_t win = __reduce_max_sync(0xffffffffu, best);
     uint32_t idx = 0xffffffffu;
 #pragma unroll
-    for (int s = 7; s >= 0; --s)
+    for (int s = 15; s >= 0; --s)
       if (win && k[s] == win) idx = static_cast<uint32_t>(lane + 32 * s);
     const uint32_t wi = __reduce_min_sync(0xffffffffu, idx);
     if (lane == 0) sel[r] = win ? static_cast<int>(wi) : -1;
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
+    for (int s = 0; s < 16; ++s)
       if (win && static_cast<uint32_t>(lane + 32 * s) == wi) k[s] = 0u;
   }
   __syncwarp();
@@ -316,7 +328,7 @@ __device__ __noinline__ void exact_reselect(const double* e, double s, int act, 
 }
 
 // A boundary the fast selection could not order (risky_boundary): re-select
-// on exact fp32 logit keys first (m <= 256); only a boundary that is still
+// on exact fp32 logit keys first (m <= 512); only a boundary that is still
 // ambiguous on the fp64 gates (equal logits, gap <= 2^-40, underflow) pays
 // for the full fp64 re-selection (measured ~13 us for one token at M = 256,
 // where the fp32 re-selection costs ~1 us). `b2` < want: a second boundary
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kMaxStages = 12;  // ring stages (the token-split GEMM runs deep rings)
   __shared__ uint64_t bars[2 * kMaxStages + 4];  // full[], empty[], tdone, recv, selx, mask
-  __shared__ uint32_t s_mask[kFrontCta];         // coreset slices (distributed rank)
+  __shared__ uint64_t s_mask[kFrontCta];         // coreset slices (distributed rank)
   __shared__ uint32_t s_tag;                     // this call's hand-off tag
   __shared__ uint32_t tmem_slot[2];
   __shared__ int s_bad, s_nm;
@@ -601,7 +613,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     mbar_init(bar_selx, 1);
     mbar_init(bar_mask, 1);
     fence_mbar_init();
-    if (dist_rank) mbar_arrive_expect_tx(bar_mask, static_cast<uint32_t>(C * 4));
+    if (dist_rank) mbar_arrive_expect_tx(bar_mask, static_cast<uint32_t>(C * 8));
     s_bad = 0;
     // arm: chunk 0's partials for this CTA's own tokens from all C senders,
     // and (DES) every token's top-`depth` selection
@@ -980,8 +992,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           const int* sj = sel + j * 33;
           const float* xr = xrow + j * m;
           const double* er = erow + j * ew;
-          bool r = want < m && risky_boundary(xr, er, act, sj, want);
-          if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
+          bool r = want < m && risky_boundary(xr, er, act, sj, want, m);
+          if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth, m);
           risky[j] = r;
         }
       }
@@ -1101,8 +1113,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           s_ts[36] = gtime();
         }
         if (lane == 0) {
-          bool r = want < m && risky_boundary(xr, er, act, sj, want);
-          if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth);
+          bool r = want < m && risky_boundary(xr, er, act, sj, want, m);
+          if (!vanilla && depth < want) r |= risky_boundary(xr, er, act, sj, depth, m);
           risky[j] = r;
         }
         if (tracing && warp == 0 && lane == 0 && j == 0) s_ts[37] = gtime();
@@ -1313,20 +1325,24 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
         flag[tid] = static_cast<uint8_t>(r < a.m_core);
       }
     } else {
-      // this CTA's slice -> one membership word pushed to every CTA (ms <= 32)
+      // this CTA's slice -> one 64-bit membership word pushed to every CTA
+      // (ms <= 64: pools of up to 512 experts)
       if (warp == 0) {
-        int r = 0;
-        if (lane < me) {
+        int r0 = 0, r1 = 0;
 #pragma unroll 1
-          for (int q = 0; q < parts; ++q) r += rankp[q * ms + lane];
+        for (int q = 0; q < parts; ++q) {
+          if (lane < me) r0 += rankp[q * ms + lane];
+          if (lane + 32 < me) r1 += rankp[q * ms + lane + 32];
         }
-        const uint32_t word = __ballot_sync(0xffffffffu, lane < me && r < a.m_core);
+        const uint32_t w0 = __ballot_sync(0xffffffffu, lane < me && r0 < a.m_core);
+        const uint32_t w1 = __ballot_sync(0xffffffffu, lane + 32 < me && r1 < a.m_core);
+        const uint64_t word = (static_cast<uint64_t>(w1) << 32) | w0;
         if (lane < C)
-          st_async_b32(mapa_u32(smem_u32(s_mask + rk), lane), word,
+          st_async_b64(mapa_u32(smem_u32(s_mask + rk), lane), word,
                        mapa_u32(smem_u32(bar_mask), lane));
       }
       mbar_wait_cluster(bar_mask, 0);
-      if (tid < m) flag[tid] = static_cast<uint8_t>((s_mask[tid / ms] >> (tid % ms)) & 1u);
+      if (tid < m) flag[tid] = static_cast<uint8_t>((s_mask[tid / ms] >> (tid % ms)) & 1ull);
     }
   }
   const int nm = __syncthreads_count(tid < m && flag[tid]);  // m <= 256 < kFrontThreads
@@ -1359,7 +1375,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
       if (!covered) {
         const int rounds = cnt < nm ? cnt + 1 : cnt;
         warp_rank_select(xr, m, rounds, flag, wsel);  // rank order
-        r = cnt < nm && risky_boundary(xr, er, act, wsel, cnt);
+        r = cnt < nm && risky_boundary(xr, er, act, wsel, cnt, m);
         if (r) fix_boundary(xr, er, s, act, m, cnt, 0, flag, scratch, wsel);  // rare
       }
       write_route(er, s, act, wsel, cnt, k, own_tok[j], wp, a.route_idx, a.route_gate,
@@ -1552,7 +1568,9 @@ cudaError_t launch_router_cluster(const CUtensorMap& wr_map, const BoxMaps& x_ma
 // Host plan: token chunk, pipeline depth, shared memory. Returns false when
 // the shape is outside the kernel's envelope.
 bool front_plan(int n, int m, int k, int d, FrontArgs* a, size_t* smem, int tsplit) {
-  if (n < 1 || n > 256 || m < 1 || m > 256 || k < 1 || k > 32 || k > m) return false;
+  // pools of 257-512 experts only with the router GEMM ahead (logits in)
+  if (n < 1 || n > 256 || m < 1 || m > (tsplit == 3 ? 512 : 256) || k < 1 || k > 32 || k > m)
+    return false;
   if (tsplit == 3) {
     // logits in (router_cluster_kernel): no ring, no partial exchange
     const int own_max = (n + kFrontCta - 1) / kFrontCta;

@@ -38,7 +38,7 @@ _PROBE = {}
 
 def probe(d):
     if d not in _PROBE:
-        _PROBE[d] = LayerProbe(max_n=256, max_m=256, max_k=16, d=d)
+        _PROBE[d] = LayerProbe(max_n=256, max_m=512, max_k=16, d=d)
     return _PROBE[d]
 
 
@@ -156,7 +156,7 @@ def constructed_vote_tie(n, m, k, m_core, seed):
 # ---- cases ------------------------------------------------------------------------
 
 SHAPES = [(8, 64, 8), (32, 64, 8), (64, 128, 8), (32, 256, 8), (160, 128, 8), (256, 256, 8),
-          (29, 40, 6)]
+          (29, 40, 6), (32, 512, 8), (96, 384, 8)]
 
 
 @pytest.mark.parametrize("n,m,k", SHAPES)
@@ -247,9 +247,10 @@ def test_ties_every_gemm_variant(ref, monkeypatch, variant):
 
 
 def criterion6_instances(ref, count=1000):
-    """acceptance.cpp:207-230's generator (Rng(61000 + i) draws m, n, k, the
-    activation and the budget; random_block(n, m, 62000 + i, 1.5) logits,
-    quantised to fp32), with the pool capped at the front kernel's M <= 256."""
+    """acceptance.cpp:207-230's generator, exactly (Rng(61000 + i) draws m in
+    2..512, n, k, the activation and the budget; random_block(n, m, 62000 + i,
+    1.5) logits, quantised to fp32). Pools above 256 run the router kernel +
+    the front's logits-in mode."""
     for i in range(count):
         u = synth.u64_stream(61000 + i, 64)
         draws = iter(int(v) for v in u)
@@ -262,7 +263,7 @@ def criterion6_instances(ref, count=1000):
                 if x >= threshold:
                     return x % b
 
-        m = 2 + below(255)
+        m = 2 + below(511)
         n = 1 + below(64)
         k = 1 + below(min(m, 16))
         act = 1 if below(4) == 0 else 0

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 
 CASES = [  # m, d, f, n, beta
     (256, 2048, 512, 32, 0.15),   # C3, in the envelope (router kernel + front)
-    (512, 2048, 512, 32, 0.075),  # M > 256: split path
+    (512, 2048, 512, 32, 0.075),  # M = 512: router kernel + logits-in front
     (512, 2048, 512, 64, 0.075),
     (256, 1536, 512, 32, 0.15),   # d = 3 x 512: in the envelope
     (256, 1280, 512, 32, 0.15),   # d not a multiple of 512: split path
@@ -33,7 +33,7 @@ def main():
         wg, wu, wd = synth.swiglu_weights(m, d, f, seed=1)
         wr = synth.router_weights(m, d, seed=2)
         row = {"m": m, "d": d, "f": f, "n": n, "beta": beta,
-               "front_envelope": bool(m <= 256 and n <= 256 and d % 512 == 0)}
+               "front_envelope": bool(m <= 512 and n <= 256 and d % 512 == 0)}
         for strat in ("vanilla", "vote"):
             layer = DesMoeLayer(LayerConfig(m, 8, d, f, strategy=strat, vote_beta=beta), wr, wg, wu, wd)
             xs = [synth.hidden_states(n, d, seed=100 + i, rho=0.3) for i in range(23)]
