@@ -1239,10 +1239,11 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   *used = false;
   const int m = cfg->experts, k = cfg->top_k, d = ex->d;
   if (std::getenv("DESMOE_NO_FRONT")) return DESMOE_OK;
-  // pools of 257-512 experts: only in the logits-in mode (router kernel ahead)
-  if (n > 256 || m > 512 || (d / kBK) % kFrontCta != 0 || d % kBK) return DESMOE_OK;
-  if (m > 256 && ((d / kBK) / kFrontCta > 8 || std::getenv("DESMOE_FRONT_ROUTER") ||
-                  std::getenv("DESMOE_FRONT_TSPLIT")))
+  // pools of 257-512 experts, and hidden sizes that are not a multiple of
+  // 8 x 64: only in the logits-in mode (router kernel ahead, uneven K split)
+  if (n > 256 || m > 512 || d % kBK || (d / kBK + kFrontCta - 1) / kFrontCta > 8) return DESMOE_OK;
+  const bool lin_only = m > 256 || (d / kBK) % kFrontCta != 0;
+  if (lin_only && (std::getenv("DESMOE_FRONT_ROUTER") || std::getenv("DESMOE_FRONT_TSPLIT")))
     return DESMOE_OK;
   if (cfg->strategy == DESMOE_VANILLA) {
     if (k < 1 || k > m) return fail(DESMOE_EINVAL, "top_k out of range");
@@ -1264,7 +1265,7 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   // the front reads the logits (DESMOE_FRONT_ROUTER=0/1 overrides)
   bool router = n > kRouterTc || m > 128;
   if (const char* rv = std::getenv("DESMOE_FRONT_ROUTER")) router = std::atoi(rv) != 0;
-  if (router && (d / kBK) / kFrontCta <= 8) tsplit = 3;
+  if ((router || lin_only) && (d / kBK + kFrontCta - 1) / kFrontCta <= 8) tsplit = 3;
   if (const char* ts = std::getenv("DESMOE_FRONT_TSPLIT")) tsplit = std::atoi(ts);
   if (!front_plan(n, m, k, d, &a, &smem, tsplit) && !front_plan(n, m, k, d, &a, &smem, 0))
     return DESMOE_OK;
@@ -1314,7 +1315,7 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
     ra.d = d;
     ra.tc = kRouterTc;
     ra.mtiles = (m + kBM - 1) / kBM;
-    ra.kb_cta = (d / kBK) / kFrontCta;
+    ra.kb_cta = (d / kBK + kFrontCta - 1) / kFrontCta;  // most K blocks of a CTA (smem)
     ra.b_rows = b_rows_for(n < kRouterTc ? n : kRouterTc);
     int bi = 0;
     while ((16 << bi) < ra.b_rows) ++bi;

@@ -1437,12 +1437,17 @@ __global__ void __launch_bounds__(256, 1)
   const int nt = a.n - t0 < a.tc ? a.n - t0 : a.tc;  // tokens of this cluster
   const int e0 = mtile * kBM;
   const int me = a.m - e0 < kBM ? a.m - e0 : kBM;     // experts of this tile
-  const int kb = a.kb_cta, kb0 = rk * kb;
+  // K blocks of this CTA: an even split of d / 64 over the cluster (any
+  // hidden size that is a multiple of 64; a CTA may get none)
+  const int kbt = a.d / kBK;
+  const int kb0 = (kbt * rk) / C, kb = (kbt * (rk + 1)) / C - kb0;
   const int ocm = (a.tc + C - 1) / C;                 // owner rows per sender
   const uint32_t xbytes = static_cast<uint32_t>(a.b_rows) * 128u;
   const int stage_bytes = kATile + a.b_rows * 128;
   unsigned char* ring = smem;                                                   // [kb][W tile | X box]
-  float* stage = reinterpret_cast<float*>(smem + static_cast<size_t>(kb) * stage_bytes);  // [tc][128]
+  // (laid out for the largest K share, a.kb_cta: every CTA's stage / recv at
+  // the same offset, since peers address them through mapa)
+  float* stage = reinterpret_cast<float*>(smem + static_cast<size_t>(a.kb_cta) * stage_bytes);  // [tc][128]
   float* recv = stage + a.tc * kBM;                                             // [C][ocm][128]
   uint64_t* full = bars;
   uint64_t* tdone = bars + 8;
@@ -1480,7 +1485,7 @@ __global__ void __launch_bounds__(256, 1)
   cluster_arrive_relaxed();
   cluster_wait();
   const int n_mma = (nt + 15) & ~15;
-  if (warp == 1) {
+  if (warp == 1 && kb > 0) {
     const uint32_t idesc = idesc_bf16_f32(kBM, n_mma);
     for (int i = 0; i < kb; ++i) {
       mbar_wait(&full[i], 0);
@@ -1497,18 +1502,22 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {
-    // drain: partial[token][expert] of this CTA's K slice
-    mbar_wait(tdone, 0);
-    tc_fence_after();
+    // drain: partial[token][expert] of this CTA's K slice (zeros without one)
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    const uint32_t lb = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    for (int cc = 0; cc < n_mma; cc += 16) {
-      float v[16];
-      tmem_ld16(lb + cc, v);
+    if (kb > 0) {
+      mbar_wait(tdone, 0);
+      tc_fence_after();
+      const uint32_t lb = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+      for (int cc = 0; cc < n_mma; cc += 16) {
+        float v[16];
+        tmem_ld16(lb + cc, v);
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (cc + j < nt) stage[(cc + j) * kBM + r] = v[j];
+        for (int j = 0; j < 16; ++j)
+          if (cc + j < nt) stage[(cc + j) * kBM + r] = v[j];
+      }
+    } else {
+      for (int t = 0; t < nt; ++t) stage[t * kBM + r] = 0.0f;
     }
     tc_fence_before();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -285,3 +285,14 @@ def test_criterion6_through_layer(ref):
             check_case(ref, L, k, "vanilla", act=act, d=512)
         done += 1
     assert done == 1000
+
+
+@pytest.mark.parametrize("d", [384, 640, 1664])
+@pytest.mark.parametrize("strategy", ["vanilla", "seq", "vote"])
+def test_ties_uneven_router_split(ref, d, strategy):
+    """Hidden sizes that are not a multiple of 8 x 64: the router kernel splits
+    the K blocks unevenly over its cluster (384: two CTAs get none) and the
+    front reads the logits — injected exactly, routed exactly."""
+    n, m = 64, 128
+    check_case(ref, tied_levels(n, m, 11), 8, strategy, seq_k=2, beta=0.3, d=d)
+    check_case(ref, near_ties(n, m, 12), 8, strategy, seq_k=3, beta=0.25, d=d)
