@@ -24,5 +24,9 @@ for w in $WHAT; do
            echo "stack rc=$?" ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_${TAG}.log 2>&1
            echo "smoke rc=$?" ;;
+    envelope) timeout 600 python tools/envelope_probe.py > $OUT/envelope_${TAG}.json 2> $OUT/envelope_${TAG}.err
+           echo "envelope rc=$?" ;;
+    ref)   timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_${TAG}.json 2> $OUT/bench_ref_${TAG}.err
+           echo "ref rc=$?" ;;
   esac
 done
