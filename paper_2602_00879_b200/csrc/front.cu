@@ -1270,7 +1270,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     }
     __syncthreads();  // list reads done before votes / keys reuse the region
   } else {
-    // DES-Seq: the union of every token's top-seq_k
+    // DES-Seq: the union of every token's top-seq_k. (The barrier orders the
+    // zeroing above before any thread's set: without it a late zero could
+    // erase another thread's member — a rare wrong coreset / re-route, ~1 in
+    // 1500 calls of one criterion-6 instance.)
+    __syncthreads();
 #pragma unroll 1
     for (int w = tid; w < n * depth; w += kFrontThreads) {
       const int t = w / depth, j = w - t * depth;
