@@ -138,58 +138,6 @@ __device__ inline int box_for(int count) {
 
 __device__ inline float silu(float g) { return g / (1.0f + expf(-g)); }
 
-// Epilogue bodies, out of line so a dry pass at CTA start (no tokens: no
-// stores) brings their code into the SM's instruction caches while HBM is
-// still idle. Run cold in the middle of the weight stream, each missing
-// instruction line waited behind the SM's in-flight TMA data: a CTA's first
-// phase-A epilogue took ~10-13 us (its first H chunk ~10 us, later ~1.8 us).
-// Phase A: lanes 0-63 hold G, 64-127 U of F columns tile*64 + (r mod 64);
-// H = bf16(silu(G) * U) for `count` tokens. hbase = h_perm row block + tile.
-__device__ __noinline__ void epi_phase_a(uint32_t lane_base, int nt, int n_mma, int count,
-                                         __nv_bfloat16* hbase, int f, float* xchg, int r) {
-  const bool is_g = r < kHalf;
-  const int rr = r & (kHalf - 1);
-  for (int tt = 0; tt < nt; ++tt) {
-    __nv_bfloat16* hrow = hbase + tt * kHalf + rr;
-    for (int c0 = 0; c0 < n_mma; c0 += 16) {
-      float v[16];
-      tmem_ld16(lane_base + tt * 128u + c0, v);
-      if (!is_g) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) xchg[j * kHalf + rr] = v[j];
-      }
-      named_bar_sync(1, 128);
-      if (is_g) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = c0 + j;
-          if (col < count)
-            hrow[static_cast<size_t>(col) * f] = __float2bfloat16_rn(silu(v[j]) * xchg[j * kHalf + rr]);
-        }
-      }
-      named_bar_sync(1, 128);
-    }
-  }
-}
-
-// Phase B (one GPU): Y rows of `count` slots, raw (dense) or gate-scaled.
-// ybase = y_slot row block + tile * 128 + r.
-__device__ __noinline__ void epi_phase_b(uint32_t lane_base, int nt, int n_mma, int count,
-                                         float* ybase, int d, bool dense, const float* gate) {
-  for (int tt = 0; tt < nt; ++tt) {
-    float* yrow = ybase + tt * kBM;
-    for (int c0 = 0; c0 < n_mma; c0 += 16) {
-      float v[16];
-      tmem_ld16(lane_base + tt * 128u + c0, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = c0 + j;
-        if (col < count) yrow[static_cast<size_t>(col) * d] = dense ? v[j] : v[j] * gate[col];
-      }
-    }
-  }
-}
-
 // Block-wide exclusive scan of v[0..n) (n <= 4 * kThreads) in place; returns total.
 __device__ int block_exclusive_scan(int* v, int n, int* warp_sums) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -350,22 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (a.trace && tid < 8) s_pts[tid] = 0;
   __shared__ int s_upub;         // early mode: owned published experts
   __shared__ int s_pcnt;         // early mode: published list length
-  if (warp == 2) {
-    tmem_alloc(tmem_slot, 512);
-    tc_fence_before();
-    named_bar_arrive(6, 160);  // the TMEM address for the epilogue warps' dry pass
-  }
-  if (warp >= 4) {
-    named_bar_sync(6, 160);
-    tc_fence_after();
-    if (!(a.flags & 32)) {  // dry pass (DESMOE_FFN_FLAGS=32 skips it)
-      const uint32_t tb = *tmem_slot + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-      const int r = (warp & 3) * 32 + lane;
-      if (swiglu) epi_phase_a(tb, 1, 16, 0, a.h_perm, f, xchg, r);
-      if (a.world <= 1) epi_phase_b(tb, 1, 16, 0, a.y_slot, d, dense, t.slot_gate);
-      tc_fence_before();
-    }
-  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
   pdl_launch_dependents();  // the combine kernel may launch; it waits for us
   // standalone: route + zeroed counters from the previous kernel. Behind the
   // front kernel (early mode) nothing waits for its completion: the expert
@@ -888,12 +821,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (etid == 0) trace_put(tc, 8, uu);  // accumulator ready
       const uint32_t lane_base = tmem_base + buf * 256u + (static_cast<uint32_t>(q4 * 32) << 16);
       if (phaseA) {
-        epi_phase_a(lane_base, ui.nt, n_mma, ui.count,
-                    a.h_perm + static_cast<size_t>(ui.brow) * f + ui.tile * kHalf, f, xchg, r);
+        // lanes 0-63: G, lanes 64-127: U of F columns tile*64 + (r mod 64)
+        const bool is_g = r < kHalf;
+        const int rr = r & (kHalf - 1);
+        for (int tt = 0; tt < ui.nt; ++tt) {
+        __nv_bfloat16* hrow =
+            a.h_perm + static_cast<size_t>(ui.brow) * f + (ui.tile + tt) * kHalf + rr;
+        for (int c0 = 0; c0 < n_mma; c0 += 16) {
+          float v[16];
+          tmem_ld16(lane_base + tt * 128u + c0, v);
+          if (!is_g) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xchg[j * kHalf + rr] = v[j];
+          }
+          named_bar_sync(1, 128);
+          if (is_g) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = c0 + j;
+              if (col < ui.count)
+                hrow[static_cast<size_t>(col) * f] =
+                    __float2bfloat16_rn(silu(v[j]) * xchg[j * kHalf + rr]);
+            }
+          }
+          named_bar_sync(1, 128);
+        }
+        }  // tiles of the unit
       } else if (a.world <= 1) {
-        epi_phase_b(lane_base, ui.nt, n_mma, ui.count,
-                    a.y_slot + static_cast<size_t>(ui.brow) * d + ui.tile * kBM + r, d, dense,
-                    t.slot_gate + ui.brow);
+        for (int tt = 0; tt < ui.nt; ++tt) {
+        float* yrow = a.y_slot + static_cast<size_t>(ui.brow) * d + (ui.tile + tt) * kBM + r;
+        for (int c0 = 0; c0 < n_mma; c0 += 16) {
+          float v[16];
+          tmem_ld16(lane_base + tt * 128u + c0, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = c0 + j;
+            if (col < ui.count)
+              yrow[static_cast<size_t>(col) * d] =
+                  dense ? v[j] : v[j] * t.slot_gate[ui.brow + col];
+          }
+        }
+        }  // tiles of the unit
       } else {
         // expert parallel: push the gate-scaled rows straight into every
         // rank's slot buffer (own + NVLink peers) while later tiles stream
