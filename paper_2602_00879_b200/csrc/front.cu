@@ -659,6 +659,37 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_exptab + 2 * tid)),
                  "l"(kExpTab + 2 * tid)
                  : "memory");
+  // instruction-cache prewarm: the layer's FFN streams hundreds of MB
+  // between two calls, so this kernel's code comes back from far memory and
+  // every new code region costs a miss chain (~2 µs measured at the top-K
+  // entry). Four idle warps each run one later phase's code once on scratch
+  // (s_pw; 32 dummy experts), in parallel so the misses overlap: during the
+  // router GEMM, or in logits-in mode before griddepcontrol.wait, while
+  // router_cluster_kernel still runs (DESMOE_FRONT_FLAGS=1 disables)
+  auto prewarm = [&]() {
+    uint8_t* df = reinterpret_cast<uint8_t*>(s_pw + 48);      // [32] flags; pub words at +52
+    int* ds = wsel_all + warp * 33;
+    if (warp == 8) {
+      warp_rank_select(reinterpret_cast<const float*>(erow), m, k < m ? k + 1 : k, nullptr, ds);
+    } else if (warp == 9) {
+      if (lane == 0) {
+        // (the global table: the shared copy may still be in flight here)
+        volatile double sink = f_exp(-1.5, kExpTab) + f_div(1.0, 2.0);
+        (void)sink;
+      }
+    } else if (warp == 10) {
+      df[lane] = static_cast<uint8_t>(lane & 1);
+      __syncwarp();
+      publish_list(df, 32, 0u, reinterpret_cast<uint32_t*>(s_pw + 52), nullptr, nullptr);
+    } else {
+      write_route(erow, 1.0, 2, ds, 0, 0, 0, reinterpret_cast<double*>(s_pw + 64), nullptr,
+                  nullptr, ds, nullptr, 0u);
+    }
+    // (The exact near-tie path is not prewarmed: a fifth prewarm warp running
+    // it cost the coreset 2-2.7 us at C2/C3 N = 32 — that warp joins the
+    // activation late — more than its rare cold misses.)
+  };
+  if (kLin && !(a.flags & 1) && warp >= 8 && warp < 12) prewarm();
   pdl_wait();  // x (the previous kernel's output) is complete from here on
   // the expert-FFN kernel may launch now — not earlier: it reads the call
   // sequence word the previous call's combine advances, and that combine
@@ -694,36 +725,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
   // from shared memory after the GEMM's barrier (loaded by every thread at
   // this point, it stalled all 16 warps, the MMA issuer included, ~1 us)
   if (tid == 96) s_tag = a.seq ? hand_tag(*a.seq) : 0u;
-  // (logits-in mode has no GEMM to hide the prewarm behind: skipped)
-  if (!kLin && !(a.flags & 1) && warp >= 8 && warp < 12) {
-    // instruction-cache prewarm: the layer's FFN streams hundreds of MB
-    // between two calls, so this kernel's code comes back from far memory and
-    // every new code region costs a miss chain (~2 µs measured at the top-K
-    // entry). While the router GEMM runs, four idle warps each run one later
-    // phase's code once on scratch (s_pw; 32 dummy experts), in parallel so
-    // the misses overlap (DESMOE_FRONT_FLAGS=1 disables)
-    uint8_t* df = reinterpret_cast<uint8_t*>(s_pw + 48);      // [32] flags; pub words at +52
-    int* ds = wsel_all + warp * 33;
-    if (warp == 8) {
-      warp_rank_select(reinterpret_cast<const float*>(erow), m, k < m ? k + 1 : k, nullptr, ds);
-    } else if (warp == 9) {
-      if (lane == 0) {
-        // (the global table: the shared copy may still be in flight here)
-        volatile double sink = f_exp(-1.5, kExpTab) + f_div(1.0, 2.0);
-        (void)sink;
-      }
-    } else if (warp == 10) {
-      df[lane] = static_cast<uint8_t>(lane & 1);
-      __syncwarp();
-      publish_list(df, 32, 0u, reinterpret_cast<uint32_t*>(s_pw + 52), nullptr, nullptr);
-    } else {
-      write_route(erow, 1.0, 2, ds, 0, 0, 0, reinterpret_cast<double*>(s_pw + 64), nullptr,
-                  nullptr, ds, nullptr, 0u);
-    }
-    // (The exact near-tie path is not prewarmed: a fifth prewarm warp running
-    // it cost the coreset 2-2.7 us at C2/C3 N = 32 — that warp joins the
-    // activation late — more than its rare cold misses.)
-  }
+  if (!kLin && !(a.flags & 1) && warp >= 8 && warp < 12) prewarm();
 
   // ---- R + L1: per token chunk, split-K GEMM, then the owners' logit sums ----------
   int own = 0;
