@@ -1036,8 +1036,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
             s = 0.0;
             const double* er = erow + j * ew;
             int i = 0;
-#pragma unroll 1
-            for (; i + 8 <= m; i += 8) {
+#pragma unroll 4
+            for (; i + 8 <= m; i += 8) {  // (unrolled: the next batch's loads overlap the adds)
               double v[8];
 #pragma unroll
               for (int q = 0; q < 8; ++q) v[q] = er[i + q];
@@ -1085,7 +1085,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1)
           s = 0.0;
           const double* er = erow + j * ew;
           int i = 0;
-#pragma unroll 1
+#pragma unroll 4
           for (; i + 8 <= m; i += 8) {  // ascending index (gating.cpp:31-33)
             double v[8];
 #pragma unroll

@@ -13,7 +13,8 @@ import json, sys
 d = json.load(open(f"gpurun_out/abso_{sys.argv[1]}.json"))
 bc = d.get("front_by_cta", {})
 mx = lambda k: max(bc[k].values()) if k in bc else None
-print(sys.argv[1], sys.argv[2], sys.argv[3], "coreset", mx("coreset"), "rerouted", mx("rerouted"),
+print(sys.argv[1], sys.argv[2], sys.argv[3], *[f"{k} {mx(k)}" for k in ("rowmax", "activated", "sums_done", "selected", "v_gathered", "ranked")],
+      "coreset", mx("coreset"), "rerouted", mx("rerouted"),
       "ffn_counted", d.get("ffn_counted"), "combine_end", d.get("combine_end_us"))
 PY
     done
