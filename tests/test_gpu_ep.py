@@ -175,3 +175,31 @@ def test_ep_stack_matches_single_gpu(strategy):
             assert torch.equal(st[:, :3], want_stats[:, :3])
             owned += st[:, 3].long()
         assert torch.equal(owned, want_stats[:, 0].long())
+
+
+def test_ep_peer_loss_reports_timeout_not_hang():
+    """A rank whose peer never runs the call (a lost process): its arrival
+    wait (ep_wait_kernel, 4 s bound) raises the exchange-timeout flag and the
+    call fails with the C ABI's error instead of hanging the stream; the
+    device stays usable for the next layer."""
+    import time
+    m, d, f, n, k = 64, 512, 512, 32, 8
+    cfg = LayerConfig(m, k, d, f, strategy="vote", vote_beta=0.4)
+    wr = synth.router_weights(m, d, seed=5)
+    ranks = [DesMoeLayer(cfg, wr, *synth.swiglu_weights(m, d, f, seed=9, lo=lo, hi=hi),
+                         expert_range=(lo, hi), own_context=True)
+             for lo, hi in ep.partition(m, 2)]
+    ep.connect_local([r.experts for r in ranks])
+    x = synth.hidden_states(n, d, seed=7, rho=0.3)
+    y = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    t0 = time.monotonic()
+    ranks[0].forward(x, y)  # rank 1 never issues this call
+    with pytest.raises(RuntimeError, match="timed out"):
+        ranks[0].check()
+    waited = time.monotonic() - t0
+    assert 3.5 < waited < 30, waited
+    full = DesMoeLayer(cfg, wr, *synth.swiglu_weights(m, d, f, seed=9))
+    y1 = full.forward(x)
+    full.check()
+    assert torch.isfinite(y1).all()
