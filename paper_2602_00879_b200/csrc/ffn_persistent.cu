@@ -331,28 +331,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the published expert list (coreset / union) -> the unit list; claim
     // the first unit and start streaming its weights while the route is
     // still being computed (one warp polls the list in parallel)
-    uint32_t w0 = 0;
+    // claim the first unit at once: this kernel launched behind the front's
+    // griddepcontrol.wait, so the last call's combine (which zeroes the
+    // counter) is complete; the claim's round trip overlaps the list's
     int u0 = 0;
-    if (lane == 0) {
-      do {
-        w0 = ld_relaxed_u32(a.pub);
-      } while ((w0 >> 10) != tag);
-      // claim the first unit now (the counter was zeroed before the front
-      // published): its round trip overlaps the list words' below
-      u0 = atomicAdd(sched, 1);
-      if (a.trace) s_pts[5] = gtime();  // list count seen
-    }
-    const int cnt = static_cast<int>(__shfl_sync(0xffffffffu, w0, 0) & 1023u);
+    if (lane == 0) u0 = atomicAdd(sched, 1);
+    // the count word and the first 32 list words in ONE round trip per poll
+    // (each word carries the call's tag): every lane loads both
+    uint32_t w0, w1;
+    bool ok;
+    do {
+      w0 = ld_relaxed_u32(a.pub);
+      w1 = ld_relaxed_u32(a.pub + 1 + lane);
+      const int c0 = static_cast<int>(w0 & 1023u);
+      ok = (w0 >> 10) == tag && (lane >= c0 || (w1 >> 10) == tag);
+    } while (!__all_sync(0xffffffffu, ok));
+    if (a.trace && lane == 0) s_pts[5] = gtime();  // list count seen
+    const int cnt = static_cast<int>(w0 & 1023u);
     if (lane == 0) s_pcnt = cnt;
     int u = 0;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
       const int i = i0 + lane;
       int e = -1;
       if (i < cnt) {
-        uint32_t w;
-        do {
-          w = ld_relaxed_u32(a.pub + 1 + i);
-        } while ((w >> 10) != tag);
+        uint32_t w = w1;
+        if (i0 > 0) {
+          do {
+            w = ld_relaxed_u32(a.pub + 1 + i);
+          } while ((w >> 10) != tag);
+        }
         e = static_cast<int>(w & 1023u);
       }
       const bool own = e >= lo && e < hi;
