@@ -215,6 +215,7 @@ struct desmoe_experts {
   __nv_bfloat16* h_perm = nullptr;  // [max_n*max_k x f]
   float* y_slot = nullptr;          // [max_n*max_k x d]
   int* counters = nullptr;          // FFN scheduler / readiness counters
+  uint32_t* b_done = nullptr;       // [m][d/128] + 1: phase-B unit tags (streamed host-entry combine)
   void* packed_a = nullptr;         // gate/up tiles (SwiGLU)
   void* packed_b = nullptr;         // W_d / W_lin tiles
 };
@@ -801,6 +802,10 @@ int desmoe_experts_create_ep(desmoe_ctx* c, int kind, int m, int lo, int hi, int
   if (e == cudaSuccess) e = cudaMalloc(&ex->pub, pub_words * 4);
   if (e == cudaSuccess) e = cudaMemset(ex->pub, 0xFF, pub_words * 4);
   ex->route_done = ex->pub + pub_words - 32;
+  // (all-ones: no call's tag, kernels.cuh)
+  const size_t bd_words = static_cast<size_t>(m) * std::max(1, d / kBM) + 1;
+  if (e == cudaSuccess) e = cudaMalloc(&ex->b_done, bd_words * 4);
+  if (e == cudaSuccess) e = cudaMemset(ex->b_done, 0xFF, bd_words * 4);
   if (e != cudaSuccess) {
     desmoe_experts_destroy(ex);
     return fail(DESMOE_ECUDA, std::string("expert workspace: ") + cudaGetErrorString(e));
@@ -872,6 +877,7 @@ void desmoe_experts_destroy(desmoe_experts* ex) {
   if (ex->ep_state) cudaFree(ex->ep_state);
   if (ex->route_words) cudaFree(ex->route_words);
   if (ex->pub) cudaFree(ex->pub);
+  if (ex->b_done) cudaFree(ex->b_done);
   delete ex;
 }
 
@@ -1007,6 +1013,16 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   a.pub = ex->pub;
   a.route_words = ex->route_words;
   a.route_done = ex->route_done;
+  // host-buffer entry (dense, one rank): the combine streams on per-(expert,
+  // d tile) tags, so y's bus writes overlap the FFN's last units. Measured:
+  // e2e -1.6 us; on the device-resident path the per-unit release costs the
+  // FFN ~0.8 us and the early combine more, so it stays off there
+  // (DESMOE_NO_STREAM_COMBINE=1 disables, DESMOE_STREAM_COMBINE=1 forces)
+  const bool stream_combine =
+      dense && ex->world <= 1 && !std::getenv("DESMOE_NO_STREAM_COMBINE") &&
+      (host_link || std::getenv("DESMOE_STREAM_COMBINE"));
+  a.b_done = stream_combine ? ex->b_done : nullptr;
+  a.b_drained = stream_combine ? ex->b_done + static_cast<size_t>(m) * (d / kBM) : nullptr;
   a.wa_base = ex->packed_a;
   a.wc_base = ex->packed_b;
   const size_t slot_stride = static_cast<size_t>(c->max_n) * c->max_k * d;
@@ -1108,6 +1124,9 @@ int ffn_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, int n, int 
   ca.expert_lo = ex->lo;
   ca.expert_hi = ex->hi;
   ca.stats = stats;
+  ca.b_done = a.b_done;
+  ca.b_drained = a.b_drained;
+  ca.tiles_b = d / kBM;
   ca.trace = c->trace;
   ca.trace_cap = c->trace_cap;
   if (host_link) {  // host-buffer entry: publish completion to the spinning host

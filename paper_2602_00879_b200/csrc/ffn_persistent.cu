@@ -609,6 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool pre = qi == 0 && a.early;  // claimed (and started) before the prologue
         const int u = pre ? (pre_u >= 0 ? pre_u : n_units) : atomicAdd(sched, 1);
         const int uu = u < n_units ? u : -1;
+        // the first claim past the end: every unit is out (streamed combine)
+        if (u == n_units && a.b_drained) st_relaxed_u32(a.b_drained, tag);
         mbar_wait(&qempty[q], ((qi / kQ) & 1) ^ 1);
         unit_q[q] = uu;
         mbar_arrive(&qfull[q]);
@@ -869,6 +871,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         }  // tiles of the unit
+        if (a.b_done) {
+          // (streamed combine) the barrier orders every epilogue thread's row
+          // stores before the cumulative release the combine acquires
+          named_bar_sync(1, 128);
+          if (etid == 0)
+            for (int tt = 0; tt < ui.nt; ++tt)
+              st_release_u32(&a.b_done[ui.expert * tilesB + ui.tile + tt], tag);
+        }
       } else {
         // expert parallel: push the gate-scaled rows straight into every
         // rank's slot buffer (own + NVLink peers) while later tiles stream
@@ -1120,7 +1130,42 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
       }
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // streamed (host-buffer entry): wait only for the phase-B units (expert,
+  // d tile) of this thread's experts and columns — their tags are released
+  // after the rows' stores — so the sums and y's bus writes overlap the
+  // FFN's last units. One thread per CTA first waits (slow polls) until the
+  // unit queue ran dry; then every warp polls its flags, all in flight at
+  // once (relaxed), followed by one fence. A 2 s bound falls back to the
+  // grid wait (never a hang).
+  bool ready = false;
+  if (a.b_done) {
+    if (tid == 0) {
+      const uint64_t t0 = gtime();
+      while (ld_relaxed_u32(a.b_drained) != tag && gtime() - t0 < 2000000000ull) __nanosleep(512);
+    }
+    __syncthreads();
+  }
+  if (a.b_done && mine) {
+    const uint32_t* bd = a.b_done + c / kBM;
+    const uint64_t t0 = gtime();
+    ready = true;
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j)
+        if (j < a.k && e[j] >= 0) ok &= ld_relaxed_u32(bd + e[j] * a.tiles_b) == tag;
+      if (!ok) {
+        if (gtime() - t0 > 2000000000ull) {
+          ready = false;
+          break;
+        }
+        __nanosleep(256);
+      }
+    } while (!ok);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  if (!ready) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (blockIdx.x == 0 && tid == 0) trace(a.trace, a.trace_cap, 80, -1);
   const float* y_slot = a.y_slot;
   if (a.world > 1) y_slot += (static_cast<size_t>(s_epoch) & 1u) * a.slot_stride;
@@ -1133,6 +1178,9 @@ __global__ void __launch_bounds__(256) combine_dense_kernel(CombineArgs a) {
     }
     store_row4(a, static_cast<size_t>(tok) * a.d + c, acc);
   }
+  // the FFN grid is complete before its counters are zeroed and the call
+  // sequence advances (a no-op for the threads that already waited)
+  if (ready || !mine) asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int w = i; w < a.zero_words; w += gridDim.x * blockDim.x) a.zero[w] = 0;
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) trace(a.trace, a.trace_cap, 81, -1);

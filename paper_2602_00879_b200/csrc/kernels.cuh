@@ -241,6 +241,12 @@ struct FfnArgs {
   const uint32_t* pub;
   const uint64_t* route_words;
   const uint32_t* route_done;  // [kFrontCta] the front CTAs' route-complete tags
+  // host-buffer entry, dense mode, one rank: [m][d / 128] the call's tag,
+  // stored (release) once the phase-B unit (expert, d tile) has stored its
+  // rows, and the call's tag once the unit queue ran dry; the combine
+  // streams on these (its y rows cross the bus while the last units finish)
+  uint32_t* b_done;
+  uint32_t* b_drained;
   const void* wa_base;       // packed gate/up tiles (L2 prefetch of the first unit)
   const void* wc_base;       // packed W_d / W_lin tiles
   int flags;                 // experiments: 1 = no L2 prefetch of the first unit
@@ -277,6 +283,9 @@ struct CombineArgs {
   const uint32_t* pub;       // published list (tagged words)
   int m, expert_lo, expert_hi;
   int* stats;                // optional [4]
+  const uint32_t* b_done;    // FfnArgs::b_done (nullptr: wait for the FFN grid)
+  const uint32_t* b_drained;
+  int tiles_b;               // d / 128
   __nv_bfloat16* y_bf16;     // optional: write bf16 here instead of fp32 y (layer stacks)
   const __nv_bfloat16* resid;  // optional residual stream added before the store (stacks)
   uint64_t* trace;           // optional timeline (events 80 start, 81 end; CTA 0)

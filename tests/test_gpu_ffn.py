@@ -403,3 +403,41 @@ def test_recreated_expert_bank_does_not_replay_stale_graph(ref):
         assert st[0] == u and st[2] == total, (m, d, strat, st, u, total)
         del layer, wg, wu, wd
         gc.collect()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,d,f,n,beta", [
+    (64, 2048, 1024, 32, 0.4),    # C2
+    (256, 2048, 512, 32, 0.15),   # C3 at N = 32 (dense)
+    (128, 2048, 768, 16, 0.3),    # C4 shape, N = 16
+])
+def test_streamed_combine_matches_grid_wait(monkeypatch, m, d, f, n, beta):
+    """The host-buffer entry's combine streams on per-(expert, d tile) tags
+    the FFN releases after each phase-B unit's stores, instead of waiting for
+    the FFN grid: over repeated calls with rotating inputs its y equals the
+    device entry's (grid wait) bit for bit; forced on the device entry too
+    (DESMOE_STREAM_COMBINE=1, a fresh context so the graph is re-captured)."""
+    import torch
+    from paper_2602_00879_b200.layer import DesMoeLayer, LayerConfig
+    wg, wu, wd = synth.swiglu_weights(m, d, f, seed=5)
+    wr = synth.router_weights(m, d, seed=6)
+    cfg = LayerConfig(m, 8, d, f, strategy="vote", vote_beta=beta)
+    layer = DesMoeLayer(cfg, wr, wg, wu, wd, own_context=True)
+    xs = [synth.hidden_states(n, d, seed=90 + i, rho=0.3) for i in range(4)]
+    want = []
+    for x in xs:
+        want.append(layer.forward(x).cpu())
+        torch.cuda.synchronize()
+    xh = [x.cpu().pin_memory() for x in xs]
+    yh = torch.empty((n, d), dtype=torch.float32).pin_memory()
+    for rep in range(5):
+        for i in range(len(xs)):
+            layer.forward_host(xh[i], yh)
+            assert torch.equal(yh, want[i]), (rep, i)
+    monkeypatch.setenv("DESMOE_STREAM_COMBINE", "1")
+    forced = DesMoeLayer(cfg, wr, wg, wu, wd, own_context=True)
+    for rep in range(3):
+        for i, x in enumerate(xs):
+            y = forced.forward(x)
+            forced.check()
+            assert torch.equal(y.cpu(), want[i]), (rep, i)
