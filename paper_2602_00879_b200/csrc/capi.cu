@@ -1279,10 +1279,14 @@ int front_impl(desmoe_ctx* c, const desmoe_experts* ex, const void* x, const voi
   // blocks: no exchange, no token chunking; each CTA streams all of W_r).
   // Measured crossover (tools/sweep.py): token split wins from N*M = 32768.
   int tsplit = static_cast<long>(n) * m >= 32768 ? 2 : 0;
-  // larger blocks / pools: the router GEMM runs ahead in its own clusters
-  // (router_cluster_kernel: one 8-CTA cluster per 32 tokens x 128 experts),
-  // the front reads the logits (DESMOE_FRONT_ROUTER=0/1 overrides)
-  bool router = n > kRouterTc || m > 128;
+  // the router GEMM runs ahead in its own clusters (router_cluster_kernel:
+  // one 8-CTA cluster per 32 tokens x 128 experts) and the front reads the
+  // logits, for every block. (Round 2 first used it for N > 32 or M > 128
+  // only; once the front's i-cache prewarm ran under the router kernel, the
+  // small blocks gained too — same-box A/B: C2 N = 8 / 16 / 32 DES-Vote
+  // -2.0 us, vanilla -1 to -2 us, C4 N = 32 -1.3 us, none slower.)
+  // DESMOE_FRONT_ROUTER=0 keeps the GEMM in the front (split-K / token split).
+  bool router = true;
   if (const char* rv = std::getenv("DESMOE_FRONT_ROUTER")) router = std::atoi(rv) != 0;
   if ((router || lin_only) && (d / kBK + kFrontCta - 1) / kFrontCta <= 8) tsplit = 3;
   if (const char* ts = std::getenv("DESMOE_FRONT_TSPLIT")) tsplit = std::atoi(ts);
